@@ -1,0 +1,170 @@
+/*
+ * pe3d_b200.h -- C ABI of the B200 (sm_100a) range-marching library
+ * libpe3d_b200.so.  Plain C types only: pointers, sizes, doubles; no torch
+ * or CUDA types in the signatures (streams are passed as void*).
+ *
+ * The reference package (pe3d, pure Python + numpy) has no FFI; its
+ * "operator API" is a handful of Python functions.  Each entry point below
+ * names the reference interface it replaces; the Python host
+ * (paper_1711_00005_b200/) binds them with ctypes and keeps the reference's
+ * names, argument meaning and exceptions.
+ *
+ * Layouts at the boundary are the reference's: a slab is [n_theta][n_depth]
+ * complex128, depth fastest (ref environment.py:199-222); TL stacks are
+ * [S][n_theta][n_depth] float64 (ref marching.py:185-193); tridiagonal
+ * batches are (row, member) structure-of-arrays (ref tridiag.py:82-142).
+ * Frequencies are an outer batch dimension.  The device-side field layout
+ * is private.
+ *
+ * Conventions: every function returns a pe3d_status; on failure the
+ * optional pe3d_error record is filled.  Nothing aborts or exits.  A handle
+ * owns device scratch and must be used from one host thread at a time.
+ */
+#ifndef PE3D_B200_H
+#define PE3D_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PE3D_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define PE3D_API __attribute__((visibility("default")))
+#else
+#define PE3D_API
+#endif
+
+typedef struct { double re, im; } pe3d_c128;
+
+typedef enum {
+    PE3D_OK = 0,
+    PE3D_SINGULAR = 1,      /* SingularSystemError / StepError (ref errors.py:33-60) */
+    PE3D_BAD_ARGUMENT = 2,  /* shape / invariant violation detected by the library */
+    PE3D_CUDA_ERROR = 3     /* no device, launch or copy failure */
+} pe3d_status;
+
+typedef enum { PE3D_PERIODIC = 0, PE3D_SECTOR = 1 } pe3d_topology;  /* ref environment.py:24-26 */
+typedef enum { PE3D_SWEEP_DEPTH = 0, PE3D_SWEEP_AZIMUTH = 1 } pe3d_sweep;
+
+/* Failure record.  For a failed step it carries StepError(range_index,
+ * sweep, member_index) with the SingularSystemError(pivot, member) cause
+ * (ref marching.py:122-131, tridiag.py:274-280: lowest failing member). */
+typedef struct {
+    int32_t range_index;   /* step number j+1, or -1 outside a step (solve_batch) */
+    int32_t sweep;         /* pe3d_sweep */
+    int32_t member;        /* lowest failing batch member */
+    int32_t pivot;         /* elimination row of the failing pivot */
+    int32_t rank1;         /* 1: the cyclic rank-1 correction was singular */
+    int32_t frequency;     /* index of the failing frequency inside the batch */
+    char message[208];
+} pe3d_error;
+
+/* Grid and march controls (ref Grid3D environment.py:34-90, RunOptions
+ * config.py:71-95, run_frequency marching.py:144-193). */
+typedef struct {
+    int32_t n_freq;         /* frequencies in this batch (>= 1) */
+    int32_t n_theta;        /* azimuth points (>= 3) */
+    int32_t n_depth;        /* depth points (>= 3) */
+    int32_t topology;       /* pe3d_topology */
+    int32_t n_steps;        /* range steps to take (>= 0), after max_range */
+    int32_t output_stride;  /* TL sample every stride steps; sample 0 = input slab */
+    int32_t first_index;    /* range index j of the input slab (StepError numbering) */
+    int32_t flags;          /* PE3D_FLAG_* */
+    double delta_r, delta_theta, delta_z;
+    double r_start;         /* grid r_start: the slab after step s is at r_start + (first_index+s+1)*delta_r
+                               (ref Grid3D.range_at, environment.py:89-90) */
+    double r_input;         /* range_m of the input slab (ref FieldSlab.range_m) */
+} pe3d_grid;
+
+#define PE3D_FLAG_NO_GRAPH   1   /* launch the step loop directly instead of a CUDA graph */
+#define PE3D_FLAG_SERIAL     2   /* use the thread-per-system kernels (reference op order) */
+#define PE3D_FLAG_PROFILE    4   /* no graph; CUDA events around every launch (see pe3d_profile_last) */
+
+/* Per-frequency step coefficients (ref operators.py:31-62, StepCoefficients). */
+typedef struct {
+    double k0;
+    pe3d_c128 cx_lhs, cx_rhs, cy_lhs, cy_rhs;
+} pe3d_coeffs;
+
+PE3D_API int pe3d_abi_version(void);
+PE3D_API int pe3d_device_count(int32_t* count);
+
+PE3D_API int pe3d_handle_create(int32_t device, void** handle, pe3d_error* err);
+PE3D_API int pe3d_handle_destroy(void* handle);
+
+/* Number of TL samples a march of n_steps with this stride records:
+ * 1 + floor(n_steps / stride)  (ref marching.py:167-183). */
+PE3D_API int32_t pe3d_sample_count(int32_t n_steps, int32_t output_stride);
+
+/*
+ * pe3d_march_host -- replaces run_frequency (ref marching.py:144-193) for
+ * range-independent media, for a batch of frequencies (the body of
+ * frequency_farm, ref parallel.py:126-185).  HOST buffers; the copies are
+ * part of the call.
+ *   local      [F][n_depth]            n^2 - 1 (ref operators.py:93)
+ *   u0         [F][n_theta][n_depth]   input slab at range r_start + first_index*delta_r
+ *   u_final    [F][n_theta][n_depth]   slab after n_steps (NULL: not returned)
+ *   tl         [F][S][n_theta][n_depth] transmission loss (NULL: not recorded)
+ *   snapshots  [F][S][n_theta][n_depth] field at each TL sample (NULL: off)
+ *   clamped    [F]                     exactly-zero TL samples (ref environment.py:308-315)
+ */
+PE3D_API int pe3d_march_host(void* handle, const pe3d_grid* grid, const pe3d_coeffs* coeffs,
+                    const pe3d_c128* local, const pe3d_c128* u0,
+                    pe3d_c128* u_final, double* tl, pe3d_c128* snapshots,
+                    int64_t* clamped, pe3d_error* err);
+
+/* Same with DEVICE pointers, enqueued on `stream` (a cudaStream_t, NULL =
+ * legacy default stream).  Synchronises the stream before returning so
+ * that failures can be reported. */
+PE3D_API int pe3d_march_device(void* handle, const pe3d_grid* grid, const pe3d_coeffs* coeffs,
+                      const pe3d_c128* d_local, const pe3d_c128* d_u0,
+                      pe3d_c128* d_u_final, double* d_tl, pe3d_c128* d_snapshots,
+                      int64_t* d_clamped, void* stream, pe3d_error* err);
+
+/*
+ * pe3d_step_general_host -- replaces range_step (ref marching.py:93-136)
+ * for media that vary with range and azimuth: one step with explicit
+ * per-point local terms at the old and the new range, host buffers.
+ *   local_now, local_new [F][n_theta][n_depth]; u_in, u_out [F][n_theta][n_depth]
+ * grid->n_steps must be 1; grid->first_index is j of u_in.  tl_out
+ * [F][n_theta][n_depth] and clamped [F] (NULL: skipped) receive the TL of
+ * u_out at the new range.
+ */
+PE3D_API int pe3d_step_general_host(void* handle, const pe3d_grid* grid, const pe3d_coeffs* coeffs,
+                           const pe3d_c128* local_now, const pe3d_c128* local_new,
+                           const pe3d_c128* u_in, pe3d_c128* u_out,
+                           double* tl_out, int64_t* clamped, pe3d_error* err);
+
+/*
+ * pe3d_solve_batch_host -- replaces solve_batch (ref tridiag.py:248-281):
+ * `members` systems of size n, one topology.  Diagonals and rhs are
+ * (row, member) SoA with element (k, i) at [k*row_stride + i*member_stride];
+ * a stride of 0 broadcasts (the reference's broadcast views).  Off-diagonals
+ * have n rows (cyclic, corners at sub[0] / sup[n-1]) or n-1 rows (open).
+ * Output x is [members][n].
+ */
+typedef struct {
+    const pe3d_c128* ptr;
+    int64_t row_stride;
+    int64_t member_stride;
+} pe3d_strided;
+
+PE3D_API int pe3d_solve_batch_host(void* handle, int32_t n, int32_t members, int32_t cyclic,
+                          pe3d_strided sub, pe3d_strided main_diag, pe3d_strided sup,
+                          pe3d_strided rhs, pe3d_c128* x, pe3d_error* err);
+
+/*
+ * pe3d_profile_last -- kernel timings of the last march run with
+ * PE3D_FLAG_PROFILE on this handle: ms[k] is the summed CUDA-event time and
+ * launches[k] the launch count of kernel class k (0 depth sweep, 1 azimuth
+ * sweep, 2 everything else).  No reference counterpart (measurement only).
+ */
+PE3D_API int pe3d_profile_last(void* handle, double* ms, int32_t* launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PE3D_B200_H */

@@ -1,0 +1,156 @@
+"""ctypes binding of ``libpe3d_b200.so`` (the C ABI in ``include/pe3d_b200.h``).
+
+This is the only way the package computes anything: there is no CPU
+fallback.  If the library is missing or no CUDA device is visible, every
+compute entry point raises :class:`~.errors.NativeError`.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+from pathlib import Path
+from typing import Optional
+
+import numpy as np
+
+from .errors import NativeError, raise_from_record
+
+LIB_NAME = "libpe3d_b200.so"
+LIB_PATH = Path(__file__).resolve().parent / LIB_NAME
+ABI_VERSION = 1
+
+PERIODIC, SECTOR = 0, 1
+FLAG_NO_GRAPH, FLAG_SERIAL, FLAG_PROFILE = 1, 2, 4
+
+# Every symbol include/pe3d_b200.h declares (checked by tests/test_abi.py).
+EXPORTED_SYMBOLS = (
+    "pe3d_abi_version", "pe3d_device_count", "pe3d_handle_create", "pe3d_handle_destroy",
+    "pe3d_sample_count", "pe3d_march_host", "pe3d_march_device", "pe3d_step_general_host",
+    "pe3d_solve_batch_host", "pe3d_profile_last",
+)
+
+
+class C128(C.Structure):
+    _fields_ = [("re", C.c_double), ("im", C.c_double)]
+
+
+class ErrorRecord(C.Structure):
+    _fields_ = [("range_index", C.c_int32), ("sweep", C.c_int32), ("member", C.c_int32),
+                ("pivot", C.c_int32), ("rank1", C.c_int32), ("frequency", C.c_int32),
+                ("message", C.c_char * 208)]
+
+
+class GridParams(C.Structure):
+    _fields_ = [("n_freq", C.c_int32), ("n_theta", C.c_int32), ("n_depth", C.c_int32),
+                ("topology", C.c_int32), ("n_steps", C.c_int32), ("output_stride", C.c_int32),
+                ("first_index", C.c_int32), ("flags", C.c_int32),
+                ("delta_r", C.c_double), ("delta_theta", C.c_double), ("delta_z", C.c_double),
+                ("r_start", C.c_double), ("r_input", C.c_double)]
+
+
+class Coeffs(C.Structure):
+    _fields_ = [("k0", C.c_double), ("cx_lhs", C128), ("cx_rhs", C128), ("cy_lhs", C128),
+                ("cy_rhs", C128)]
+
+
+class Strided(C.Structure):
+    _fields_ = [("ptr", C.c_void_p), ("row_stride", C.c_int64), ("member_stride", C.c_int64)]
+
+
+_P = C.c_void_p
+_SIGNATURES = {
+    "pe3d_abi_version": (C.c_int, []),
+    "pe3d_device_count": (C.c_int, [C.POINTER(C.c_int32)]),
+    "pe3d_handle_create": (C.c_int, [C.c_int32, C.POINTER(C.c_void_p), C.POINTER(ErrorRecord)]),
+    "pe3d_handle_destroy": (C.c_int, [_P]),
+    "pe3d_sample_count": (C.c_int32, [C.c_int32, C.c_int32]),
+    "pe3d_march_host": (C.c_int, [_P, C.POINTER(GridParams), C.POINTER(Coeffs), _P, _P, _P, _P, _P, _P,
+                                  C.POINTER(ErrorRecord)]),
+    "pe3d_march_device": (C.c_int, [_P, C.POINTER(GridParams), C.POINTER(Coeffs), _P, _P, _P, _P, _P, _P,
+                                    _P, C.POINTER(ErrorRecord)]),
+    "pe3d_step_general_host": (C.c_int, [_P, C.POINTER(GridParams), C.POINTER(Coeffs), _P, _P, _P, _P,
+                                         _P, _P, C.POINTER(ErrorRecord)]),
+    "pe3d_solve_batch_host": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, Strided, Strided, Strided,
+                                        Strided, _P, C.POINTER(ErrorRecord)]),
+    "pe3d_profile_last": (C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_int32)]),
+}
+
+_lib: Optional[C.CDLL] = None
+_lock = threading.Lock()
+_handles: dict = {}
+
+
+def load_library(path: Optional[Path] = None) -> C.CDLL:
+    """Load (once) and type the shared library; raises NativeError if absent."""
+    global _lib
+    with _lock:
+        if _lib is not None and path is None:
+            return _lib
+        p = Path(path or os.environ.get("PE3D_B200_LIB", LIB_PATH))
+        if not p.exists():
+            raise NativeError(f"{p} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+                              "(or `make -C paper_1711_00005_b200/csrc`); there is no CPU fallback")
+        try:
+            lib = C.CDLL(str(p))
+        except OSError as exc:
+            raise NativeError(f"cannot load {p}: {exc}") from exc
+        for name, (res, args) in _SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        if lib.pe3d_abi_version() != ABI_VERSION:
+            raise NativeError(f"{p}: ABI version {lib.pe3d_abi_version()} != {ABI_VERSION}")
+        if path is None:
+            _lib = lib
+        return lib
+
+
+def device_count() -> int:
+    n = C.c_int32(0)
+    load_library().pe3d_device_count(C.byref(n))
+    return int(n.value)
+
+
+def handle(device: int = 0) -> C.c_void_p:
+    """Per-(thread, device) library handle (a handle owns device scratch)."""
+    key = (threading.get_ident(), device)
+    h = _handles.get(key)
+    if h is None:
+        lib = load_library()
+        if device_count() <= device:
+            raise NativeError(f"no CUDA device {device} visible; the B200 path has no CPU fallback")
+        h = C.c_void_p()
+        err = ErrorRecord()
+        raise_from_record(lib.pe3d_handle_create(device, C.byref(h), C.byref(err)), err)
+        _handles[key] = h
+    return h
+
+
+def ptr(a: Optional[np.ndarray]):
+    if a is None:
+        return None
+    if not a.flags.c_contiguous:
+        raise ValueError("native buffers must be C-contiguous")
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def c128(z) -> C128:
+    z = complex(z)
+    return C128(z.real, z.imag)
+
+
+def make_coeffs(k0s, coeffs_list) -> "C.Array":
+    arr = (Coeffs * len(k0s))()
+    for i, (k0, co) in enumerate(zip(k0s, coeffs_list)):
+        arr[i] = Coeffs(float(k0), c128(co.cx_lhs), c128(co.cx_rhs), c128(co.cy_lhs), c128(co.cy_rhs))
+    return arr
+
+
+def call(fn_name: str, *args) -> None:
+    """Call an ABI entry point and raise the mapped exception on failure."""
+    lib = load_library()
+    err = ErrorRecord()
+    status = getattr(lib, fn_name)(*args, C.byref(err))
+    raise_from_record(status, err)

@@ -1,0 +1,614 @@
+// pe3d_abi.cu -- the C ABI of libpe3d_b200.so (include/pe3d_b200.h): handle
+// and workspace management, the device-resident march (one CUDA graph per
+// call), the general single step and the batched tridiagonal solve.
+//
+// Reference entry points replaced (pkg/src/pe3d): run_frequency
+// (marching.py:144-193) and the frequency batch of frequency_farm
+// (parallel.py:143-185) -> pe3d_march_*; range_step (marching.py:93-136)
+// -> pe3d_step_general_host; solve_batch (tridiag.py:248-281) ->
+// pe3d_solve_batch_host.
+
+#include <complex>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "../../include/pe3d_b200.h"
+#include "pe3d_internal.h"
+
+using pe3d::cplx;
+
+namespace {
+
+struct DevBuf {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+    cudaError_t ensure(size_t want) {
+        if (want <= bytes) return cudaSuccess;
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        bytes = 0;
+        cudaError_t e = cudaMalloc(&ptr, want);
+        if (e == cudaSuccess) bytes = want;
+        return e;
+    }
+    void release() {
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        bytes = 0;
+    }
+    template <class T> T* as() const { return static_cast<T*>(ptr); }
+};
+
+struct Handle {
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t stream = nullptr;
+    // march workspace
+    DevBuf field_a, field_b, field_c;     // device tiles [F][n_tiles][n_theta][8]
+    DevBuf loc_tab, mul_tab, fdev, w_abs, err;
+    DevBuf az_cp, az_inv, az_q, az_ring, fail_row, fail_mag;
+    // staging for the host entry points
+    DevBuf h_local, h_local2, h_u0, h_final, h_tl, h_snap, h_clamped;
+    // solve_batch
+    DevBuf sb_in, sb_x, sb_cp, sb_inv, sb_y, sb_q;
+    // one cached step-loop graph (reused when a march repeats with identical arguments)
+    std::vector<unsigned char> graph_key;
+    cudaGraphExec_t graph_exec = nullptr;
+    // PE3D_FLAG_PROFILE accounting
+    double prof_ms[3] = {0, 0, 0};
+    int32_t prof_n[3] = {0, 0, 0};
+};
+
+// Launch wrapper: in profile mode, bracket each launch with events.
+struct Prof {
+    Handle* h;
+    bool on;
+    cudaStream_t s;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
+    template <class F> cudaError_t run(int cls, F&& f) {
+        if (!on) return f();
+        cudaEvent_t a, b;
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+        cudaEventRecord(a, s);
+        cudaError_t e = f();
+        cudaEventRecord(b, s);
+        ev.push_back({cls, {a, b}});
+        return e;
+    }
+    void collect() {
+        if (!on) return;
+        for (int k = 0; k < 3; ++k) { h->prof_ms[k] = 0; h->prof_n[k] = 0; }
+        for (auto& p : ev) {
+            float ms = 0;
+            cudaEventSynchronize(p.second.second);
+            cudaEventElapsedTime(&ms, p.second.first, p.second.second);
+            h->prof_ms[p.first] += ms;
+            h->prof_n[p.first] += 1;
+            cudaEventDestroy(p.second.first);
+            cudaEventDestroy(p.second.second);
+        }
+        ev.clear();
+    }
+};
+
+constexpr unsigned long long NO_ERROR = ~0ull;
+
+void set_error(pe3d_error* err, int32_t range_index, int32_t sweep, const char* fmt, const char* what) {
+    if (!err) return;
+    std::memset(err, 0, sizeof(*err));
+    err->range_index = range_index;
+    err->sweep = sweep;
+    std::snprintf(err->message, sizeof(err->message), fmt, what);
+}
+
+int cuda_fail(pe3d_error* err, cudaError_t e, const char* where) {
+    if (err) {
+        std::memset(err, 0, sizeof(*err));
+        err->range_index = -1;
+        std::snprintf(err->message, sizeof(err->message), "%s: %s", where, cudaGetErrorString(e));
+    }
+    return PE3D_CUDA_ERROR;
+}
+
+int bad_arg(pe3d_error* err, const char* what) {
+    set_error(err, -1, 0, "%s", what);
+    return PE3D_BAD_ARGUMENT;
+}
+
+#define CK(call, where)                                   \
+    do {                                                  \
+        cudaError_t e_ = (call);                          \
+        if (e_ != cudaSuccess) return cuda_fail(err, e_, where); \
+    } while (0)
+
+int check_grid(const pe3d_grid* g, const pe3d_coeffs* c, pe3d_error* err) {
+    if (!g || !c) return bad_arg(err, "null grid or coefficients");
+    if (g->n_freq < 1) return bad_arg(err, "n_freq >= 1");
+    if (g->n_theta < 3 || g->n_depth < 3) return bad_arg(err, "n_theta >= 3 and n_depth >= 3");
+    if (g->n_theta > 4096) return bad_arg(err, "n_theta <= 4096 (ring kernels)");
+    if (g->n_depth > 4096) return bad_arg(err, "n_depth <= 4096 (depth kernels)");
+    if (g->n_steps < 0) return bad_arg(err, "n_steps >= 0");
+    if (g->output_stride < 1) return bad_arg(err, "output_stride >= 1");
+    if (g->topology != PE3D_PERIODIC && g->topology != PE3D_SECTOR) return bad_arg(err, "topology");
+    if (!(g->delta_r > 0) || !(g->delta_theta > 0) || !(g->delta_z > 0)) return bad_arg(err, "spacings > 0");
+    if (!(g->r_input > 0)) return bad_arg(err, "r_input > 0");
+    for (int f = 0; f < g->n_freq; ++f)
+        if (!(c[f].k0 > 0)) return bad_arg(err, "k0 > 0");
+    return PE3D_OK;
+}
+
+std::vector<pe3d::FreqDev> freq_table(const pe3d_grid* g, const pe3d_coeffs* c) {
+    std::vector<pe3d::FreqDev> t(g->n_freq);
+    for (int f = 0; f < g->n_freq; ++f) {
+        pe3d::FreqDev& d = t[f];
+        d.k0 = c[f].k0;
+        const double kz = c[f].k0 * g->delta_z;
+        d.s_z = 1.0 / (kz * kz);                                    // ref operators.py:94
+        d.cx_lhs = pe3d::mk(c[f].cx_lhs.re, c[f].cx_lhs.im);
+        d.cx_rhs = pe3d::mk(c[f].cx_rhs.re, c[f].cx_rhs.im);
+        d.cy_lhs = pe3d::mk(c[f].cy_lhs.re, c[f].cy_lhs.im);
+        d.cy_rhs = pe3d::mk(c[f].cy_rhs.re, c[f].cy_rhs.im);
+        d.off_z = pe3d::mk(d.cx_lhs.re * d.s_z, d.cx_lhs.im * d.s_z);  // complex(coeff * s)
+    }
+    return t;
+}
+
+// |w(r)| exactly as the reference computes it (environment.py:287-294):
+// abs(complex(cos(k0 r), sin(k0 r)) / sqrt(r))
+double hankel_abs_host(double k0, double r) {
+    const double s = std::sqrt(r);
+    return std::hypot(std::cos(k0 * r) / s, std::sin(k0 * r) / s);
+}
+
+bool needs_serial(const pe3d_grid* g, const std::vector<pe3d::FreqDev>& fd) {
+    if (g->flags & PE3D_FLAG_SERIAL) return true;
+    for (const auto& d : fd)
+        if (d.off_z.re == 0.0 && d.off_z.im == 0.0) return true;
+    return false;
+}
+
+int decode_error(Handle* h, cudaStream_t stream, pe3d_error* err) {
+    pe3d::DevError de;
+    CK(cudaMemcpyAsync(&de, h->err.ptr, sizeof(de), cudaMemcpyDeviceToHost, stream), "error readback");
+    CK(cudaStreamSynchronize(stream), "march");
+    if (de.key == NO_ERROR) return PE3D_OK;
+    if (err) {
+        std::memset(err, 0, sizeof(*err));
+        err->range_index = int32_t(de.key >> 40);
+        err->sweep = int32_t((de.key >> 39) & 1);
+        err->frequency = int32_t((de.key >> 24) & 0x7fff);
+        err->member = int32_t(de.key & 0xffffff);
+        err->pivot = de.pivot;
+        err->rank1 = de.rank1;
+        std::snprintf(err->message, sizeof(err->message), "singular system: pivot %d, batch member %d", de.pivot,
+                      err->member);
+    }
+    return PE3D_SINGULAR;
+}
+
+struct MarchPlan {
+    pe3d::LaunchCtx ctx;
+    bool serial;
+    int64_t field_elems;
+    int n_samples;
+};
+
+// Enqueue the step loop (the body graphed by pe3d_march_device).
+cudaError_t enqueue_steps(Handle* h, const pe3d_grid* g, const MarchPlan& p, const cplx* d_local,
+                          double* d_tl, cplx* d_snap, cplx* d_final, int64_t* d_clamped,
+                          const double* d_wabs, Prof& prof) {
+    const pe3d::LaunchCtx& c = p.ctx;
+    cplx* A = h->field_a.as<cplx>();
+    cplx* B = h->field_b.as<cplx>();
+    cplx* C = h->field_c.as<cplx>();
+    const int cols = pe3d::depth_cols_per_block(c);
+    const bool periodic = g->topology == PE3D_PERIODIC;
+    for (int s = 0; s < g->n_steps; ++s) {
+        const int j_new = g->first_index + s + 1;
+        const double r_new = g->r_start + j_new * g->delta_r;          // Grid3D.range_at
+        cudaError_t e;
+        if (p.serial) {
+            e = prof.run(0, [&] { return pe3d::launch_depth_serial(c, A, B, C, d_local, d_local, g->n_depth, 0,
+                                                                   h->fail_row.as<int>(), h->fail_mag.as<double>()); });
+            if (e == cudaSuccess)
+                e = prof.run(2, [&] { return pe3d::launch_reduce_failures(h->fail_row.as<int>(), h->fail_mag.as<double>(),
+                                                                          c.n_freq, c.n_theta, j_new, 0, -1, c.err,
+                                                                          c.stream); });
+        } else {
+            e = prof.run(0, [&] { return pe3d::launch_depth_scan(c, A, B, cols); });
+        }
+        if (e != cudaSuccess) return e;
+        pe3d::EpilogueArgs ea{};
+        const bool record = ((s + 1) % g->output_stride) == 0;
+        ea.tl = record ? d_tl : nullptr;
+        ea.snap = record ? d_snap : nullptr;
+        ea.final_out = (s == g->n_steps - 1) ? d_final : nullptr;
+        ea.clamped = d_clamped;
+        ea.n_samples = p.n_samples;
+        ea.sample = (s + 1) / g->output_stride;
+        ea.w_abs = d_wabs + int64_t(ea.sample) * g->n_freq;
+        ea.periodic = periodic;
+        ea.write_temp = (s < g->n_steps - 1);
+        if (periodic && !p.serial) {
+            e = prof.run(1, [&] { return pe3d::launch_azimuth_scan(c, B, A, r_new, ea, j_new); });
+        } else {
+            e = prof.run(1, [&] { return pe3d::launch_azimuth_serial(c, B, C, h->az_cp.as<cplx>(), h->az_inv.as<cplx>(),
+                                                                     h->az_q.as<cplx>(), h->az_ring.as<cplx>(), r_new,
+                                                                     j_new); });
+            if (e == cudaSuccess) e = prof.run(2, [&] { return pe3d::launch_finish(c, C, 1, A, r_new, ea); });
+        }
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pe3d_abi_version(void) { return PE3D_ABI_VERSION; }
+
+int pe3d_device_count(int32_t* count) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (count) *count = (e == cudaSuccess) ? n : 0;
+    return e == cudaSuccess ? PE3D_OK : PE3D_CUDA_ERROR;
+}
+
+int32_t pe3d_sample_count(int32_t n_steps, int32_t output_stride) {
+    if (n_steps < 0 || output_stride < 1) return -1;
+    return 1 + n_steps / output_stride;
+}
+
+int pe3d_handle_create(int32_t device, void** handle, pe3d_error* err) {
+    if (!handle) return bad_arg(err, "null handle pointer");
+    *handle = nullptr;
+    int n = 0;
+    CK(cudaGetDeviceCount(&n), "cudaGetDeviceCount");
+    if (device < 0 || device >= n) return bad_arg(err, "device index out of range");
+    CK(cudaSetDevice(device), "cudaSetDevice");
+    Handle* h = new (std::nothrow) Handle();
+    if (!h) return bad_arg(err, "out of host memory");
+    h->device = device;
+    CK(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device), "attribute");
+    CK(cudaStreamCreate(&h->stream), "cudaStreamCreate");
+    *handle = h;
+    return PE3D_OK;
+}
+
+int pe3d_handle_destroy(void* handle) {
+    Handle* h = static_cast<Handle*>(handle);
+    if (!h) return PE3D_OK;
+    cudaSetDevice(h->device);
+    for (DevBuf* b : {&h->field_a, &h->field_b, &h->field_c, &h->loc_tab, &h->mul_tab, &h->fdev, &h->w_abs, &h->err,
+                      &h->az_cp, &h->az_inv, &h->az_q, &h->az_ring, &h->fail_row, &h->fail_mag, &h->h_local,
+                      &h->h_local2, &h->h_u0, &h->h_final, &h->h_tl, &h->h_snap, &h->h_clamped, &h->sb_in, &h->sb_x,
+                      &h->sb_cp, &h->sb_inv, &h->sb_y, &h->sb_q})
+        b->release();
+    if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
+    if (h->stream) cudaStreamDestroy(h->stream);
+    delete h;
+    return PE3D_OK;
+}
+
+int pe3d_march_device(void* handle, const pe3d_grid* g, const pe3d_coeffs* coeffs, const pe3d_c128* d_local,
+                      const pe3d_c128* d_u0, pe3d_c128* d_u_final, double* d_tl, pe3d_c128* d_snapshots,
+                      int64_t* d_clamped, void* stream_v, pe3d_error* err) {
+    Handle* h = static_cast<Handle*>(handle);
+    if (!h) return bad_arg(err, "null handle");
+    int st = check_grid(g, coeffs, err);
+    if (st != PE3D_OK) return st;
+    if (!d_local || !d_u0) return bad_arg(err, "null local or u0");
+    CK(cudaSetDevice(h->device), "cudaSetDevice");
+    cudaStream_t stream = stream_v ? static_cast<cudaStream_t>(stream_v) : h->stream;
+
+    const int F = g->n_freq, NT = g->n_theta, NZ = g->n_depth;
+    const int n_tiles = (NZ + 7) / 8;
+    const int64_t field = int64_t(F) * n_tiles * NT * 8;
+    const int S = pe3d_sample_count(g->n_steps, g->output_stride);
+    std::vector<pe3d::FreqDev> fd = freq_table(g, coeffs);
+    MarchPlan p{};
+    p.serial = needs_serial(g, fd);
+    p.field_elems = field;
+    p.n_samples = S;
+
+    CK(h->field_a.ensure(field * sizeof(cplx)), "alloc field");
+    CK(h->field_b.ensure(field * sizeof(cplx)), "alloc field");
+    CK(h->loc_tab.ensure(int64_t(F) * n_tiles * 8 * sizeof(cplx)), "alloc tables");
+    CK(h->mul_tab.ensure(int64_t(F) * n_tiles * 8 * sizeof(cplx)), "alloc tables");
+    CK(h->fdev.ensure(F * sizeof(pe3d::FreqDev)), "alloc coeffs");
+    CK(h->w_abs.ensure(int64_t(S) * F * sizeof(double)), "alloc w");
+    CK(h->err.ensure(sizeof(pe3d::DevError)), "alloc err");
+    const bool need_c = p.serial || g->topology != PE3D_PERIODIC;
+    if (need_c) {
+        CK(h->field_c.ensure(field * sizeof(cplx)), "alloc field");
+        CK(h->az_cp.ensure(int64_t(F) * NT * sizeof(cplx)), "alloc az");
+        CK(h->az_inv.ensure(int64_t(F) * NT * sizeof(cplx)), "alloc az");
+        CK(h->az_q.ensure(int64_t(F) * NT * sizeof(cplx)), "alloc az");
+        CK(h->az_ring.ensure(int64_t(F) * 2 * sizeof(cplx)), "alloc az");
+        CK(h->fail_row.ensure(int64_t(F) * (NT > NZ ? NT : NZ) * sizeof(int)), "alloc fail");
+        CK(h->fail_mag.ensure(int64_t(F) * (NT > NZ ? NT : NZ) * sizeof(double)), "alloc fail");
+    }
+
+    // per-sample |w(r)| table [S][F]
+    std::vector<double> wabs(int64_t(S) * F);
+    for (int s = 0; s < S; ++s) {
+        const double r = (s == 0) ? g->r_input : g->r_start + (g->first_index + int64_t(s) * g->output_stride) * g->delta_r;
+        for (int f = 0; f < F; ++f) wabs[int64_t(s) * F + f] = hankel_abs_host(coeffs[f].k0, r);
+    }
+    pe3d::DevError de0{NO_ERROR, 0, 0};
+    CK(cudaMemcpyAsync(h->fdev.ptr, fd.data(), F * sizeof(pe3d::FreqDev), cudaMemcpyHostToDevice, stream), "H2D");
+    CK(cudaMemcpyAsync(h->w_abs.ptr, wabs.data(), wabs.size() * sizeof(double), cudaMemcpyHostToDevice, stream), "H2D");
+    CK(cudaMemcpyAsync(h->err.ptr, &de0, sizeof(de0), cudaMemcpyHostToDevice, stream), "H2D");
+    if (d_clamped) CK(cudaMemsetAsync(d_clamped, 0, F * sizeof(int64_t), stream), "memset");
+
+    pe3d::LaunchCtx& c = p.ctx;
+    c.n_freq = F; c.n_theta = NT; c.n_depth = NZ; c.n_tiles = n_tiles;
+    c.sector = g->topology == PE3D_SECTOR;
+    c.num_sms = h->num_sms;
+    c.delta_theta = g->delta_theta;
+    c.fdev = h->fdev.as<pe3d::FreqDev>();
+    c.loc_tab = h->loc_tab.as<cplx>();
+    c.mul_tab = h->mul_tab.as<cplx>();
+    c.err = h->err.as<pe3d::DevError>();
+    c.stream = stream;
+
+    const cplx* local = reinterpret_cast<const cplx*>(d_local);
+    Prof prof{h, (g->flags & PE3D_FLAG_PROFILE) != 0, stream, {}};
+    if (!p.serial) CK(prof.run(2, [&] { return pe3d::launch_factor_depth(c, local, NZ, g->first_index + 1); }), "factor");
+
+    // starter: boundary, TL sample 0, first temp (ref marching.py:159-172)
+    pe3d::EpilogueArgs ea0{};
+    ea0.tl = d_tl;
+    ea0.snap = reinterpret_cast<cplx*>(d_snapshots);
+    ea0.final_out = g->n_steps == 0 ? reinterpret_cast<cplx*>(d_u_final) : nullptr;
+    ea0.clamped = d_clamped;
+    ea0.w_abs = h->w_abs.as<double>();
+    ea0.n_samples = S;
+    ea0.sample = 0;
+    ea0.periodic = g->topology == PE3D_PERIODIC;
+    ea0.write_temp = g->n_steps > 0;
+    CK(prof.run(2, [&] { return pe3d::launch_finish(c, reinterpret_cast<const cplx*>(d_u0), 0, h->field_a.as<cplx>(),
+                                                     g->r_input, ea0); }),
+       "prepare");
+
+    const bool use_graph = !(g->flags & (PE3D_FLAG_NO_GRAPH | PE3D_FLAG_PROFILE)) && g->n_steps >= 2;
+    if (use_graph) {
+        // The step loop bakes pointers and scalars into kernel nodes: reuse the
+        // instantiated graph only when every one of them is unchanged.
+        std::vector<unsigned char> key;
+        auto add = [&](const void* q, size_t n) {
+            const unsigned char* b = static_cast<const unsigned char*>(q);
+            key.insert(key.end(), b, b + n);
+        };
+        const void* ptrs[8] = {d_local, d_tl, d_snapshots, d_u_final, d_clamped, h->field_a.ptr, h->field_b.ptr,
+                               h->field_c.ptr};
+        add(g, sizeof(*g));
+        add(coeffs, sizeof(pe3d_coeffs) * F);
+        add(ptrs, sizeof(ptrs));
+        add(&stream, sizeof(stream));
+        const void* tabs[4] = {h->w_abs.ptr, h->fdev.ptr, h->loc_tab.ptr, h->err.ptr};
+        add(tabs, sizeof(tabs));
+        if (!(h->graph_exec && key == h->graph_key)) {
+            if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
+            h->graph_exec = nullptr;
+            h->graph_key.clear();
+            cudaGraph_t graph = nullptr;
+            CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal), "capture");
+            cudaError_t e = enqueue_steps(h, g, p, local, d_tl, reinterpret_cast<cplx*>(d_snapshots),
+                                          reinterpret_cast<cplx*>(d_u_final), d_clamped, h->w_abs.as<double>(), prof);
+            cudaError_t e2 = cudaStreamEndCapture(stream, &graph);
+            if (e != cudaSuccess) { if (graph) cudaGraphDestroy(graph); return cuda_fail(err, e, "enqueue"); }
+            if (e2 != cudaSuccess) return cuda_fail(err, e2, "end capture");
+            e = cudaGraphInstantiate(&h->graph_exec, graph, 0);
+            cudaGraphDestroy(graph);
+            if (e != cudaSuccess) { h->graph_exec = nullptr; return cuda_fail(err, e, "instantiate"); }
+            h->graph_key = key;
+        }
+        CK(cudaGraphLaunch(h->graph_exec, stream), "graph launch");
+    } else {
+        CK(enqueue_steps(h, g, p, local, d_tl, reinterpret_cast<cplx*>(d_snapshots),
+                         reinterpret_cast<cplx*>(d_u_final), d_clamped, h->w_abs.as<double>(), prof),
+           "enqueue");
+    }
+    CK(cudaGetLastError(), "launch");
+    prof.collect();
+    return decode_error(h, stream, err);
+}
+
+int pe3d_march_host(void* handle, const pe3d_grid* g, const pe3d_coeffs* coeffs, const pe3d_c128* local,
+                    const pe3d_c128* u0, pe3d_c128* u_final, double* tl, pe3d_c128* snapshots, int64_t* clamped,
+                    pe3d_error* err) {
+    Handle* h = static_cast<Handle*>(handle);
+    if (!h) return bad_arg(err, "null handle");
+    int st = check_grid(g, coeffs, err);
+    if (st != PE3D_OK) return st;
+    if (!local || !u0) return bad_arg(err, "null local or u0");
+    CK(cudaSetDevice(h->device), "cudaSetDevice");
+    const int64_t F = g->n_freq, slab = int64_t(g->n_theta) * g->n_depth;
+    const int64_t S = pe3d_sample_count(g->n_steps, g->output_stride);
+    cudaStream_t s = h->stream;
+    CK(h->h_local.ensure(F * g->n_depth * sizeof(cplx)), "alloc");
+    CK(h->h_u0.ensure(F * slab * sizeof(cplx)), "alloc");
+    CK(h->h_clamped.ensure(F * sizeof(int64_t)), "alloc");
+    if (u_final) CK(h->h_final.ensure(F * slab * sizeof(cplx)), "alloc");
+    if (tl) CK(h->h_tl.ensure(F * S * slab * sizeof(double)), "alloc");
+    if (snapshots) CK(h->h_snap.ensure(F * S * slab * sizeof(cplx)), "alloc");
+    CK(cudaMemcpyAsync(h->h_local.ptr, local, F * g->n_depth * sizeof(cplx), cudaMemcpyHostToDevice, s), "H2D");
+    CK(cudaMemcpyAsync(h->h_u0.ptr, u0, F * slab * sizeof(cplx), cudaMemcpyHostToDevice, s), "H2D");
+    st = pe3d_march_device(handle, g, coeffs, h->h_local.as<pe3d_c128>(), h->h_u0.as<pe3d_c128>(),
+                           u_final ? h->h_final.as<pe3d_c128>() : nullptr, tl ? h->h_tl.as<double>() : nullptr,
+                           snapshots ? h->h_snap.as<pe3d_c128>() : nullptr, h->h_clamped.as<int64_t>(), s, err);
+    if (st != PE3D_OK) return st;
+    if (u_final) CK(cudaMemcpyAsync(u_final, h->h_final.ptr, F * slab * sizeof(cplx), cudaMemcpyDeviceToHost, s), "D2H");
+    if (tl) CK(cudaMemcpyAsync(tl, h->h_tl.ptr, F * S * slab * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
+    if (snapshots)
+        CK(cudaMemcpyAsync(snapshots, h->h_snap.ptr, F * S * slab * sizeof(cplx), cudaMemcpyDeviceToHost, s), "D2H");
+    if (clamped) CK(cudaMemcpyAsync(clamped, h->h_clamped.ptr, F * sizeof(int64_t), cudaMemcpyDeviceToHost, s), "D2H");
+    CK(cudaStreamSynchronize(s), "sync");
+    return PE3D_OK;
+}
+
+int pe3d_step_general_host(void* handle, const pe3d_grid* g, const pe3d_coeffs* coeffs, const pe3d_c128* local_now,
+                           const pe3d_c128* local_new, const pe3d_c128* u_in, pe3d_c128* u_out, double* tl_out,
+                           int64_t* clamped, pe3d_error* err) {
+    Handle* h = static_cast<Handle*>(handle);
+    if (!h) return bad_arg(err, "null handle");
+    int st = check_grid(g, coeffs, err);
+    if (st != PE3D_OK) return st;
+    if (g->n_steps != 1) return bad_arg(err, "n_steps == 1 for a single step");
+    if (!local_now || !local_new || !u_in || !u_out) return bad_arg(err, "null buffer");
+    CK(cudaSetDevice(h->device), "cudaSetDevice");
+    cudaStream_t s = h->stream;
+    const int F = g->n_freq, NT = g->n_theta, NZ = g->n_depth, n_tiles = (NZ + 7) / 8;
+    const int64_t slab = int64_t(NT) * NZ, field = int64_t(F) * n_tiles * NT * 8;
+    std::vector<pe3d::FreqDev> fd = freq_table(g, coeffs);
+    CK(h->field_a.ensure(field * sizeof(cplx)), "alloc");
+    CK(h->field_b.ensure(field * sizeof(cplx)), "alloc");
+    CK(h->field_c.ensure(field * sizeof(cplx)), "alloc");
+    CK(h->fdev.ensure(F * sizeof(pe3d::FreqDev)), "alloc");
+    CK(h->err.ensure(sizeof(pe3d::DevError)), "alloc");
+    CK(h->w_abs.ensure(F * sizeof(double)), "alloc");
+    CK(h->az_cp.ensure(int64_t(F) * NT * sizeof(cplx)), "alloc");
+    CK(h->az_inv.ensure(int64_t(F) * NT * sizeof(cplx)), "alloc");
+    CK(h->az_q.ensure(int64_t(F) * NT * sizeof(cplx)), "alloc");
+    CK(h->az_ring.ensure(int64_t(F) * 2 * sizeof(cplx)), "alloc");
+    CK(h->fail_row.ensure(int64_t(F) * (NT > NZ ? NT : NZ) * sizeof(int)), "alloc");
+    CK(h->fail_mag.ensure(int64_t(F) * (NT > NZ ? NT : NZ) * sizeof(double)), "alloc");
+    CK(h->h_local.ensure(F * slab * sizeof(cplx)), "alloc");
+    CK(h->h_local2.ensure(F * slab * sizeof(cplx)), "alloc");
+    CK(h->h_u0.ensure(F * slab * sizeof(cplx)), "alloc");
+    CK(h->h_final.ensure(F * slab * sizeof(cplx)), "alloc");
+    CK(h->h_tl.ensure(F * slab * sizeof(double)), "alloc");
+    CK(h->h_clamped.ensure(F * sizeof(int64_t)), "alloc");
+    pe3d::DevError de0{NO_ERROR, 0, 0};
+    const int j_new = g->first_index + 1;
+    const double r_new = g->r_start + j_new * g->delta_r;
+    std::vector<double> wabs(F);
+    for (int f = 0; f < F; ++f) wabs[f] = hankel_abs_host(coeffs[f].k0, r_new);
+    CK(cudaMemcpyAsync(h->w_abs.ptr, wabs.data(), F * sizeof(double), cudaMemcpyHostToDevice, s), "H2D");
+    CK(cudaMemsetAsync(h->h_clamped.ptr, 0, F * sizeof(int64_t), s), "memset");
+    CK(cudaMemcpyAsync(h->fdev.ptr, fd.data(), F * sizeof(pe3d::FreqDev), cudaMemcpyHostToDevice, s), "H2D");
+    CK(cudaMemcpyAsync(h->err.ptr, &de0, sizeof(de0), cudaMemcpyHostToDevice, s), "H2D");
+    CK(cudaMemcpyAsync(h->h_local.ptr, local_now, F * slab * sizeof(cplx), cudaMemcpyHostToDevice, s), "H2D");
+    CK(cudaMemcpyAsync(h->h_local2.ptr, local_new, F * slab * sizeof(cplx), cudaMemcpyHostToDevice, s), "H2D");
+    CK(cudaMemcpyAsync(h->h_u0.ptr, u_in, F * slab * sizeof(cplx), cudaMemcpyHostToDevice, s), "H2D");
+
+    pe3d::LaunchCtx c{};
+    c.n_freq = F; c.n_theta = NT; c.n_depth = NZ; c.n_tiles = n_tiles;
+    c.sector = g->topology == PE3D_SECTOR;
+    c.num_sms = h->num_sms;
+    c.delta_theta = g->delta_theta;
+    c.fdev = h->fdev.as<pe3d::FreqDev>();
+    c.err = h->err.as<pe3d::DevError>();
+    c.stream = s;
+    pe3d::EpilogueArgs ea{};
+    ea.periodic = g->topology == PE3D_PERIODIC;
+    ea.write_temp = 1;
+    ea.w_abs = h->w_abs.as<double>();
+    CK(pe3d::launch_finish(c, h->h_u0.as<cplx>(), 0, h->field_a.as<cplx>(), g->r_input, ea), "prepare");
+    CK(pe3d::launch_depth_serial(c, h->field_a.as<cplx>(), h->field_b.as<cplx>(), h->field_c.as<cplx>(),
+                                 h->h_local.as<cplx>(), h->h_local2.as<cplx>(), slab, NZ, h->fail_row.as<int>(),
+                                 h->fail_mag.as<double>()),
+       "depth");
+    CK(pe3d::launch_reduce_failures(h->fail_row.as<int>(), h->fail_mag.as<double>(), F, NT, j_new, 0, -1, c.err, s),
+       "reduce");
+    pe3d::EpilogueArgs ef{};
+    ef.periodic = ea.periodic;
+    ef.final_out = h->h_final.as<cplx>();
+    ef.w_abs = h->w_abs.as<double>();
+    ef.tl = tl_out ? h->h_tl.as<double>() : nullptr;
+    ef.clamped = h->h_clamped.as<int64_t>();
+    ef.n_samples = 1;
+    ef.write_temp = 0;
+    CK(pe3d::launch_azimuth_serial(c, h->field_b.as<cplx>(), h->field_c.as<cplx>(), h->az_cp.as<cplx>(),
+                                   h->az_inv.as<cplx>(), h->az_q.as<cplx>(), h->az_ring.as<cplx>(), r_new, j_new),
+       "azimuth");
+    CK(pe3d::launch_finish(c, h->field_c.as<cplx>(), 1, h->field_a.as<cplx>(), r_new, ef), "finish");
+    st = decode_error(h, s, err);
+    if (st != PE3D_OK) return st;
+    CK(cudaMemcpyAsync(u_out, h->h_final.ptr, F * slab * sizeof(cplx), cudaMemcpyDeviceToHost, s), "D2H");
+    if (tl_out) CK(cudaMemcpyAsync(tl_out, h->h_tl.ptr, F * slab * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
+    if (clamped) CK(cudaMemcpyAsync(clamped, h->h_clamped.ptr, F * sizeof(int64_t), cudaMemcpyDeviceToHost, s), "D2H");
+    CK(cudaStreamSynchronize(s), "sync");
+    return PE3D_OK;
+}
+
+int pe3d_solve_batch_host(void* handle, int32_t n, int32_t members, int32_t cyclic, pe3d_strided sub,
+                          pe3d_strided main_diag, pe3d_strided sup, pe3d_strided rhs, pe3d_c128* x, pe3d_error* err) {
+    Handle* h = static_cast<Handle*>(handle);
+    if (!h) return bad_arg(err, "null handle");
+    if (members < 1) return bad_arg(err, "batch nonempty");
+    if (n < 1 || (cyclic && n < 3)) return bad_arg(err, cyclic ? "n >= 3 for cyclic systems" : "n >= 1");
+    if (!sub.ptr || !main_diag.ptr || !sup.ptr || !rhs.ptr || !x) return bad_arg(err, "null buffer");
+    CK(cudaSetDevice(h->device), "cudaSetDevice");
+    cudaStream_t s = h->stream;
+    const int n_off = cyclic ? n : n - 1;
+    // Copy the four operands into one device buffer; each keeps its strides.
+    auto extent = [&](const pe3d_strided& a, int rows) -> int64_t {
+        if (rows <= 0) return 1;
+        return (rows - 1) * a.row_stride + int64_t(members - 1) * a.member_stride + 1;
+    };
+    const int64_t e_sub = extent(sub, n_off), e_main = extent(main_diag, n), e_sup = extent(sup, n_off),
+                  e_rhs = extent(rhs, n);
+    const int64_t total = e_sub + e_main + e_sup + e_rhs;
+    CK(h->sb_in.ensure(total * sizeof(cplx)), "alloc");
+    CK(h->sb_x.ensure(int64_t(members) * n * sizeof(cplx)), "alloc");
+    for (DevBuf* b : {&h->sb_cp, &h->sb_inv, &h->sb_y, &h->sb_q}) CK(b->ensure(int64_t(members) * n * sizeof(cplx)), "alloc");
+    CK(h->fail_row.ensure(int64_t(members) * sizeof(int)), "alloc");
+    CK(h->fail_mag.ensure(int64_t(members) * sizeof(double)), "alloc");
+    CK(h->err.ensure(sizeof(pe3d::DevError)), "alloc");
+    cplx* base = h->sb_in.as<cplx>();
+    int64_t off = 0;
+    pe3d::StridedC dsub, dmain, dsup, drhs;
+    auto put = [&](const pe3d_strided& a, int64_t ext, pe3d::StridedC& d) -> cudaError_t {
+        d.ptr = base + off;
+        d.row_stride = a.row_stride;
+        d.member_stride = a.member_stride;
+        cudaError_t e = cudaMemcpyAsync(base + off, a.ptr, ext * sizeof(cplx), cudaMemcpyHostToDevice, s);
+        off += ext;
+        return e;
+    };
+    CK(put(sub, e_sub, dsub), "H2D");
+    CK(put(main_diag, e_main, dmain), "H2D");
+    CK(put(sup, e_sup, dsup), "H2D");
+    CK(put(rhs, e_rhs, drhs), "H2D");
+    pe3d::DevError de0{NO_ERROR, 0, 0};
+    CK(cudaMemcpyAsync(h->err.ptr, &de0, sizeof(de0), cudaMemcpyHostToDevice, s), "H2D");
+    CK(pe3d::launch_solve_batch(n, members, cyclic, dsub, dmain, dsup, drhs, h->sb_x.as<cplx>(), h->sb_cp.as<cplx>(),
+                                h->sb_inv.as<cplx>(), h->sb_y.as<cplx>(), h->sb_q.as<cplx>(), h->fail_row.as<int>(),
+                                h->fail_mag.as<double>(), s),
+       "solve");
+    CK(pe3d::launch_reduce_failures(h->fail_row.as<int>(), h->fail_mag.as<double>(), 1, members, 0, 0, n,
+                                    h->err.as<pe3d::DevError>(), s),
+       "reduce");
+
+    int st = decode_error(h, s, err);
+    if (st != PE3D_OK) {
+        if (err) err->range_index = -1;
+        if (err && err->rank1) std::snprintf(err->message, sizeof(err->message),
+                                             "singular system: pivot %d, batch member %d (singular rank-1 correction)",
+                                             err->pivot, err->member);
+        return st;
+    }
+    CK(cudaMemcpyAsync(x, h->sb_x.ptr, int64_t(members) * n * sizeof(cplx), cudaMemcpyDeviceToHost, s), "D2H");
+    CK(cudaStreamSynchronize(s), "sync");
+    return PE3D_OK;
+}
+
+int pe3d_profile_last(void* handle, double* ms, int32_t* launches) {
+    Handle* h = static_cast<Handle*>(handle);
+    if (!h) return PE3D_BAD_ARGUMENT;
+    for (int k = 0; k < 3; ++k) {
+        if (ms) ms[k] = h->prof_ms[k];
+        if (launches) launches[k] = h->prof_n[k];
+    }
+    return PE3D_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,118 @@
+// pe3d_device.cuh -- complex fp64 arithmetic and shared types for the
+// sm_100a range-marching kernels.
+//
+// Complex multiply follows the FMA pattern numpy's complex128 loops use on
+// the reference host: re = fma(ar, br, -(ai*bi)),
+// im = fma(ar, bi, ai*br); complex division uses Smith's algorithm as
+// numpy does.  Matching them is not required by the 1e-9 parity contract
+// but keeps the drift against the oracle at the 1e-15 level per step.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace pe3d {
+
+struct __align__(16) cplx {
+    double re, im;
+};
+
+__host__ __device__ __forceinline__ cplx mk(double re, double im) { cplx c; c.re = re; c.im = im; return c; }
+__host__ __device__ __forceinline__ cplx czero() { return mk(0.0, 0.0); }
+__host__ __device__ __forceinline__ cplx cone() { return mk(1.0, 0.0); }
+__host__ __device__ __forceinline__ cplx cadd(cplx a, cplx b) { return mk(a.re + b.re, a.im + b.im); }
+__host__ __device__ __forceinline__ cplx csub(cplx a, cplx b) { return mk(a.re - b.re, a.im - b.im); }
+__host__ __device__ __forceinline__ cplx cneg(cplx a) { return mk(-a.re, -a.im); }
+// real scalar times complex, as numpy's float64 * complex128 (imaginary part of the scalar is 0)
+__host__ __device__ __forceinline__ cplx crmul(double s, cplx a) { return mk(s * a.re, s * a.im); }
+
+__host__ __device__ __forceinline__ cplx cmul(cplx a, cplx b) {
+    return mk(fma(a.re, b.re, -(a.im * b.im)), fma(a.re, b.im, a.im * b.re));
+}
+// a*b + c with fused accumulation (used on the scan paths, not reference-ordered)
+__host__ __device__ __forceinline__ cplx cfma(cplx a, cplx b, cplx c) {
+    return mk(fma(a.re, b.re, fma(-a.im, b.im, c.re)), fma(a.re, b.im, fma(a.im, b.re, c.im)));
+}
+
+// Smith's complex division a / b (numpy's algorithm for complex128).
+__host__ __device__ __forceinline__ cplx cdiv(cplx a, cplx b) {
+    const double abr = fabs(b.re), abi = fabs(b.im);
+    if (abr >= abi) {
+        if (abr == 0.0 && abi == 0.0) return mk(a.re / abr, a.im / abi);
+        const double rat = b.im / b.re;
+        const double scl = 1.0 / (b.re + b.im * rat);
+        return mk((a.re + a.im * rat) * scl, (a.im - a.re * rat) * scl);
+    }
+    const double rat = b.re / b.im;
+    const double scl = 1.0 / (b.im + b.re * rat);
+    return mk((a.re * rat + a.im) * scl, (a.im * rat - a.re) * scl);
+}
+__host__ __device__ __forceinline__ cplx crecip(cplx b) { return cdiv(cone(), b); }
+__host__ __device__ __forceinline__ double cabs(cplx a) { return hypot(a.re, a.im); }
+
+// principal square root
+__host__ __device__ __forceinline__ cplx csqrt(cplx z) {
+    if (z.re == 0.0 && z.im == 0.0) return czero();
+    const double r = hypot(z.re, z.im);
+    if (z.re >= 0.0) {
+        const double a = sqrt(0.5 * (r + z.re));
+        return mk(a, z.im / (2.0 * a));
+    }
+    const double b = copysign(sqrt(0.5 * (r - z.re)), z.im);
+    return mk(z.im / (2.0 * b), b);
+}
+
+__device__ __forceinline__ cplx ldc(const cplx* p) {
+    const double2 v = *reinterpret_cast<const double2*>(p);
+    return mk(v.x, v.y);
+}
+__device__ __forceinline__ cplx ldc_stream(const cplx* p) {
+    const double2 v = __ldcs(reinterpret_cast<const double2*>(p));
+    return mk(v.x, v.y);
+}
+__device__ __forceinline__ void stc(cplx* p, cplx v) {
+    *reinterpret_cast<double2*>(p) = make_double2(v.re, v.im);
+}
+__device__ __forceinline__ void stc_stream(cplx* p, cplx v) {
+    __stcs(reinterpret_cast<double2*>(p), make_double2(v.re, v.im));
+}
+
+__device__ __forceinline__ cplx shfl_up(cplx v, int d) {
+    return mk(__shfl_up_sync(0xffffffffu, v.re, d), __shfl_up_sync(0xffffffffu, v.im, d));
+}
+__device__ __forceinline__ cplx shfl_down(cplx v, int d) {
+    return mk(__shfl_down_sync(0xffffffffu, v.re, d), __shfl_down_sync(0xffffffffu, v.im, d));
+}
+__device__ __forceinline__ cplx shfl_idx(cplx v, int src) {
+    return mk(__shfl_sync(0xffffffffu, v.re, src), __shfl_sync(0xffffffffu, v.im, src));
+}
+
+constexpr double PIVOT_FLOOR = 1e-300;   // ref tridiag.py:31
+constexpr double TL_FLOOR_DB = 300.0;    // ref environment.py:29
+constexpr int TILE_ROWS = 8;             // depth rows per 128-B device tile
+
+// Per-frequency constants, built on the host from pe3d_coeffs.
+struct FreqDev {
+    double k0;
+    double s_z;          // 1/(k0 dz)^2                  (ref operators.py:94)
+    cplx cx_lhs, cx_rhs, cy_lhs, cy_rhs;
+    cplx off_z;          // cx_lhs * s_z: depth off-diagonal (ref operators.py:231)
+};
+
+// Device layout of the field ("depth tiles"): element (f, m, l) lives at
+//   ((f * n_tiles + l / 8) * n_theta + m) * 8 + l % 8
+// so the 8 depths of one azimuth form one 128-byte line.  A depth column
+// is n_tiles lines of 128 B; an azimuth ring of 8 depths is contiguous.
+__host__ __device__ __forceinline__ int64_t tidx(int f, int m, int l, int n_tiles, int n_theta) {
+    return ((int64_t(f) * n_tiles + (l >> 3)) * n_theta + m) * 8 + (l & 7);
+}
+
+// Error flag shared by all kernels of a march: the first failure (lowest
+// packed key) wins.  key = (step << 40) | (sweep << 39) | (freq << 24) | member
+struct DevError {
+    unsigned long long key;   // ~0ull = none
+    int32_t pivot;
+    int32_t rank1;
+};
+
+}  // namespace pe3d

@@ -1,0 +1,64 @@
+// pe3d_internal.h -- launch interface between the C ABI (pe3d_abi.cu) and
+// the kernels (pe3d_kernels.cu).  Not part of the public ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "pe3d_device.cuh"
+
+namespace pe3d {
+
+struct StridedC {
+    const cplx* ptr;
+    int64_t row_stride;
+    int64_t member_stride;
+};
+
+// What the ring epilogue writes besides nothing: TL sample, snapshot,
+// final slab (reference layout), and the next step's temp (device tiles).
+struct EpilogueArgs {
+    double* tl;             // [F][n_samples][n_theta][n_depth] or null
+    cplx* snap;             // [F][n_samples][n_theta][n_depth] or null
+    cplx* final_out;        // [F][n_theta][n_depth] or null
+    int64_t* clamped;       // [F]
+    const double* w_abs;    // [F] |w(r)| of this sample
+    int n_samples;
+    int sample;
+    int periodic;
+    int write_temp;
+};
+
+struct LaunchCtx {
+    int n_freq, n_theta, n_depth, n_tiles;
+    int sector;
+    int num_sms;
+    double delta_theta;
+    const FreqDev* fdev;
+    cplx* loc_tab;          // [F][n_tiles*8]
+    cplx* mul_tab;          // [F][n_tiles*8]
+    DevError* err;
+    cudaStream_t stream;
+};
+
+void ring_shape(int n_theta, int* L, int* RW);
+int depth_cols_per_block(const LaunchCtx& c);
+cudaError_t launch_factor_depth(const LaunchCtx& c, const cplx* local, int64_t local_fstride, int step_for_error);
+cudaError_t launch_depth_scan(const LaunchCtx& c, const cplx* src, cplx* dst, int cols_per_block);
+cudaError_t launch_azimuth_scan(const LaunchCtx& c, const cplx* src, cplx* dst, double r_new,
+                                const EpilogueArgs& ea, int step_for_error);
+cudaError_t launch_finish(const LaunchCtx& c, const cplx* src, int src_tiled, cplx* dst, double r,
+                          const EpilogueArgs& ea);
+cudaError_t launch_depth_serial(const LaunchCtx& c, const cplx* src, cplx* dst, cplx* scratch, const cplx* local_now,
+                                const cplx* local_new, int64_t fstride, int64_t mstride, int* fail_row,
+                                double* fail_mag);
+cudaError_t launch_azimuth_serial(const LaunchCtx& c, const cplx* src, cplx* dst, cplx* cp, cplx* inv, cplx* qv,
+                                  cplx* ring, double r_new, int step_for_error);
+cudaError_t launch_solve_batch(int n, int members, int cyclic, StridedC sub, StridedC mainv, StridedC sup,
+                               StridedC rhs, cplx* x, cplx* cp, cplx* inv, cplx* y, cplx* q, int* fail_row,
+                               double* fail_mag, cudaStream_t stream);
+cudaError_t launch_zero(cplx* p, int64_t n, cudaStream_t stream);
+cudaError_t launch_reduce_failures(const int* fail_row, const double* fail_mag, int n_freq, int members, int step,
+                                   int sweep, int rank1_row, DevError* err, cudaStream_t stream);
+
+}  // namespace pe3d

@@ -1,0 +1,332 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's
+golden fixtures and the CPU oracle.
+
+Contract (BASELINE.json north_star): field relative L2 <= 1e-9 and
+|dTL| <= 1e-4 dB wherever TL < 150 dB, at every output range.  Tighter
+bounds are used where the reference's own tests pin them (criteria 1, 2,
+4 of ref tests/test_acceptance.py).
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+from oracle import pe3d_oracle as O
+from paper_1711_00005_b200 import (
+    Absorber, Environment, FieldSlab, Grid3D, MarchState, SoundSpeedProfile, SourceSpec, StepCoefficients,
+    configs, gaussian_starter, march_frequencies, range_step, run_frequency, wavenumber,
+)
+from paper_1711_00005_b200 import _native
+from paper_1711_00005_b200.config import Config, RunOptions
+from paper_1711_00005_b200.environment import PERIODIC, SECTOR
+from paper_1711_00005_b200.errors import DomainError, SingularSystemError, StepError
+from paper_1711_00005_b200.tridiag import CYCLIC, OPEN, SolveBatch, TriDiagSystem, solve_batch, solve_cyclic, solve_thomas
+
+pytestmark = pytest.mark.gpu
+
+FIELD_TOL = 1e-9
+TL_TOL = 1e-4
+
+
+def rel_l2(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def tl_err(a, b):
+    mask = b < 150.0
+    return float(np.abs(a - b)[mask].max()) if mask.any() else 0.0
+
+
+def make_grid(n_range=10, n_azimuth=8, n_depth=32, delta_r=5.0, delta_z=4.0, r_start=None, topology=PERIODIC):
+    dth = 2 * math.pi / n_azimuth if topology == PERIODIC else math.radians(2.0)
+    return Grid3D(n_range, n_azimuth, n_depth, delta_r, dth, delta_z, delta_r if r_start is None else r_start,
+                  topology)
+
+
+def make_env(grid, attenuation=0.01, start_frac=0.75, profile=None):
+    return Environment(1500.0, profile or SoundSpeedProfile.uniform(1500.0), 6000.0,
+                       Absorber(start_frac * grid.depth_extent, attenuation), grid.depth_extent)
+
+
+# ------------------------------------------------------------ solve_batch
+
+def _fixture_systems(fx, tag):
+    off = offo = 0
+    for n in fx[f"{tag}_n"]:
+        n = int(n)
+        n_off = n if tag == "cyclic" else n - 1
+        yield TriDiagSystem(fx[f"{tag}_sub"][offo:offo + n_off], fx[f"{tag}_main"][off:off + n],
+                            fx[f"{tag}_sup"][offo:offo + n_off], fx[f"{tag}_rhs"][off:off + n],
+                            OPEN if tag == "open" else CYCLIC), fx[f"{tag}_x"][off:off + n]
+        off += n
+        offo += n_off
+
+
+@pytest.mark.parametrize("tag", ["open", "cyclic"])
+def test_solve_matches_reference_solutions(golden, tag):
+    fx = golden("tridiag_systems.npz")
+    for system, x_ref in _fixture_systems(fx, tag):
+        x = solve_thomas(system) if tag == "open" else solve_cyclic(system)
+        assert np.abs(x - x_ref).max() <= 1e-12 * np.abs(x_ref).max()
+
+
+def test_criterion_01_random_systems_vs_dense():
+    rng = np.random.default_rng(1001)
+    for cyclic in (False, True):
+        for _ in range(100):
+            n = int(rng.integers(3, 129))
+            sub, main, sup, rhs = O.random_system(rng, n, cyclic)
+            x = solve_batch(SolveBatch(sub[:, None], main[:, None], sup[:, None], rhs[:, None],
+                                       CYCLIC if cyclic else OPEN))[0]
+            ref = O.dense_solve(sub, main, sup, rhs, cyclic)
+            assert np.abs(x - ref).max() <= 1e-10 * np.abs(ref).max()
+
+
+def test_batch_fixture_broadcast_and_order(golden):
+    fx = golden("tridiag_systems.npz")
+    x = solve_batch(SolveBatch(fx["batch_sub"], fx["batch_main"], fx["batch_sup"], fx["batch_rhs"], CYCLIC))
+    assert np.abs(x - fx["batch_x"]).max() <= 1e-12 * np.abs(fx["batch_x"]).max()
+    # broadcast views (stride 0), as assemble_azimuth_batch builds them
+    n, w = 17, 40
+    rng = np.random.default_rng(3)
+    rhs = rng.standard_normal((n, w)) + 1j * rng.standard_normal((n, w))
+    b = SolveBatch(np.broadcast_to(np.complex128(0.3 - 0.1j), (n, w)),
+                   np.broadcast_to(np.complex128(2.0 + 1j), (n, w)),
+                   np.broadcast_to(np.complex128(0.3 - 0.1j), (n, w)), rhs, CYCLIC)
+    x = solve_batch(b)
+    ref = O.solve_batch(b.sub, b.main, b.sup, b.rhs, cyclic=True)
+    assert np.abs(x - ref).max() <= 1e-13 * np.abs(ref).max()
+
+
+def test_singular_lowest_member_across_tiles():
+    rng = np.random.default_rng(6)
+    systems = [TriDiagSystem(*O.random_system(rng, 6, False)) for _ in range(200)]
+    bad = TriDiagSystem(np.ones(5), np.zeros(6), np.ones(5), np.ones(6))
+    systems[70] = systems[150] = bad
+    with pytest.raises(SingularSystemError) as info:
+        solve_batch(SolveBatch.from_systems(systems), parallel_hint=4)
+    assert info.value.member_index == 70 and info.value.pivot_index == 0
+
+
+def test_zero_pivot_and_single_unknown():
+    with pytest.raises(SingularSystemError) as info:
+        solve_thomas(TriDiagSystem(np.ones(2), np.zeros(3), np.ones(2), np.ones(3)))
+    assert info.value.pivot_index == 0
+    assert solve_thomas(TriDiagSystem(np.zeros(0), np.array([2.0]), np.zeros(0), np.array([5.0])))[0] == 2.5
+    x = solve_cyclic(TriDiagSystem(np.full(3, -1.0), np.full(3, 3.0), np.full(3, -1.0), np.ones(3), CYCLIC))
+    assert np.allclose(x, 1.0, rtol=1e-12)
+
+
+# ------------------------------------------------------------ range_step
+
+def test_criterion_02_dense_step_3x3(golden):
+    fx = golden("dense_step_3x3.npz")
+    grid = Grid3D(10, 3, 3, 4.0, 2 * math.pi / 3, 7.0, 30.0)
+    env = make_env(grid, attenuation=0.0, start_frac=0.5)
+    k0 = float(fx["k0"])
+    state = MarchState(FieldSlab(fx["u0"].copy(), 30.0), 0, StepCoefficients.for_step(k0, 4.0), env, grid, k0)
+    out = range_step(state).slab.values
+    assert np.abs(out - fx["out"]).max() <= 1e-12 * np.abs(fx["out"]).max()
+
+
+def test_criterion_03_delta_zero_bitwise():
+    rng = np.random.default_rng(1003)
+    grid = make_grid()
+    env = make_env(grid)
+    v = rng.standard_normal((8, 32)) + 1j * rng.standard_normal((8, 32))
+    v[:, 0] = 0
+    k0 = wavenumber(50.0, 1500.0)
+    state = MarchState(FieldSlab(v.copy(), grid.r_start), 0, StepCoefficients.for_step(k0, 0.0), env, grid, k0)
+    after = range_step(state)
+    assert after.range_index == 1 and after.slab.values.tobytes() == v.tobytes()
+
+
+@pytest.mark.parametrize("topology", [PERIODIC, SECTOR])
+def test_small_march_every_step(golden, topology):
+    fx = golden(f"small_march_{topology}.npz")
+    grid = make_grid(n_range=30, n_azimuth=8, n_depth=32, delta_r=5.0, delta_z=4.0, r_start=5.0, topology=topology)
+    env = make_env(grid, profile=SoundSpeedProfile(fx["profile_z"], fx["profile_c"]))
+    k0 = float(fx["k0"])
+    state = MarchState(FieldSlab(fx["u0"].copy(), grid.r_start), 0, StepCoefficients.for_step(k0, 5.0),
+                       env, grid, k0)
+    for j in range(30):
+        state = range_step(state)
+        assert rel_l2(state.slab.values, fx["slabs"][j]) <= 1e-12, f"step {j + 1}"
+        assert state.slab.range_m == grid.range_at(j + 1)
+
+
+def test_singular_depth_becomes_step_error():
+    grid = make_grid(n_azimuth=4, n_depth=8, delta_z=1.0)
+    env = make_env(grid)
+    coeffs = StepCoefficients(delta=1j, cx_lhs=0.5 + 0j, cx_rhs=0j, cy_lhs=0j, cy_rhs=0j)
+    state = MarchState(FieldSlab(np.ones((4, 8), dtype=complex), grid.r_start), 0, coeffs, env, grid, 1.0)
+    with pytest.raises(StepError) as info:
+        range_step(state)
+    assert info.value.sweep == "depth" and info.value.range_index == 1 and info.value.member_index == 0
+
+
+def test_step_beyond_grid_rejected():
+    grid = make_grid(n_range=3)
+    env = make_env(grid)
+    k0 = wavenumber(50.0, 1500.0)
+    state = MarchState(gaussian_starter(grid, SourceSpec((50.0,), 60.0), k0), 0,
+                       StepCoefficients.for_step(k0, grid.delta_r), env, grid, k0)
+    for _ in range(3):
+        state = range_step(state)
+    with pytest.raises(DomainError, match="n_range"):
+        range_step(state)
+
+
+# ------------------------------------------------------------ run_frequency
+
+def test_cfg1_full_length_vs_reference(golden):
+    fx = golden("cfg1_full.npz")
+    res = run_frequency(configs.build("cfg1"), 50.0)
+    assert np.array_equal(res.ranges, fx["ranges"])
+    assert rel_l2(res.final_slab.values, fx["final"]) <= FIELD_TOL
+    assert tl_err(res.tl_field[:, 0, :], fx["tl_theta0"]) <= TL_TOL
+    # azimuth independent medium + starter: every azimuth carries the same TL
+    assert np.ptp(res.tl_field, axis=1).max() <= 1e-6
+
+
+def test_snapshots_every_output_range_vs_oracle():
+    cfg = configs.build("cfg1", n_range=60, frequencies=(50.0, 65.0), output_stride=10)
+    for r in march_frequencies(cfg, [50.0, 65.0], keep_snapshots=True):
+        ref = O.run_frequency(cfg, r.frequency, keep_snapshots=True)
+        assert r.snapshots.shape == ref.snapshots.shape
+        for s in range(ref.snapshots.shape[0]):
+            assert rel_l2(r.snapshots[s], ref.snapshots[s]) <= FIELD_TOL, s
+        assert tl_err(r.tl_field, ref.tl_field) <= TL_TOL
+        assert r.clamped_samples == ref.clamped
+
+
+FULL = {"cfg2": (100.0, 20), "cfg4a": (50.0, 10), "cfg4b": (500.0, 10), "cfg5": (500.0, 3), "cfg3": (25.0, 20)}
+
+
+@pytest.mark.parametrize("key", ["cfg2", "cfg4a", "cfg4b", "cfg5", "cfg3"])
+def test_full_size_steps_vs_reference(golden, key):
+    name = key[:4]
+    freq, steps = FULL[key]
+    fx = golden(f"{name}_f{int(freq)}_{steps}steps.npz")
+    cfg = configs.build(name, n_range=steps, frequencies=(freq,), output_stride=1)
+    r = march_frequencies(cfg, [freq], keep_snapshots=True)[0]
+    for j in range(steps):
+        u = r.snapshots[j + 1]
+        got = u[fx["mi"], fx["li"]]
+        assert np.linalg.norm(got - fx["samples"][j]) <= FIELD_TOL * np.linalg.norm(fx["samples"][j]), j
+        assert abs(np.linalg.norm(u) - fx["norms"][j]) <= FIELD_TOL * fx["norms"][j]
+    assert rel_l2(r.final_slab.values[0], fx["col0"]) <= FIELD_TOL
+
+
+def test_serial_and_scan_paths_agree():
+    cfg = configs.build("cfg4", n_range=12, frequencies=(50.0, 200.0), output_stride=4)
+    a = march_frequencies(cfg, [50.0, 200.0])
+    b = march_frequencies(cfg, [50.0, 200.0], flags=_native.FLAG_SERIAL)
+    for x, y in zip(a, b):
+        assert rel_l2(x.final_slab.values, y.final_slab.values) <= 1e-11
+        assert tl_err(x.tl_field, y.tl_field) <= 1e-8
+
+
+def test_batch_equals_single_and_rerun_bitwise():
+    cfg = configs.build("cfg4", n_range=8, frequencies=(50.0, 90.0, 300.0), output_stride=4)
+    batch = march_frequencies(cfg, [50.0, 90.0, 300.0])
+    single = march_frequencies(cfg, [90.0])[0]
+    again = march_frequencies(cfg, [50.0, 90.0, 300.0])
+    assert batch[1].final_slab.values.tobytes() == single.final_slab.values.tobytes()
+    assert batch[1].tl_field.tobytes() == single.tl_field.tobytes()
+    for x, y in zip(batch, again):
+        assert x.final_slab.values.tobytes() == y.final_slab.values.tobytes()
+
+
+def test_run_frequency_contract():
+    grid = make_grid(n_range=10, delta_r=5.0, r_start=5.0)
+    env = make_env(grid)
+    src = SourceSpec((50.0,), 62.0)
+    res = run_frequency(Config(grid, env, src, RunOptions(output_stride=4)), 50.0)
+    assert res.tl_field.shape == (3, 8, 32) and res.output_stride == 4
+    res = run_frequency(Config(grid, env, src, RunOptions(max_range=26.0, output_stride=1)), 50.0)
+    assert res.final_slab.range_m == 25.0 and res.tl_field.shape[0] == 5
+    res = run_frequency(Config(grid, env, src, RunOptions(max_range=1.0, output_stride=1)), 50.0)
+    assert res.ranges.tolist() == [5.0] and res.tl_field.shape[0] == 1
+    with pytest.raises(DomainError, match="not one of the source"):
+        run_frequency(Config(grid, env, src, RunOptions()), 60.0)
+    assert np.all(np.isfinite(res.tl_field))
+
+
+def test_criterion_04_azimuth_symmetry_100_steps():
+    grid = make_grid(n_range=100, n_azimuth=64, n_depth=256, delta_r=5.0, delta_z=4.0, r_start=5.0)
+    env = make_env(grid)
+    cfg = Config(grid, env, SourceSpec((50.0,), 200.0), RunOptions(output_stride=1))
+    r = march_frequencies(cfg, [50.0], keep_snapshots=True)[0]
+    for s in r.snapshots[1:]:
+        mags = np.abs(s)
+        assert (mags.max(axis=0) - mags.min(axis=0)).max() <= 1e-9 * mags.max()
+
+
+def test_criterion_05_cylindrical_spreading():
+    grid = Grid3D(3200, 8, 65, 5.0, 2 * math.pi / 8, 3.125, 5.0)
+    env = Environment(1500.0, SoundSpeedProfile.uniform(1500.0), 6000.0, Absorber(0.9 * grid.depth_extent, 0.0),
+                      grid.depth_extent)
+    res = run_frequency(Config(grid, env, SourceSpec((50.0,), 75.0), RunOptions(output_stride=1)), 50.0)
+    tl = res.tl_field[:, 0, round(75.0 / grid.delta_z)]
+    r = res.ranges
+    diffs = []
+    for i, ri in enumerate(r):
+        if 20 * 30.0 <= ri <= grid.max_range / 2:
+            j = int(round((2 * ri - r[0]) / grid.delta_r))
+            if j < len(r) and abs(r[j] - 2 * ri) < 1e-6:
+                diffs.append(tl[j] - tl[i])
+    assert abs(np.mean(diffs) - 3.01) <= 0.5
+
+
+def test_criterion_06_convergence_order():
+    def run(dr, n):
+        grid = make_grid(n_range=n, n_azimuth=8, n_depth=128, delta_r=dr, delta_z=3.0, r_start=10.0)
+        env = make_env(grid)
+        l = np.arange(128)
+        modes = sum(a * np.sin(q * math.pi * l / 128) for q, a in ((2, 1.0), (3, 0.6), (5, 0.3)))
+        az = 1.0 + 0.3 * np.cos(np.arange(8) * grid.delta_theta)
+        v = np.outer(az, modes).astype(np.complex128)
+        k0 = wavenumber(50.0, 1500.0)
+        local = np.ascontiguousarray(O_local(env, grid, k0))
+        out = np.empty_like(v)
+        g = _native.GridParams(1, 8, 128, 0, n, n, 0, 0, dr, grid.delta_theta, 3.0, 10.0, 10.0)
+        _native.call("pe3d_march_host", _native.handle(), g,
+                     _native.make_coeffs([k0], [StepCoefficients.for_step(k0, dr)]),
+                     _native.ptr(local), _native.ptr(v), _native.ptr(out), None, None, None)
+        return out
+    e1 = np.linalg.norm(run(5.0, 160) - run(2.5, 320))
+    e2 = np.linalg.norm(run(2.5, 320) - run(1.25, 640))
+    assert math.log2(e1 / e2) >= 1.0
+
+
+def O_local(env, grid, k0):
+    from paper_1711_00005_b200.environment import local_term_grid
+    return local_term_grid(env, grid, grid.r_start, k0)[0]
+
+
+def test_linearity_and_rhs_scaling_full_cfg4():
+    """Size-independent property at the full cfg4 grid (64 frequencies):
+    the march is linear in the starter."""
+    cfg = configs.build("cfg4", n_range=5)
+    grid = cfg.grid
+    freqs = list(cfg.source.frequencies)
+    k0s = [wavenumber(f, 1500.0) for f in freqs]
+    rng = np.random.default_rng(11)
+    F = len(freqs)
+    u1 = rng.standard_normal((F, 256, 1024)) + 1j * rng.standard_normal((F, 256, 1024))
+    u2 = rng.standard_normal((F, 256, 1024)) + 1j * rng.standard_normal((F, 256, 1024))
+    a, b = 0.7 - 1.1j, -2.0 + 0.4j
+    local = np.ascontiguousarray(np.stack([O_local(cfg.environment, grid, k0) for k0 in k0s]))
+    coeffs = _native.make_coeffs(k0s, [StepCoefficients.for_step(k0, grid.delta_r) for k0 in k0s])
+
+    def march(u):
+        out = np.empty_like(u)
+        g = _native.GridParams(F, 256, 1024, 0, 5, 5, 0, 0, grid.delta_r, grid.delta_theta, grid.delta_z,
+                               grid.r_start, grid.r_start)
+        _native.call("pe3d_march_host", _native.handle(), g, coeffs, _native.ptr(local),
+                     _native.ptr(np.ascontiguousarray(u)), _native.ptr(out), None, None, None)
+        return out
+    x1, x2, x12 = march(u1), march(u2), march(a * u1 + b * u2)
+    assert rel_l2(x12, a * x1 + b * x2) <= 1e-12
