@@ -869,6 +869,10 @@ cudaError_t launch_depth_scan(const LaunchCtx& c, const cplx* src, cplx* dst, in
     const int nwarps = nthreads / 32;
     const size_t sm = sizeof(cplx) * (nwarps * 256 + 6 * nwarps);
     dim3 grid((c.n_theta + cols_per_block - 1) / cols_per_block, c.n_freq);
+    if (sm > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(k_depth_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        if (e != cudaSuccess) return e;
+    }
     k_depth_scan<<<grid, nthreads, sm, c.stream>>>(src, dst, c.loc_tab, c.mul_tab, c.fdev, c.n_theta, c.n_tiles,
                                                    cols_per_block, c.sector);
     return cudaGetLastError();
