@@ -50,7 +50,7 @@ struct Handle {
     // march workspace
     DevBuf field_a, field_b, field_c;     // device tiles [F][n_tiles][n_theta][8]
     DevBuf loc_tab, mul_tab, fdev, w_abs, err;
-    DevBuf az_cp, az_inv, az_q, az_ring, fail_row, fail_mag;
+    DevBuf az_cp, az_inv, az_q, az_ring, fail_row, fail_mag, ring_tab;
     // staging for the host entry points
     DevBuf h_local, h_local2, h_u0, h_final, h_tl, h_snap, h_clamped;
     // solve_batch
@@ -206,7 +206,6 @@ cudaError_t enqueue_steps(Handle* h, const pe3d_grid* g, const MarchPlan& p, con
     cplx* A = h->field_a.as<cplx>();
     cplx* B = h->field_b.as<cplx>();
     cplx* C = h->field_c.as<cplx>();
-    const int cols = pe3d::depth_cols_per_block(c);
     const bool periodic = g->topology == PE3D_PERIODIC;
     for (int s = 0; s < g->n_steps; ++s) {
         const int j_new = g->first_index + s + 1;
@@ -220,7 +219,7 @@ cudaError_t enqueue_steps(Handle* h, const pe3d_grid* g, const MarchPlan& p, con
                                                                           c.n_freq, c.n_theta, j_new, 0, -1, c.err,
                                                                           c.stream); });
         } else {
-            e = prof.run(0, [&] { return pe3d::launch_depth_scan(c, A, B, cols); });
+            e = prof.run(0, [&] { return pe3d::launch_depth_scan(c, A, B); });
         }
         if (e != cudaSuccess) return e;
         pe3d::EpilogueArgs ea{};
@@ -235,7 +234,8 @@ cudaError_t enqueue_steps(Handle* h, const pe3d_grid* g, const MarchPlan& p, con
         ea.periodic = periodic;
         ea.write_temp = (s < g->n_steps - 1);
         if (periodic && !p.serial) {
-            e = prof.run(1, [&] { return pe3d::launch_azimuth_scan(c, B, A, r_new, ea, j_new); });
+            const cplx* tab = h->ring_tab.as<cplx>() + int64_t(s) * c.n_freq * pe3d::ring_table_elems(c.n_theta);
+            e = prof.run(1, [&] { return pe3d::launch_azimuth_scan(c, B, A, tab, r_new, ea); });
         } else {
             e = prof.run(1, [&] { return pe3d::launch_azimuth_serial(c, B, C, h->az_cp.as<cplx>(), h->az_inv.as<cplx>(),
                                                                      h->az_q.as<cplx>(), h->az_ring.as<cplx>(), r_new,
@@ -286,7 +286,7 @@ int pe3d_handle_destroy(void* handle) {
     if (!h) return PE3D_OK;
     cudaSetDevice(h->device);
     for (DevBuf* b : {&h->field_a, &h->field_b, &h->field_c, &h->loc_tab, &h->mul_tab, &h->fdev, &h->w_abs, &h->err,
-                      &h->az_cp, &h->az_inv, &h->az_q, &h->az_ring, &h->fail_row, &h->fail_mag, &h->h_local,
+                      &h->az_cp, &h->az_inv, &h->az_q, &h->az_ring, &h->fail_row, &h->fail_mag, &h->ring_tab, &h->h_local,
                       &h->h_local2, &h->h_u0, &h->h_final, &h->h_tl, &h->h_snap, &h->h_clamped, &h->sb_in, &h->sb_x,
                       &h->sb_cp, &h->sb_inv, &h->sb_y, &h->sb_q})
         b->release();
@@ -361,6 +361,13 @@ int pe3d_march_device(void* handle, const pe3d_grid* g, const pe3d_coeffs* coeff
     const cplx* local = reinterpret_cast<const cplx*>(d_local);
     Prof prof{h, (g->flags & PE3D_FLAG_PROFILE) != 0, stream, {}};
     if (!p.serial) CK(prof.run(2, [&] { return pe3d::launch_factor_depth(c, local, NZ, g->first_index + 1); }), "factor");
+    if (!p.serial && g->topology == PE3D_PERIODIC && g->n_steps > 0) {
+        const int64_t E = pe3d::ring_table_elems(NT);
+        CK(h->ring_tab.ensure(int64_t(g->n_steps) * F * E * sizeof(cplx)), "alloc ring table");
+        CK(prof.run(2, [&] { return pe3d::launch_ring_setup(c, h->ring_tab.as<cplx>(), g->n_steps, g->first_index,
+                                                            g->r_start, g->delta_r); }),
+           "ring setup");
+    }
 
     // starter: boundary, TL sample 0, first temp (ref marching.py:159-172)
     pe3d::EpilogueArgs ea0{};
@@ -392,7 +399,7 @@ int pe3d_march_device(void* handle, const pe3d_grid* g, const pe3d_coeffs* coeff
         add(coeffs, sizeof(pe3d_coeffs) * F);
         add(ptrs, sizeof(ptrs));
         add(&stream, sizeof(stream));
-        const void* tabs[4] = {h->w_abs.ptr, h->fdev.ptr, h->loc_tab.ptr, h->err.ptr};
+        const void* tabs[5] = {h->w_abs.ptr, h->fdev.ptr, h->loc_tab.ptr, h->err.ptr, h->ring_tab.ptr};
         add(tabs, sizeof(tabs));
         if (!(h->graph_exec && key == h->graph_key)) {
             if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);

@@ -115,4 +115,34 @@ struct DevError {
     int32_t rank1;
 };
 
+// ------------------------------------------------------------- shared helpers
+
+__device__ __forceinline__ void report_failure(DevError* err, unsigned long long key, int pivot, int rank1) {
+    const unsigned long long old = atomicMin(&err->key, key);
+    if (key < old) {            // benign race on the payload: the lowest key's writer wins last
+        err->pivot = pivot;
+        err->rank1 = rank1;
+    }
+}
+
+__host__ __device__ __forceinline__ unsigned long long fail_key(int step, int sweep, int f, int member) {
+    return (static_cast<unsigned long long>(step) << 40) | (static_cast<unsigned long long>(sweep) << 39) |
+           (static_cast<unsigned long long>(f) << 24) | static_cast<unsigned long long>(member);
+}
+
+// s_theta = 1/(k0 r dtheta)^2, evaluated in the reference's order (operators.py:102)
+__host__ __device__ __forceinline__ double azimuth_scale(double k0, double r, double dth) {
+    const double x = (k0 * r) * dth;
+    return 1.0 / (x * x);
+}
+
+// cp.async (LDGSTS): 16-byte global -> shared copies, grouped and awaited per thread.
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
 }  // namespace pe3d

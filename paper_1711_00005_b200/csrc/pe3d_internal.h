@@ -42,11 +42,13 @@ struct LaunchCtx {
 };
 
 void ring_shape(int n_theta, int* L, int* RW);
-int depth_cols_per_block(const LaunchCtx& c);
+int ring_table_elems(int n_theta);   // complex entries per (step, frequency) ring table
 cudaError_t launch_factor_depth(const LaunchCtx& c, const cplx* local, int64_t local_fstride, int step_for_error);
-cudaError_t launch_depth_scan(const LaunchCtx& c, const cplx* src, cplx* dst, int cols_per_block);
-cudaError_t launch_azimuth_scan(const LaunchCtx& c, const cplx* src, cplx* dst, double r_new,
-                                const EpilogueArgs& ea, int step_for_error);
+cudaError_t launch_depth_scan(const LaunchCtx& c, const cplx* src, cplx* dst);
+cudaError_t launch_ring_setup(const LaunchCtx& c, cplx* table, int n_steps, int first_index, double r_start,
+                              double delta_r);
+cudaError_t launch_azimuth_scan(const LaunchCtx& c, const cplx* src, cplx* dst, const cplx* table_step, double r_new,
+                                const EpilogueArgs& ea);
 cudaError_t launch_finish(const LaunchCtx& c, const cplx* src, int src_tiled, cplx* dst, double r,
                           const EpilogueArgs& ea);
 cudaError_t launch_depth_serial(const LaunchCtx& c, const cplx* src, cplx* dst, cplx* scratch, const cplx* local_now,
