@@ -58,17 +58,49 @@ __global__ void k_factor_depth(const cplx* __restrict__ local, int64_t local_fst
     }
 }
 
-// Stage one column's 32 depth tiles of this warp (32 lines of 128 B) into
-// shared memory: lane -> (line 4k + lane/8, element lane%8), XOR-swizzled
-// so that the per-thread tile reads are bank-conflict free.
-__device__ __forceinline__ void stage_column(cplx* stage, const cplx* col_base, int64_t line_stride, int warp,
-                                             int lane, int n_tiles) {
+// Per-lane addressing of one column's 32 depth tiles of this warp (32 lines
+// of 128 B): lane -> (line 4k + lane/8, element lane%8), k = 0..7, so one
+// warp instruction moves 4 full lines.  In shared memory the element is
+// XOR-swizzled by the line index so that the per-thread tile reads
+// (lane = line) are bank-conflict free.
+struct LaneLines {
+    int64_t goff;          // global element offset of k = 0 relative to the column base
+    int64_t gstep;         // 4 lines
+    int soff_even, soff_odd;
+    unsigned valid;        // bit k: line 4k + lane/8 exists
+};
+
+__device__ __forceinline__ LaneLines lane_lines(int warp, int lane, int n_tiles, int64_t line_stride) {
+    LaneLines ll;
+    const int ln = lane >> 3, e = lane & 7;
+    ll.goff = int64_t(warp * 32 + ln) * line_stride + e;
+    ll.gstep = 4 * line_stride;
+    ll.soff_even = ln * 8 + (e ^ ln);
+    ll.soff_odd = ln * 8 + (e ^ (ln | 4));
+    ll.valid = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+        if (warp * 32 + 4 * k + ln < n_tiles) ll.valid |= 1u << k;
+    return ll;
+}
+
+__device__ __forceinline__ void stage_column(cplx* stage, const cplx* col_base, const LaneLines& ll) {
+    const cplx* gp = col_base + ll.goff;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-        const int line = 4 * k + (lane >> 3), e = lane & 7, tile = warp * 32 + line;
-        cplx* d = stage + line * 8 + (e ^ (line & 7));
-        if (tile < n_tiles) cp_async16(d, col_base + tile * line_stride + e);
+        cplx* d = stage + 32 * k + ((k & 1) ? ll.soff_odd : ll.soff_even);
+        if (ll.valid & (1u << k)) cp_async16(d, gp);
         else *d = czero();
+        gp += ll.gstep;
+    }
+}
+
+__device__ __forceinline__ void unstage_column(cplx* col_base, const cplx* stage, const LaneLines& ll) {
+    cplx* gp = col_base + ll.goff;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        if (ll.valid & (1u << k)) stc(gp, stage[32 * k + ((k & 1) ? ll.soff_odd : ll.soff_even)]);
+        gp += ll.gstep;
     }
 }
 
@@ -90,7 +122,8 @@ __host__ __device__ constexpr size_t depth_smem_elems(int nthreads) {
 // so that b_l = m_l (A_l x_l + beta d2_l) = inv_l rhs_l with
 // beta = kappa cx_rhs s_z.  The Kogge-Stone multipliers of the tile scans
 // (products of m_l over windows of tiles) are column independent too and,
-// for up to 256 threads, are computed once per frequency into shared memory.
+// for up to 256 threads, are computed once per frequency into shared memory
+// -- with zeros where a lane has no partner, so the scans are branch free.
 template <int MAXT>
 __global__ void __launch_bounds__(MAXT, DepthCfg<MAXT>::MINB)
 k_depth_scan(const cplx* __restrict__ src, cplx* __restrict__ dst, const cplx* __restrict__ loc_tab,
@@ -116,27 +149,29 @@ k_depth_scan(const cplx* __restrict__ src, cplx* __restrict__ dst, const cplx* _
     const int64_t g0 = int64_t(blockIdx.x) * cols_per_cta;
     const int64_t g1 = g0 + cols_per_cta < total_cols ? g0 + cols_per_cta : total_cols;
     if (g0 >= g1) return;
+    const int n_cols = int(g1 - g0);
     const bool active = t < n_tiles;
     const int64_t nz8 = int64_t(n_tiles) * 8;
     const int64_t line_stride = int64_t(n_theta) * 8;
-    auto col_base = [&](int64_t g) {
-        const int64_t f = g / n_theta, m = g - f * n_theta;
-        return src + f * n_tiles * line_stride + m * 8;
-    };
+    const int64_t freq_stride = int64_t(n_tiles) * line_stride;
+    const LaneLines ll = lane_lines(warp, lane, n_tiles, line_stride);
 
-    // pipeline prologue
+    // (frequency, column) of the next column to prefetch
+    int pf = int(g0 / n_theta), pc = int(g0 - int64_t(pf) * n_theta);
 #pragma unroll
     for (int p = 0; p < STAGES - 1; ++p) {
-        if (g0 + p < g1) stage_column(stage + p * 256, col_base(g0 + p), line_stride, warp, lane, n_tiles);
+        if (p < n_cols) {
+            stage_column(stage + p * 256, src + pf * freq_stride + int64_t(pc) * 8, ll);
+            if (++pc == n_theta) { pc = 0; ++pf; }
+        }
         cp_async_commit();
     }
 
+    int f = int(g0 / n_theta), col = int(g0 - int64_t(f) * n_theta);
     int cur_f = -1;
     cplx A[8], M[8], beta = czero();
     int slot = 0;
-    for (int64_t g = g0; g < g1; ++g, slot = (slot + 1 == STAGES) ? 0 : slot + 1) {
-        const int f = int(g / n_theta);
-        const int col = int(g - int64_t(f) * n_theta);
+    for (int it = 0; it < n_cols; ++it) {
         if (f != cur_f) {
             // ---- per-frequency coefficients and scan multipliers
             const FreqDev fd = fdev[f];
@@ -156,7 +191,10 @@ k_depth_scan(const cplx* __restrict__ src, cplx* __restrict__ dst, const cplx* _
 #pragma unroll
             for (int d = 0; d < 5; ++d) {
                 const int o = 1 << d;
-                if (PRECOMP) { mf[d * nthreads + t] = Pf; mb[d * nthreads + t] = Pb; }
+                if (PRECOMP) {
+                    mf[d * nthreads + t] = lane >= o ? Pf : czero();
+                    mb[d * nthreads + t] = lane + o < 32 ? Pb : czero();
+                }
                 const cplx pu = shfl_up(Pf, o), pd = shfl_down(Pb, o);
                 if (lane >= o) Pf = cmul(Pf, pu);
                 if (lane + o < 32) Pb = cmul(Pb, pd);
@@ -166,19 +204,22 @@ k_depth_scan(const cplx* __restrict__ src, cplx* __restrict__ dst, const cplx* _
             __syncthreads();
             cur_f = f;
         }
-        // ---- prefetch g + STAGES - 1, then wait for g
+        // ---- prefetch column it + STAGES - 1, then wait for column it
         {
-            const int64_t gp = g + STAGES - 1;
             const int ps = (slot + STAGES - 1) % STAGES;
-            if (gp < g1) stage_column(stage + ps * 256, col_base(gp), line_stride, warp, lane, n_tiles);
+            if (it + STAGES - 1 < n_cols) {
+                stage_column(stage + ps * 256, src + pf * freq_stride + int64_t(pc) * 8, ll);
+                if (++pc == n_theta) { pc = 0; ++pf; }
+            }
             cp_async_commit();
             cp_async_wait<STAGES - 1>();
             __syncwarp();
         }
         cplx* cur = stage + slot * 256;
+        const int sw = lane & 7;
         cplx x[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) x[i] = cur[lane * 8 + (i ^ (lane & 7))];
+        for (int i = 0; i < 8; ++i) x[i] = cur[lane * 8 + (i ^ sw)];
 
         // ---- halos: last row of the tile above, first row of the tile below
         cplx up = shfl_up(x[7], 1), dn = shfl_down(x[0], 1);
@@ -191,21 +232,25 @@ k_depth_scan(const cplx* __restrict__ src, cplx* __restrict__ dst, const cplx* _
         if (t >= n_tiles - 1) dn = czero();
 
         // ---- b_l = inv_l * rhs_l (ref operators.py:115-121,139,210; marching.py:114)
-        const bool zero_col = sector && (col == 0 || col == n_theta - 1);
         cplx b[8];
+        if (sector && (col == 0 || col == n_theta - 1)) {       // uniform per CTA
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const cplx um = i ? x[i - 1] : up;
-            const cplx upp = i < 7 ? x[i + 1] : dn;
-            const cplx d2 = cadd(csub(upp, crmul(2.0, x[i])), um);
-            b[i] = zero_col ? czero() : cmul(M[i], cfma(A[i], x[i], cmul(beta, d2)));
+            for (int i = 0; i < 8; ++i) b[i] = czero();
+        } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const cplx um = i ? x[i - 1] : up;
+                const cplx upp = i < 7 ? x[i + 1] : dn;
+                const cplx d2 = cadd(csub(upp, cadd(x[i], x[i])), um);
+                b[i] = cmul(M[i], cfma(A[i], x[i], cmul(beta, d2)));
+            }
         }
 
         // ---- forward elimination: local chunk, scan, exact re-run
+        // (inactive threads have m = 0 and x = 0, hence Y = 0)
         cplx Y = czero();
 #pragma unroll
         for (int i = 0; i < 8; ++i) Y = cfma(M[i], Y, b[i]);
-        if (!active) Y = czero();
         cplx Pacc = cone();
         if (!PRECOMP) {
 #pragma unroll
@@ -217,7 +262,7 @@ k_depth_scan(const cplx* __restrict__ src, cplx* __restrict__ dst, const cplx* _
             const int o = 1 << d;
             const cplx Yp = shfl_up(Y, o);
             if (PRECOMP) {
-                if (lane >= o) Y = cfma(mf[d * nthreads + t], Yp, Y);
+                Y = cfma(mf[d * nthreads + t], Yp, Y);
             } else {
                 const cplx Pp = shfl_up(Pacc, o);
                 if (lane >= o) { Y = cfma(Pacc, Yp, Y); Pacc = cmul(Pacc, Pp); }
@@ -236,7 +281,6 @@ k_depth_scan(const cplx* __restrict__ src, cplx* __restrict__ dst, const cplx* _
         cplx X = czero();
 #pragma unroll
         for (int i = 7; i >= 0; --i) X = cfma(M[i], X, b[i]);
-        if (!active) X = czero();
         cplx Qacc = cone();
         if (!PRECOMP) {
 #pragma unroll
@@ -248,7 +292,7 @@ k_depth_scan(const cplx* __restrict__ src, cplx* __restrict__ dst, const cplx* _
             const int o = 1 << d;
             const cplx Xn = shfl_down(X, o);
             if (PRECOMP) {
-                if (lane + o < 32) X = cfma(mb[d * nthreads + t], Xn, X);
+                X = cfma(mb[d * nthreads + t], Xn, X);
             } else {
                 const cplx Qn = shfl_down(Qacc, o);
                 if (lane + o < 32) { X = cfma(Qacc, Xn, X); Qacc = cmul(Qacc, Qn); }
@@ -265,15 +309,12 @@ k_depth_scan(const cplx* __restrict__ src, cplx* __restrict__ dst, const cplx* _
 
         // ---- stage out through the same buffer, full-line stores
 #pragma unroll
-        for (int i = 0; i < 8; ++i) cur[lane * 8 + (i ^ (lane & 7))] = b[i];
+        for (int i = 0; i < 8; ++i) cur[lane * 8 + (i ^ sw)] = b[i];
         __syncwarp();
-        cplx* out_base = dst + (g / n_theta) * n_tiles * line_stride + int64_t(col) * 8;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const int line = 4 * k + (lane >> 3), e = lane & 7, tile = warp * 32 + line;
-            if (tile < n_tiles) stc(out_base + tile * line_stride + e, cur[line * 8 + (e ^ (line & 7))]);
-        }
+        unstage_column(dst + f * freq_stride + int64_t(col) * 8, cur, ll);
         __syncwarp();
+        if (++col == n_theta) { col = 0; ++f; }
+        slot = (slot + 1 == STAGES) ? 0 : slot + 1;
     }
     cp_async_wait<0>();
 }
