@@ -160,7 +160,7 @@ def cpu_sample(name, frequencies, sample_freqs, sample_steps):
                       f"{cores} processes (spawn), wall {wall:.1f} s incl. process start"}
 
 
-CPU_SAMPLES = {"cfg1": (1, 100), "cfg2": (1, 8), "cfg4": (16, 4), "cfg5": (1, 1)}
+CPU_SAMPLES = {"cfg1": (1, 400), "cfg2": (1, 30), "cfg4": (16, 16), "cfg5": (1, 2)}
 
 
 def run_reference_arm(a, rank, world):
