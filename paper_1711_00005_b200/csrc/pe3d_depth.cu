@@ -182,7 +182,8 @@ k_depth_scan(const cplx* __restrict__ src, cplx* __restrict__ dst, const cplx* _
             for (int i = 0; i < 8; ++i) {
                 const cplx lc = active ? ldc(loc_tab + f * nz8 + 8 * t + i) : czero();
                 M[i] = active ? ldc(mul_tab + f * nz8 + 8 * t + i) : czero();
-                A[i] = cmul(kappa, cadd(cone(), cmul(fd.cx_rhs, lc)));
+                // A'_l = kappa (1 + cx_rhs local_l) - 2 beta  (the -2x of d2 folded in)
+                A[i] = csub(cmul(kappa, cadd(cone(), cmul(fd.cx_rhs, lc))), cadd(beta, beta));
                 P = cmul(M[i], P);
             }
             if (!active) P = cone();
@@ -231,7 +232,8 @@ k_depth_scan(const cplx* __restrict__ src, cplx* __restrict__ dst, const cplx* _
         if (t == 0) up = czero();
         if (t >= n_tiles - 1) dn = czero();
 
-        // ---- b_l = inv_l * rhs_l (ref operators.py:115-121,139,210; marching.py:114)
+        // ---- r'_l = kappa rhs_l = A'_l x_l + beta (x_{l+1} + x_{l-1})
+        //      (ref operators.py:115-121,139,210; marching.py:114: row 0 has m_0 = 0)
         cplx b[8];
         if (sector && (col == 0 || col == n_theta - 1)) {       // uniform per CTA
 #pragma unroll
@@ -241,16 +243,15 @@ k_depth_scan(const cplx* __restrict__ src, cplx* __restrict__ dst, const cplx* _
             for (int i = 0; i < 8; ++i) {
                 const cplx um = i ? x[i - 1] : up;
                 const cplx upp = i < 7 ? x[i + 1] : dn;
-                const cplx d2 = cadd(csub(upp, cadd(x[i], x[i])), um);
-                b[i] = cmul(M[i], cfma(A[i], x[i], cmul(beta, d2)));
+                b[i] = cfma(A[i], x[i], cmul(beta, cadd(upp, um)));
             }
         }
 
-        // ---- forward elimination: local chunk, scan, exact re-run
+        // ---- forward elimination y_l = m_l (r'_l + y_{l-1}): local chunk, scan, exact re-run
         // (inactive threads have m = 0 and x = 0, hence Y = 0)
         cplx Y = czero();
 #pragma unroll
-        for (int i = 0; i < 8; ++i) Y = cfma(M[i], Y, b[i]);
+        for (int i = 0; i < 8; ++i) Y = cmul(M[i], cadd(b[i], Y));
         cplx Pacc = cone();
         if (!PRECOMP) {
 #pragma unroll
@@ -275,7 +276,7 @@ k_depth_scan(const cplx* __restrict__ src, cplx* __restrict__ dst, const cplx* _
         cplx y = shfl_up(cfma(PRECOMP ? pincf[t] : Pacc, C, Y), 1);
         if (lane == 0) y = C;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) { y = cfma(M[i], y, b[i]); b[i] = y; }
+        for (int i = 0; i < 8; ++i) { y = cmul(M[i], cadd(b[i], y)); b[i] = y; }
 
         // ---- back substitution
         cplx X = czero();

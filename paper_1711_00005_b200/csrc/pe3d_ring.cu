@@ -19,6 +19,8 @@
 #include "pe3d_device.cuh"
 #include "pe3d_internal.h"
 
+#include <cstdlib>
+
 namespace pe3d {
 
 // Circulant factorisation of B = diag*I + off*(S + S^-1):
@@ -100,151 +102,220 @@ __global__ void k_ring_setup(cplx* __restrict__ table, const FreqDev* __restrict
     T[3] = mk(rf.diagonal ? 1.0 : 0.0, 0.0);
 }
 
-// Given u on this thread's azimuth chunk of one depth row, write the TL
+// Given u on this thread's azimuth chunk of RT depth rows, write the TL
 // sample / snapshot / final slab if requested and the next step's
 // temp = u + cy_rhs * s_theta * d2_theta(u)  (ref operators.py:105-122,
 // 142-153, 207-208; periodic roll order or sector zero-exterior order).
-template <int L>
-__device__ __forceinline__ void ring_epilogue(cplx (&u)[L], int q, int n_chunks, int nvalid, int i, int rw,
-                                              int m0, int l, const EpilogueArgs& ea, int f, int n_theta,
-                                              int n_depth, cplx cy_rhs, double s_theta, cplx* sFirst,
-                                              cplx* sLast, cplx* dst_row /* blocked, element (m) at m*8 */,
-                                              bool in_range) {
+// Row h of this thread is row-in-group r_h = i + h*RWT of the CTA's RW rows;
+// its device-tile element (m) is at dst_tile[m*8 + r_h + row0].
+template <int L, int RT>
+__device__ __forceinline__ void ring_epilogue(cplx (&u)[RT][L], int q, int n_chunks, int nvalid, int i, int RWT,
+                                              int RW, int m0, int row0, int l0, const EpilogueArgs& ea, int f,
+                                              int n_theta, int n_depth, cplx scale, cplx cy_rhs, double s_theta,
+                                              cplx* sFirst, cplx* sLast, cplx* dst_tile, bool in_range) {
+    // u holds x with the field = scale * x.  temp = field + cy_rhs s (x+ + x- - 2x) scale
+    //   = b1 x + b2 (x+ + x-),  b1 = scale (1 - 2 alpha),  b2 = scale alpha,  alpha = cy_rhs s
+    const cplx alpha = crmul(s_theta, cy_rhs);
+    const cplx b2 = cmul(scale, alpha);
+    const cplx b1 = csub(scale, cadd(b2, b2));
     const bool periodic = ea.periodic;
     if (in_range) {
-        sFirst[q * rw + i] = u[0];
-        if (nvalid == L) {
-            sLast[q * rw + i] = u[L - 1];
-        } else {
-            // partial (last) chunk: predicated stores, the last one wins (a
-            // select on u[nvalid-1] would demote u[] to local memory)
 #pragma unroll
-            for (int k = 0; k < L - 1; ++k)
-                if (k < nvalid) sLast[q * rw + i] = u[k];
+        for (int h = 0; h < RT; ++h) {
+            const int r = i + h * RWT;
+            sFirst[q * RW + r] = u[h][0];
+            if (nvalid == L) {
+                sLast[q * RW + r] = u[h][L - 1];
+            } else {
+                // partial (last) chunk: predicated stores, the last one wins (a
+                // select on u[nvalid-1] would demote u[] to local memory)
+#pragma unroll
+                for (int k = 0; k < L - 1; ++k)
+                    if (k < nvalid) sLast[q * RW + r] = u[h][k];
+            }
         }
     }
     __syncthreads();
     if (!in_range) return;
-    cplx prev, next;
-    if (q > 0) prev = sLast[(q - 1) * rw + i];
-    else prev = periodic ? sLast[(n_chunks - 1) * rw + i] : czero();
-    if (q < n_chunks - 1) next = sFirst[(q + 1) * rw + i];
-    else next = periodic ? sFirst[i] : czero();
+#pragma unroll
+    for (int h = 0; h < RT; ++h) {
+        const int r = i + h * RWT;
+        const int l = l0 + r;
+        cplx prev, next;
+        if (q > 0) prev = sLast[(q - 1) * RW + r];
+        else prev = periodic ? sLast[(n_chunks - 1) * RW + r] : czero();
+        if (q < n_chunks - 1) next = sFirst[(q + 1) * RW + r];
+        else next = periodic ? sFirst[r] : czero();
 
-    const bool real_row = l < n_depth;
-    // TL / snapshots / final slab in the reference layout [..][m][l]
-    if (real_row && (ea.tl || ea.snap || ea.final_out)) {
-        long long zeros = 0;
+        // TL / snapshots / final slab in the reference layout [..][m][l]
+        if (l < n_depth && (ea.tl || ea.snap || ea.final_out)) {
+            long long zeros = 0;
+#pragma unroll
+            for (int k = 0; k < L; ++k) {
+                if (k >= nvalid) break;
+                const int m = m0 + k;
+                const int64_t o = (int64_t(f) * n_theta + m) * n_depth + l;
+                const int64_t so = (int64_t(f) * ea.n_samples + ea.sample) * n_theta * n_depth + (int64_t(m) * n_depth + l);
+                const cplx uf = cmul(scale, u[h][k]);
+                if (ea.tl) {
+                    const double mag = cabs(uf) * ea.w_abs[f];
+                    const double tl = (mag == 0.0) ? TL_FLOOR_DB : -20.0 * log10(mag);
+                    if (mag == 0.0) ++zeros;
+                    ea.tl[so] = tl;
+                }
+                if (ea.snap) stc(ea.snap + so, uf);
+                if (ea.final_out) stc(ea.final_out + o, uf);
+            }
+            if (ea.tl && zeros) atomicAdd(reinterpret_cast<unsigned long long*>(ea.clamped + f), (unsigned long long)zeros);
+        }
+        if (!ea.write_temp) continue;
+        // next step's azimuth factor (zero exterior on a sector ring: prev/next = 0)
+        cplx* dst_row = dst_tile + row0 + r;
 #pragma unroll
         for (int k = 0; k < L; ++k) {
             if (k >= nvalid) break;
-            const int m = m0 + k;
-            const int64_t o = (int64_t(f) * n_theta + m) * n_depth + l;
-            if (ea.tl) {
-                const double mag = cabs(u[k]) * ea.w_abs[f];
-                const double tl = (mag == 0.0) ? TL_FLOOR_DB : -20.0 * log10(mag);
-                if (mag == 0.0) ++zeros;
-                ea.tl[(int64_t(f) * ea.n_samples + ea.sample) * n_theta * n_depth + (int64_t(m) * n_depth + l)] = tl;
-            }
-            if (ea.snap) stc(ea.snap + (int64_t(f) * ea.n_samples + ea.sample) * n_theta * n_depth + (int64_t(m) * n_depth + l), u[k]);
-            if (ea.final_out) stc(ea.final_out + o, u[k]);
+            const cplx um = k ? u[h][k - 1] : prev;
+            const cplx up = (k + 1 < L && k < nvalid - 1) ? u[h][(k + 1) % L] : next;
+            stc_stream(dst_row + int64_t(m0 + k) * 8, cfma(b1, u[h][k], cmul(b2, cadd(up, um))));
         }
-        if (ea.tl && zeros) atomicAdd(reinterpret_cast<unsigned long long*>(ea.clamped + f), (unsigned long long)zeros);
-    }
-    if (!ea.write_temp) return;
-    // next step's azimuth factor
-#pragma unroll
-    for (int k = 0; k < L; ++k) {
-        if (k >= nvalid) break;
-        const cplx um = k ? u[k - 1] : prev;
-        const cplx up = (k + 1 < L && k < nvalid - 1) ? u[(k + 1) % L] : next;
-        cplx d2;
-        if (periodic) {
-            d2 = csub(cadd(up, um), crmul(2.0, u[k]));
-        } else {
-            const int m = m0 + k;
-            if (m == 0) d2 = csub(up, crmul(2.0, u[k]));
-            else if (m == n_theta - 1) d2 = csub(um, crmul(2.0, u[k]));
-            else d2 = cadd(csub(up, crmul(2.0, u[k])), um);
-        }
-        const cplx yu = crmul(s_theta, d2);
-        stc_stream(dst_row + int64_t(m0 + k) * 8, cadd(u[k], cmul(cy_rhs, yu)));
     }
 }
 
-// Solve B u = v for this thread's chunk (registers), given the ring table
-// in shared memory.  Thread t = i + RW*q: row i of the CTA's row group,
-// chunk q.  Only the last chunk may be partial; the scans never apply a
+// Solve B u = v for this thread's chunk of RT rows (registers), given the
+// ring table T in shared memory.  Thread t = i + RWT*q (RWT = RW/RT lane
+// slots per chunk) holds rows i + h*RWT of the CTA's RW rows, chunk q.  The
+// RT rows are independent systems interleaved for instruction-level
+// parallelism.  Only the last chunk may be partial; the scans never apply a
 // multiplier across it to a non-zero value.  Contains
 // three __syncthreads (uniform).
-template <int L, int RW>
-__device__ __forceinline__ void ring_solve(cplx (&v)[L], const cplx* __restrict__ T, int q, int i, int lane, int warp,
-                                           int nwarps, int n_theta, int nvalid, cplx* sW, cplx* sV, cplx* sTot) {
-    constexpr int G = 32 / RW;
-    const int qw = lane / RW;
+template <int L, int RW, int RT, bool FULL>
+__device__ __forceinline__ void ring_solve(cplx (&v)[RT][L], const cplx* __restrict__ T, int q, int i, int lane,
+                                           int warp, int nwarps, int n_theta, int nvalid_, cplx* sW, cplx* sV,
+                                           cplx* sTot) {
+    const int nvalid = FULL ? L : nvalid_;
+    constexpr int RWT = RW / RT;
+    constexpr int G = 32 / RWT;                      // chunks per warp
+    const int qw = lane / RWT;
     const int n_chunks = (n_theta + L - 1) / L;
     const int q_last = n_chunks - 1;
     const int nv_last = n_theta - q_last * L;
     const int n_qp = (n_chunks > G ? n_chunks : G) + 1;
     const cplx* pw = T + 4;
     const cplx* qp = pw + L + 1;
-    const cplx rho = T[0], scale = T[1], inv_wrap = T[2];
-    if (T[3].re != 0.0) {             // off == 0: B = diag * I (uniform branch)
-#pragma unroll
-        for (int k = 0; k < L; ++k) v[k] = cmul(v[k], scale);
+    const cplx rho = T[0], inv_wrap = T[2];
+    if (T[3].re != 0.0) {             // off == 0: B = diag * I, x = v (the scale is applied by the epilogue)
         __syncthreads();
         __syncthreads();
         __syncthreads();
         return;
     }
     // ---- forward cyclic recurrence w_m = v_m + rho w_{m-1}
-    cplx Y = czero();
+    cplx Y[RT], Yloc[RT];
 #pragma unroll
-    for (int k = 0; k < L; ++k) if (k < nvalid) { Y = cfma(rho, Y, v[k]); v[k] = Y; }
-    const cplx Yloc = Y;
+    for (int h = 0; h < RT; ++h) Y[h] = czero();
+    if (FULL || nvalid == L) {
+#pragma unroll
+        for (int k = 0; k < L; ++k)
+#pragma unroll
+            for (int h = 0; h < RT; ++h) { Y[h] = cfma(rho, Y[h], v[h][k]); v[h][k] = Y[h]; }
+    } else {
+#pragma unroll
+        for (int k = 0; k < L; ++k)
+            if (k < nvalid)
+#pragma unroll
+                for (int h = 0; h < RT; ++h) { Y[h] = cfma(rho, Y[h], v[h][k]); v[h][k] = Y[h]; }
+    }
+#pragma unroll
+    for (int h = 0; h < RT; ++h) Yloc[h] = Y[h];
 #pragma unroll
     for (int d = 1; d < G; d <<= 1) {
-        const cplx Yp = shfl_up(Y, d * RW);
-        if (qw >= d) Y = cfma(qp[d], Yp, Y);
-    }
-    cplx ex = shfl_up(Y, RW);
-    if (qw == 0) ex = czero();
-    if (qw == G - 1) sW[warp * RW + i] = Y;
-    __syncthreads();
-    cplx C = czero();
-    for (int w = 0; w < warp; ++w) C = cfma(qp[G], C, sW[w * RW + i]);
-    const cplx Yex = cfma(qp[qw], C, ex);                       // w entering chunk q (non-cyclic)
-    if (q == q_last) sTot[i] = cfma(pw[nv_last], Yex, Yloc);    // w at m = N-1 (non-cyclic)
-    __syncthreads();
-    const cplx w_last = cmul(sTot[i], inv_wrap);
-    const cplx c_in = cfma(qp[q < n_qp ? q : 0], w_last, Yex);
+        const cplx m = (qw >= d) ? qp[d] : czero();
 #pragma unroll
-    for (int k = 0; k < L; ++k) if (k < nvalid) v[k] = cfma(pw[k + 1], c_in, v[k]);
+        for (int h = 0; h < RT; ++h) Y[h] = cfma(m, shfl_up(Y[h], d * RWT), Y[h]);
+    }
+    cplx ex[RT];
+#pragma unroll
+    for (int h = 0; h < RT; ++h) {
+        ex[h] = shfl_up(Y[h], RWT);
+        if (qw == 0) ex[h] = czero();
+        if (qw == G - 1) sW[warp * RW + i + h * RWT] = Y[h];
+    }
+    __syncthreads();
+    cplx C[RT];
+#pragma unroll
+    for (int h = 0; h < RT; ++h) C[h] = czero();
+    for (int w = 0; w < warp; ++w)
+#pragma unroll
+        for (int h = 0; h < RT; ++h) C[h] = cfma(qp[G], C[h], sW[w * RW + i + h * RWT]);
+    cplx Yex[RT];
+#pragma unroll
+    for (int h = 0; h < RT; ++h) {
+        Yex[h] = cfma(qp[qw], C[h], ex[h]);                                       // w entering chunk q
+        if (q == q_last) sTot[i + h * RWT] = cfma(pw[nv_last], Yex[h], Yloc[h]);  // w at m = N-1 (non-cyclic)
+    }
+    __syncthreads();
+    const cplx qpq = qp[q < n_qp ? q : 0];
+#pragma unroll
+    for (int h = 0; h < RT; ++h) {
+        const cplx c_in = cfma(qpq, cmul(sTot[i + h * RWT], inv_wrap), Yex[h]);
+#pragma unroll
+        for (int k = 0; k < L; ++k) if (k < nvalid) v[h][k] = cfma(pw[k + 1], c_in, v[h][k]);
+    }
 
     // ---- backward cyclic recurrence x_m = w_m + rho x_{m+1}
-    cplx X = czero();
+    cplx X[RT];
 #pragma unroll
-    for (int k = L - 1; k >= 0; --k) if (k < nvalid) { X = cfma(rho, X, v[k]); v[k] = X; }
+    for (int h = 0; h < RT; ++h) X[h] = czero();
+    if (FULL || nvalid == L) {
+#pragma unroll
+        for (int k = L - 1; k >= 0; --k)
+#pragma unroll
+            for (int h = 0; h < RT; ++h) { X[h] = cfma(rho, X[h], v[h][k]); v[h][k] = X[h]; }
+    } else {
+#pragma unroll
+        for (int k = L - 1; k >= 0; --k)
+            if (k < nvalid)
+#pragma unroll
+                for (int h = 0; h < RT; ++h) { X[h] = cfma(rho, X[h], v[h][k]); v[h][k] = X[h]; }
+    }
+    if (q >= n_chunks) {              // idle lanes (FULL mode runs them unpredicated) contribute nothing
+#pragma unroll
+        for (int h = 0; h < RT; ++h) X[h] = czero();
+    }
 #pragma unroll
     for (int d = 1; d < G; d <<= 1) {
-        const cplx Xn = shfl_down(X, d * RW);
-        if (qw + d < G) X = cfma(qp[d], Xn, X);
-    }
-    const cplx nx = shfl_down(X, RW);
-    if (qw == 0) sV[warp * RW + i] = X;
-    __syncthreads();
-    cplx D = czero();
-    for (int w = nwarps - 1; w > warp; --w) D = cfma(qp[G], D, sV[w * RW + i]);
-    if (q == 0) sTot[RW + i] = cfma(qp[G], D, X);                 // S_0
-    const cplx S_next = (qw == G - 1) ? D : cfma(qp[G - qw - 1], D, nx);
-    __syncthreads();
-    const cplx x0 = cmul(sTot[RW + i], inv_wrap);
-    cplx c_up;
-    if (q >= q_last) c_up = x0;
-    else c_up = cfma(cmul(qp[q_last - q - 1], pw[nv_last]), x0, S_next);
-    const cplx cs = cmul(scale, c_up);
+        const cplx m = (qw + d < G) ? qp[d] : czero();
 #pragma unroll
-    for (int k = 0; k < L; ++k) if (k < nvalid) v[k] = cfma(pw[nvalid - k], cs, cmul(scale, v[k]));
+        for (int h = 0; h < RT; ++h) X[h] = cfma(m, shfl_down(X[h], d * RWT), X[h]);
+    }
+    cplx nx[RT];
+#pragma unroll
+    for (int h = 0; h < RT; ++h) {
+        nx[h] = shfl_down(X[h], RWT);
+        if (qw == 0) sV[warp * RW + i + h * RWT] = X[h];
+    }
+    __syncthreads();
+    cplx D[RT];
+#pragma unroll
+    for (int h = 0; h < RT; ++h) D[h] = czero();
+    for (int w = nwarps - 1; w > warp; --w)
+#pragma unroll
+        for (int h = 0; h < RT; ++h) D[h] = cfma(qp[G], D[h], sV[w * RW + i + h * RWT]);
+    cplx S_next[RT];
+#pragma unroll
+    for (int h = 0; h < RT; ++h) {
+        if (q == 0) sTot[RW + i + h * RWT] = cfma(qp[G], D[h], X[h]);           // S_0
+        S_next[h] = (qw == G - 1) ? D[h] : cfma(qp[G - qw - 1], D[h], nx[h]);
+    }
+    __syncthreads();
+    const cplx up_mult = (q >= q_last) ? czero() : cmul(qp[q_last - q - 1], pw[nv_last]);
+#pragma unroll
+    for (int h = 0; h < RT; ++h) {
+        const cplx x0 = cmul(sTot[RW + i + h * RWT], inv_wrap);
+        const cplx c_up = (q >= q_last) ? x0 : cfma(up_mult, x0, S_next[h]);
+#pragma unroll
+        for (int k = 0; k < L; ++k) if (k < nvalid) v[h][k] = cfma(pw[nvalid - k], c_up, v[h][k]);
+    }
 }
 
 template <int L, int RW>
@@ -266,46 +337,51 @@ struct RingSmem {
 };
 
 // Persistent, pipelined azimuth sweep for rings whose 8-row tile fits a
-// shared-memory stage (RW = 8).  Work items are (frequency, depth tile);
-// each thread cp.asyncs its own chunk of item n+STAGES-1 while item n is
-// solved, so no CTA barrier is needed for the staged data.
-template <int L, int STAGES>
-__global__ void __launch_bounds__(512, 1)
+// shared-memory stage.  Work items are (frequency, depth tile); each thread
+// cp.asyncs its own RT x L points of item n+STAGES-1 while item n is solved,
+// so no CTA barrier is needed for the staged data.  Stage slot of (m, r):
+// m*8 + (r ^ 4*((m/L)&1)), conflict free for the thread-own reads.
+template <int L, int STAGES, int RT, bool FULL>
+__global__ void __launch_bounds__(256, 2)
 k_azimuth_pipe(const cplx* __restrict__ src, cplx* __restrict__ dst, const cplx* __restrict__ table, int E,
                const FreqDev* __restrict__ fdev, int n_theta, int n_tiles, int n_depth, int64_t total_items,
                int items_per_cta, double r_new, double delta_theta, EpilogueArgs ea) {
-    constexpr int RW = 8;
+    constexpr int RW = 8, RWT = RW / RT;
     extern __shared__ cplx smem[];
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nwarps = blockDim.x >> 5;
-    const int i = t % RW, q = t / RW;
+    const int i = t % RWT, q = t / RWT;
     const int n_chunks = (n_theta + L - 1) / L;
     const bool in_range = q < n_chunks;
     const RingSmem<L, RW> lay(n_theta, blockDim.x, E, STAGES);
     cplx* T = smem + lay.table;
     const int m0 = q * L;
-    const int nvalid = in_range ? min(L, n_theta - m0) : 0;
+    const int nvalid = FULL ? (in_range ? L : 0) : (in_range ? min(L, n_theta - m0) : 0);
+    const int swz = 4 * (q & 1);
     const int64_t ring = int64_t(n_theta) * 8;      // elements per (f, tile) item
 
     const int64_t it0 = int64_t(blockIdx.x) * items_per_cta;
     const int64_t it1 = it0 + items_per_cta < total_items ? it0 + items_per_cta : total_items;
     if (it0 >= it1) return;
     auto fetch = [&](int64_t item, int st) {
-        const cplx* g = src + item * ring + i;
-        cplx* d = smem + st * RW * n_theta + i;
+        const cplx* g = src + item * ring;
+        cplx* d = smem + st * RW * n_theta;
 #pragma unroll
-        for (int k = 0; k < L; ++k)
-            if (k < nvalid) cp_async16(d + (m0 + k) * RW, g + int64_t(m0 + k) * 8);
+        for (int h = 0; h < RT; ++h) {
+            const int r = i + h * RWT;
+#pragma unroll
+            for (int k = 0; k < L; ++k)
+                if (k < nvalid) cp_async16(d + (m0 + k) * 8 + (r ^ swz), g + int64_t(m0 + k) * 8 + r);
+        }
     };
 #pragma unroll
     for (int p = 0; p < STAGES - 1; ++p) {
         if (it0 + p < it1) fetch(it0 + p, p);
         cp_async_commit();
     }
+    int f = int(it0 / n_tiles), tile = int(it0 - int64_t(f) * n_tiles);
     int cur_f = -1;
     int slot = 0;
-    for (int64_t item = it0; item < it1; ++item, slot = (slot + 1 == STAGES) ? 0 : slot + 1) {
-        const int f = int(item / n_tiles);
-        const int tile = int(item - int64_t(f) * n_tiles);
+    for (int64_t item = it0; item < it1; ++item) {
         if (f != cur_f) {
             __syncthreads();
             for (int e = t; e < E; e += blockDim.x) T[e] = table[int64_t(f) * E + e];
@@ -318,21 +394,219 @@ k_azimuth_pipe(const cplx* __restrict__ src, cplx* __restrict__ dst, const cplx*
             cp_async_commit();
             cp_async_wait<STAGES - 1>();
         }
-        cplx v[L];
-        const cplx* stg = smem + slot * RW * n_theta + i;
+        cplx v[RT][L];
+        const cplx* stg = smem + slot * RW * n_theta;
 #pragma unroll
-        for (int k = 0; k < L; ++k) v[k] = (k < nvalid) ? stg[(m0 + k) * RW] : czero();
-        ring_solve<L, RW>(v, T, q, i, lane, warp, nwarps, n_theta, nvalid, smem + lay.sW, smem + lay.sV,
-                          smem + lay.sTot);
-        const int l = tile * 8 + i;
-        if (l == 0 || l >= n_depth) {
+        for (int h = 0; h < RT; ++h)
 #pragma unroll
-            for (int k = 0; k < L; ++k) v[k] = czero();
+            for (int k = 0; k < L; ++k)
+                v[h][k] = (k < nvalid) ? stg[(m0 + k) * 8 + ((i + h * RWT) ^ swz)] : czero();
+        // FULL: every chunk has L points; idle threads (q >= n_chunks) carry zeros
+        ring_solve<L, RW, RT, FULL>(v, T, q, i, lane, warp, nwarps, n_theta, nvalid, smem + lay.sW,
+                                    smem + lay.sV, smem + lay.sTot);
+        const int l0 = tile * 8;
+#pragma unroll
+        for (int h = 0; h < RT; ++h) {
+            const int l = l0 + i + h * RWT;
+            if (l == 0 || l >= n_depth) {
+#pragma unroll
+                for (int k = 0; k < L; ++k) v[h][k] = czero();
+            }
         }
         const FreqDev fd = fdev[f];
-        ring_epilogue<L>(v, q, n_chunks, nvalid, i, RW, m0, l, ea, f, n_theta, n_depth, fd.cy_rhs,
-                         azimuth_scale(fd.k0, r_new, delta_theta), smem + lay.sFirst, smem + lay.sLast,
-                         dst + item * ring + i, in_range);
+        ring_epilogue<L, RT>(v, q, n_chunks, nvalid, i, RWT, RW, m0, 0, l0, ea, f, n_theta, n_depth, T[1],
+                             fd.cy_rhs, azimuth_scale(fd.k0, r_new, delta_theta), smem + lay.sFirst,
+                             smem + lay.sLast, dst + item * ring, in_range);
+        if (++tile == n_tiles) { tile = 0; ++f; }
+        slot = (slot + 1 == STAGES) ? 0 : slot + 1;
+    }
+    cp_async_wait<0>();
+}
+
+
+// ------------------------------------------- ring-per-warp azimuth sweep
+// For rings of 32*L points (L = 2..16): one warp solves whole rings, lane q
+// holding chunk q (L points) of RT rows.  All chaining is done with warp
+// shuffles -- the forward/backward scans (5 levels, multipliers R^d with
+// R = rho^L), the cyclic wrap (lane 31 / lane 0 broadcasts) and the
+// epilogue's azimuth neighbours -- so the solve itself needs no shared
+// memory and no barrier.  The CTA's 8/RT warps cover the 8 rows of a depth
+// tile; the tile (one contiguous 32*L*128-B block) is moved with full-line
+// coalesced cp.async / stores through a stage whose slot for (m, r) is
+// m*8 + (r ^ ((m/L) & 7)): conflict free both for the line-wise copies and
+// for the lane-per-chunk reads.
+template <int L>
+__device__ __forceinline__ int ring_slot(int m, int r) { return m * 8 + (r ^ ((m / L) & 7)); }
+
+template <int L, int RT, int STAGES>
+__global__ void __launch_bounds__(32 * 8 / RT)
+k_azimuth_warp(const cplx* __restrict__ src, cplx* __restrict__ dst, const cplx* __restrict__ table, int E,
+               const FreqDev* __restrict__ fdev, int n_tiles, int n_depth, int64_t total_items, int items_per_cta,
+               double r_new, double delta_theta, EpilogueArgs ea) {
+    constexpr int NT = 32 * L;                      // ring length
+    constexpr int ITEM = NT * 8;                    // elements per (f, tile) item
+    constexpr int NTHR = 32 * 8 / RT;
+    constexpr int PER = ITEM / NTHR;                // 16-B chunks per thread per item
+    extern __shared__ cplx smem[];
+    cplx* T = smem + STAGES * ITEM;                 // ring table of the current frequency
+    const cplx* pw = T + 4;                         // rho^k, k = 0..L
+    const cplx* qp = pw + L + 1;                    // R^j, j = 0..32
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int q = lane, swz = q & 7;
+    const int m0 = q * L;
+
+    const int64_t it0 = int64_t(blockIdx.x) * items_per_cta;
+    const int64_t it1 = it0 + items_per_cta < total_items ? it0 + items_per_cta : total_items;
+    if (it0 >= it1) return;
+    auto fetch = [&](int64_t item, int st) {
+        const cplx* g = src + item * ITEM;
+        cplx* d = smem + st * ITEM;
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const int e = j * NTHR + tid;
+            cp_async16(d + ring_slot<L>(e >> 3, e & 7), g + e);
+        }
+    };
+#pragma unroll
+    for (int p = 0; p < STAGES - 1; ++p) {
+        if (it0 + p < it1) fetch(it0 + p, p);
+        cp_async_commit();
+    }
+    int f = int(it0 / n_tiles), tile = int(it0 - int64_t(f) * n_tiles);
+    int cur_f = -1;
+    int slot = 0;
+    cplx rho = czero(), inv_wrap = czero(), scale = czero(), b1 = czero(), b2 = czero();
+    bool diagonal = false;
+    for (int64_t item = it0; item < it1; ++item) {
+        __syncthreads();                            // previous item's stage fully stored
+        if (f != cur_f) {
+            for (int e = tid; e < E; e += NTHR) T[e] = table[int64_t(f) * E + e];
+            __syncthreads();
+            cur_f = f;
+            rho = T[0];
+            scale = T[1];
+            inv_wrap = T[2];
+            diagonal = T[3].re != 0.0;
+            const FreqDev fd = fdev[f];
+            const cplx alpha = crmul(azimuth_scale(fd.k0, r_new, delta_theta), fd.cy_rhs);
+            b2 = cmul(scale, alpha);
+            b1 = csub(scale, cadd(b2, b2));
+        }
+        {
+            const int64_t ip = item + STAGES - 1;
+            if (ip < it1) fetch(ip, (slot + STAGES - 1) % STAGES);
+            cp_async_commit();
+            cp_async_wait<STAGES - 1>();
+        }
+        __syncthreads();                            // item's lines visible to every warp
+        cplx* stg = smem + slot * ITEM;
+        cplx v[RT][L];
+#pragma unroll
+        for (int h = 0; h < RT; ++h)
+#pragma unroll
+            for (int k = 0; k < L; ++k) v[h][k] = stg[(m0 + k) * 8 + ((warp * RT + h) ^ swz)];
+
+        if (!diagonal) {
+            // ---- forward cyclic recurrence w_m = v_m + rho w_{m-1}
+            cplx Y[RT];
+#pragma unroll
+            for (int h = 0; h < RT; ++h) {
+                Y[h] = czero();
+#pragma unroll
+                for (int k = 0; k < L; ++k) { Y[h] = cfma(rho, Y[h], v[h][k]); v[h][k] = Y[h]; }
+            }
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const cplx m = lane >= d ? qp[d] : czero();
+#pragma unroll
+                for (int h = 0; h < RT; ++h) Y[h] = cfma(m, shfl_up(Y[h], d), Y[h]);
+            }
+            const cplx qpq = qp[q];
+#pragma unroll
+            for (int h = 0; h < RT; ++h) {
+                cplx ex = shfl_up(Y[h], 1);
+                if (lane == 0) ex = czero();
+                const cplx w_last = cmul(shfl_idx(Y[h], 31), inv_wrap);   // cyclic closure
+                const cplx c_in = cfma(qpq, w_last, ex);
+#pragma unroll
+                for (int k = 0; k < L; ++k) v[h][k] = cfma(pw[k + 1], c_in, v[h][k]);
+            }
+            // ---- backward cyclic recurrence x_m = w_m + rho x_{m+1}
+            cplx X[RT];
+#pragma unroll
+            for (int h = 0; h < RT; ++h) {
+                X[h] = czero();
+#pragma unroll
+                for (int k = L - 1; k >= 0; --k) { X[h] = cfma(rho, X[h], v[h][k]); v[h][k] = X[h]; }
+            }
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const cplx m = lane + d < 32 ? qp[d] : czero();
+#pragma unroll
+                for (int h = 0; h < RT; ++h) X[h] = cfma(m, shfl_down(X[h], d), X[h]);
+            }
+            const cplx qup = qp[31 - q];
+#pragma unroll
+            for (int h = 0; h < RT; ++h) {
+                cplx nx = shfl_down(X[h], 1);
+                if (lane == 31) nx = czero();
+                const cplx x0 = cmul(shfl_idx(X[h], 0), inv_wrap);       // cyclic closure
+                const cplx c_up = cfma(qup, x0, nx);
+#pragma unroll
+                for (int k = 0; k < L; ++k) v[h][k] = cfma(pw[L - k], c_up, v[h][k]);
+            }
+        }
+        // ---- boundary (surface and pad rows), TL / snapshot / final, next temp
+        const int l0 = tile * 8 + warp * RT;
+#pragma unroll
+        for (int h = 0; h < RT; ++h) {
+            const int l = l0 + h;
+            if (l == 0 || l >= n_depth) {
+#pragma unroll
+                for (int k = 0; k < L; ++k) v[h][k] = czero();
+            }
+            if (l < n_depth && (ea.tl || ea.snap || ea.final_out)) {
+                long long zeros = 0;
+#pragma unroll
+                for (int k = 0; k < L; ++k) {
+                    const int m = m0 + k;
+                    const cplx uf = cmul(scale, v[h][k]);
+                    const int64_t so = (int64_t(f) * ea.n_samples + ea.sample) * NT * n_depth + (int64_t(m) * n_depth + l);
+                    if (ea.tl) {
+                        const double mag = cabs(uf) * ea.w_abs[f];
+                        if (mag == 0.0) ++zeros;
+                        ea.tl[so] = (mag == 0.0) ? TL_FLOOR_DB : -20.0 * log10(mag);
+                    }
+                    if (ea.snap) stc(ea.snap + so, uf);
+                    if (ea.final_out) stc(ea.final_out + (int64_t(f) * NT + m) * n_depth + l, uf);
+                }
+                if (ea.tl && zeros) atomicAdd(reinterpret_cast<unsigned long long*>(ea.clamped + f), (unsigned long long)zeros);
+            }
+            if (ea.write_temp) {
+                cplx prev = shfl_up(v[h][L - 1], 1), next = shfl_down(v[h][0], 1);
+                const cplx wrap_prev = shfl_idx(v[h][L - 1], 31), wrap_next = shfl_idx(v[h][0], 0);
+                if (lane == 0) prev = wrap_prev;
+                if (lane == 31) next = wrap_next;
+                const int r = (warp * RT + h) ^ swz;
+#pragma unroll
+                for (int k = 0; k < L; ++k) {
+                    const cplx um = k ? v[h][k - 1] : prev;
+                    const cplx up = (k + 1 < L) ? v[h][(k + 1) % L] : next;
+                    stg[(m0 + k) * 8 + r] = cfma(b1, v[h][k], cmul(b2, cadd(up, um)));   // own slots only
+                }
+            }
+        }
+        if (ea.write_temp) {
+            __syncthreads();                        // every warp's rows written
+            cplx* g = dst + item * ITEM;
+#pragma unroll
+            for (int j = 0; j < PER; ++j) {
+                const int e = j * NTHR + tid;
+                stc_stream(g + e, stg[ring_slot<L>(e >> 3, e & 7)]);
+            }
+        }
+        if (++tile == n_tiles) { tile = 0; ++f; }
+        slot = (slot + 1 == STAGES) ? 0 : slot + 1;
     }
     cp_async_wait<0>();
 }
@@ -352,27 +626,29 @@ k_azimuth_direct(const cplx* __restrict__ src, cplx* __restrict__ dst, const cpl
     const RingSmem<L, RW> lay(n_theta, blockDim.x, E, 0);
     const int groups = 8 / RW;
     const int tile = blockIdx.x / groups;
-    const int l = tile * 8 + (blockIdx.x % groups) * RW + i;
+    const int row0 = (blockIdx.x % groups) * RW;
     const int f = blockIdx.y;
     const int m0 = q * L;
     const int nvalid = in_range ? min(L, n_theta - m0) : 0;
-    const int64_t row_base = (int64_t(f) * n_tiles + tile) * n_theta * 8 + (l & 7);
-    cplx v[L];
+    cplx* tile_base = dst + (int64_t(f) * n_tiles + tile) * n_theta * 8;
+    const cplx* src_tile = src + (int64_t(f) * n_tiles + tile) * n_theta * 8 + row0 + i;
+    cplx v[1][L];
 #pragma unroll
-    for (int k = 0; k < L; ++k) v[k] = (k < nvalid) ? ldc_stream(src + row_base + int64_t(m0 + k) * 8) : czero();
+    for (int k = 0; k < L; ++k) v[0][k] = (k < nvalid) ? ldc_stream(src_tile + int64_t(m0 + k) * 8) : czero();
     cplx* T = smem + lay.table;
     for (int e = t; e < E; e += blockDim.x) T[e] = table[int64_t(f) * E + e];
     __syncthreads();
-    ring_solve<L, RW>(v, T, q, i, lane, warp, nwarps, n_theta, nvalid, smem + lay.sW, smem + lay.sV,
-                      smem + lay.sTot);
+    ring_solve<L, RW, 1, false>(v, T, q, i, lane, warp, nwarps, n_theta, nvalid, smem + lay.sW, smem + lay.sV,
+                                smem + lay.sTot);
+    const int l = tile * 8 + row0 + i;
     if (l == 0 || l >= n_depth) {
 #pragma unroll
-        for (int k = 0; k < L; ++k) v[k] = czero();
+        for (int k = 0; k < L; ++k) v[0][k] = czero();
     }
     const FreqDev fd = fdev[f];
-    ring_epilogue<L>(v, q, n_chunks, nvalid, i, RW, m0, l, ea, f, n_theta, n_depth, fd.cy_rhs,
-                     azimuth_scale(fd.k0, r_new, delta_theta), smem + lay.sFirst, smem + lay.sLast,
-                     dst + row_base, in_range);
+    ring_epilogue<L, 1>(v, q, n_chunks, nvalid, i, RW, RW, m0, row0, tile * 8 + row0, ea, f, n_theta, n_depth,
+                        T[1], fd.cy_rhs, azimuth_scale(fd.k0, r_new, delta_theta), smem + lay.sFirst,
+                        smem + lay.sLast, tile_base, in_range);
 }
 
 // Load u (reference layout [f][m][l] or device tiles), apply the boundary
@@ -390,26 +666,28 @@ k_finish(const cplx* __restrict__ src, int src_tiled, cplx* __restrict__ dst, co
     cplx* sLast = sFirst + n_chunks * RW;
     const int groups = 8 / RW;
     const int tile = blockIdx.x / groups;
-    const int l = tile * 8 + (blockIdx.x % groups) * RW + i;
+    const int row0 = (blockIdx.x % groups) * RW;
+    const int l = tile * 8 + row0 + i;
     const int f = blockIdx.y;
     const FreqDev fd = fdev[f];
     const double s = azimuth_scale(fd.k0, r, delta_theta);
     const int m0 = q * L;
     const int nvalid = in_range ? min(L, n_theta - m0) : 0;
-    const int64_t row_base = (int64_t(f) * n_tiles + tile) * n_theta * 8 + (l & 7);
-    cplx u[L];
+    const int64_t tile_off = (int64_t(f) * n_tiles + tile) * n_theta * 8;
+    cplx u[1][L];
 #pragma unroll
     for (int k = 0; k < L; ++k) {
         cplx v = czero();
         const int m = m0 + k;
         if (k < nvalid && l < n_depth) {
-            v = src_tiled ? ldc(src + row_base + int64_t(m) * 8) : ldc(src + (int64_t(f) * n_theta + m) * n_depth + l);
+            v = src_tiled ? ldc(src + tile_off + int64_t(m) * 8 + row0 + i)
+                          : ldc(src + (int64_t(f) * n_theta + m) * n_depth + l);
             if (l == 0 || (!ea.periodic && (m == 0 || m == n_theta - 1))) v = czero();
         }
-        u[k] = v;
+        u[0][k] = v;
     }
-    ring_epilogue<L>(u, q, n_chunks, nvalid, i, RW, m0, l, ea, f, n_theta, n_depth, fd.cy_rhs, s, sFirst, sLast,
-                     dst + row_base, in_range);
+    ring_epilogue<L, 1>(u, q, n_chunks, nvalid, i, RW, RW, m0, row0, tile * 8 + row0, ea, f, n_theta, n_depth,
+                        cone(), fd.cy_rhs, s, sFirst, sLast, dst + tile_off, in_range);
 }
 
 // ------------------------------------------------------------ launchers
@@ -426,17 +704,33 @@ void ring_shape(int n_theta, int* L, int* RW) {
     *L = 0; *RW = 0;   // n_theta > 4096: not supported by the ring kernels
 }
 
-int ring_table_elems(int n_theta) {
+// Which azimuth kernel serves a ring of n_theta points, and its table layout.
+struct RingPlan {
+    int kind;          // 0: ring-per-warp, 1: block pipeline / direct
     int L, RW;
-    ring_shape(n_theta, &L, &RW);
-    return ring_layout(n_theta, L, RW).E;
+    RingLayout lay;
+};
+
+static RingPlan ring_plan(int n_theta) {
+    RingPlan p;
+    if (n_theta % 32 == 0 && n_theta / 32 >= 2 && n_theta / 32 <= 16 && !(getenv("PE3D_RING_BLOCK"))) {
+        p.kind = 0;
+        p.L = n_theta / 32;
+        p.RW = 1;
+        p.lay = ring_layout(n_theta, p.L, 1);     // 32 chunks, qp[0..32]
+        return p;
+    }
+    p.kind = 1;
+    ring_shape(n_theta, &p.L, &p.RW);
+    p.lay = ring_layout(n_theta, p.L, p.RW);
+    return p;
 }
+
+int ring_table_elems(int n_theta) { return ring_plan(n_theta).lay.E; }
 
 cudaError_t launch_ring_setup(const LaunchCtx& c, cplx* table, int n_steps, int first_index, double r_start,
                               double delta_r) {
-    int L, RW;
-    ring_shape(c.n_theta, &L, &RW);
-    const RingLayout lay = ring_layout(c.n_theta, L, RW);
+    const RingLayout lay = ring_plan(c.n_theta).lay;
     const int total = c.n_freq * n_steps;
     if (total == 0) return cudaSuccess;
     k_ring_setup<<<(total + 63) / 64, 64, 0, c.stream>>>(table, c.fdev, c.n_freq, n_steps, first_index, r_start,
@@ -450,38 +744,74 @@ static cudaError_t set_smem(K kern, size_t bytes) {
     return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
 }
 
+template <int L, int RT, int STAGES>
+static cudaError_t launch_warp_ring(const LaunchCtx& c, const cplx* src, cplx* dst, const cplx* table_step, int E,
+                                   double r_new, const EpilogueArgs& ea) {
+    auto kern = k_azimuth_warp<L, RT, STAGES>;
+    const int nthr = 32 * 8 / RT;
+    const size_t bytes = sizeof(cplx) * (size_t(STAGES) * 32 * L * 8 + E);
+    cudaError_t e = set_smem(kern, bytes);
+    if (e != cudaSuccess) return e;
+    int per_sm = int((227 * 1024) / (bytes + 1024));
+    if (per_sm > 2048 / nthr) per_sm = 2048 / nthr;
+    if (per_sm < 1) per_sm = 1;
+    const int64_t items = int64_t(c.n_freq) * c.n_tiles;
+    const int64_t ctas = int64_t(c.num_sms) * per_sm;
+    const int per = int((items + ctas - 1) / ctas);
+    const int grid = int((items + per - 1) / per);
+    kern<<<grid, nthr, bytes, c.stream>>>(src, dst, table_step, E, c.fdev, c.n_tiles, c.n_depth, items, per, r_new,
+                                          c.delta_theta, ea);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_azimuth_scan(const LaunchCtx& c, const cplx* src, cplx* dst, const cplx* table_step, double r_new,
                                 const EpilogueArgs& ea) {
-    int L, RW;
-    ring_shape(c.n_theta, &L, &RW);
-    const RingLayout rl = ring_layout(c.n_theta, L, RW);
+    const RingPlan plan = ring_plan(c.n_theta);
+    if (plan.kind == 0 && ea.periodic) {
+        const int E = plan.lay.E;
+        const int stages = getenv("PE3D_RING_STAGES") ? atoi(getenv("PE3D_RING_STAGES")) : 2;
+        switch (plan.L) {
+            case 2: return launch_warp_ring<2, 2, 3>(c, src, dst, table_step, E, r_new, ea);
+            case 4: return launch_warp_ring<4, 2, 3>(c, src, dst, table_step, E, r_new, ea);
+            case 8: return stages == 3 ? launch_warp_ring<8, 2, 3>(c, src, dst, table_step, E, r_new, ea)
+                                       : launch_warp_ring<8, 2, 2>(c, src, dst, table_step, E, r_new, ea);
+            case 16: return launch_warp_ring<16, 1, 2>(c, src, dst, table_step, E, r_new, ea);
+            default: break;
+        }
+    }
+    const int L = plan.L, RW = plan.RW;
+    const RingLayout rl = plan.lay;
     const int nthreads = round32(RW * rl.n_chunks);
     const size_t stage_bytes = sizeof(cplx) * size_t(RW) * c.n_theta;
-    if (RW == 8 && 2 * stage_bytes <= 160 * 1024) {
-        const int stages = (3 * stage_bytes <= 100 * 1024) ? 3 : 2;
+    if (RW == 8 && 2 * stage_bytes <= 110 * 1024) {
+        const int stages = (3 * stage_bytes <= 72 * 1024) ? 3 : 2;
         const int64_t items = int64_t(c.n_freq) * c.n_tiles;
+        constexpr int RT = 2;
+        const int nthr = round32((8 / RT) * rl.n_chunks);
         auto go = [&](auto kern, int Lv) -> cudaError_t {
-            RingSmem<8, 8> dummy(0, 0, 0, 0);
-            (void)dummy;
             const int n_chunks = (c.n_theta + Lv - 1) / Lv;
-            const size_t elems = size_t(stages) * RW * c.n_theta + rl.E + 2 * (nthreads / 32) * RW + 2 * RW +
+            const size_t elems = size_t(stages) * RW * c.n_theta + rl.E + 2 * (nthr / 32) * RW + 2 * RW +
                                  2 * size_t(n_chunks) * RW;
             const size_t bytes = sizeof(cplx) * elems;
             cudaError_t e = set_smem(kern, bytes);
             if (e != cudaSuccess) return e;
             int per_sm = int((228 * 1024) / (bytes + 1024));
+            if (per_sm > 2048 / nthr) per_sm = 2048 / nthr;
             if (per_sm < 1) per_sm = 1;
             const int64_t ctas = int64_t(c.num_sms) * per_sm;
             const int per = int((items + ctas - 1) / ctas);
             const int grid = int((items + per - 1) / per);
-            kern<<<grid, nthreads, bytes, c.stream>>>(src, dst, table_step, rl.E, c.fdev, c.n_theta, c.n_tiles,
-                                                      c.n_depth, items, per, r_new, c.delta_theta, ea);
+            kern<<<grid, nthr, bytes, c.stream>>>(src, dst, table_step, rl.E, c.fdev, c.n_theta, c.n_tiles,
+                                                  c.n_depth, items, per, r_new, c.delta_theta, ea);
             return cudaGetLastError();
         };
-        if (L == 8 && stages == 3) return go(k_azimuth_pipe<8, 3>, 8);
-        if (L == 8 && stages == 2) return go(k_azimuth_pipe<8, 2>, 8);
-        if (L == 16 && stages == 3) return go(k_azimuth_pipe<16, 3>, 16);
-        if (L == 16 && stages == 2) return go(k_azimuth_pipe<16, 2>, 16);
+        const bool full = c.n_theta % L == 0;
+        if (nthr <= 256 && L == 8) {
+            if (full && stages == 3) return go(k_azimuth_pipe<8, 3, RT, true>, 8);
+            if (full && stages == 2) return go(k_azimuth_pipe<8, 2, RT, true>, 8);
+            if (stages == 3) return go(k_azimuth_pipe<8, 3, RT, false>, 8);
+            if (stages == 2) return go(k_azimuth_pipe<8, 2, RT, false>, 8);
+        }
     }
     dim3 grid(c.n_tiles * (8 / RW), c.n_freq);
     auto direct = [&](auto kern, int Lv, int RWv) -> cudaError_t {
