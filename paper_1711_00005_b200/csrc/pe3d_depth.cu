@@ -21,7 +21,22 @@
 #include "pe3d_device.cuh"
 #include "pe3d_internal.h"
 
+#include <cstdlib>
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 namespace pe3d {
+
+#ifdef PE3D_PHASE_TIMING
+// Phase timing of k_depth_scan (profiling builds only): per CTA, thread 0
+// accumulates clock64 deltas of each phase into g_phase[blockIdx][phase].
+__device__ unsigned long long g_phase[4096][16];
+#define PHASE_BEGIN long long _ph_t = clock64();
+#define PHASE(k) do { if (threadIdx.x == 0) { long long _n = clock64(); g_phase[blockIdx.x][k] += _n - _ph_t; _ph_t = _n; } } while (0)
+#else
+#define PHASE_BEGIN
+#define PHASE(k) do {} while (0)
+#endif
 
 // One thread per frequency: Thomas pivots of the depth matrix with the
 // surface row imposed (ref operators.py:227-238, tridiag.py:151-167) using
@@ -58,87 +73,101 @@ __global__ void k_factor_depth(const cplx* __restrict__ local, int64_t local_fst
     }
 }
 
-// Per-lane addressing of one column's 32 depth tiles of this warp (32 lines
-// of 128 B): lane -> (line 4k + lane/8, element lane%8), k = 0..7, so one
-// warp instruction moves 4 full lines.  In shared memory the element is
-// XOR-swizzled by the line index so that the per-thread tile reads
-// (lane = line) are bank-conflict free.
-struct LaneLines {
-    int64_t goff;          // global element offset of k = 0 relative to the column base
-    int64_t gstep;         // 4 lines
-    int soff_even, soff_odd;
-    unsigned valid;        // bit k: line 4k + lane/8 exists
+// Column staging.  A thread owns RPT consecutive rows (RPT = 8: a whole
+// 128-B tile line; RPT = 4: half a line); a warp owns LPW = 4*RPT lines of
+// a column.  Global <-> shared copies are line-wise (lane -> line 4k + lane/8,
+// element lane%8: one warp instruction moves 4 full lines); in shared memory
+// element e of line ln sits at ln*8 + (e ^ swz(ln)), swz = ln&7 (RPT 8) or
+// ln&3 (RPT 4), which makes both the line-wise copies and the per-thread
+// row reads bank-conflict free.
+template <int RPT>
+struct Lines {
+    static constexpr int LPW = 4 * RPT;            // lines per warp
+    static constexpr int KIN = LPW / 4;            // copy instructions per lane
+    __device__ static int swz(int ln) { return RPT == 8 ? (ln & 7) : (ln & 3); }
 };
 
-__device__ __forceinline__ LaneLines lane_lines(int warp, int lane, int n_tiles, int64_t line_stride) {
-    LaneLines ll;
-    const int ln = lane >> 3, e = lane & 7;
-    ll.goff = int64_t(warp * 32 + ln) * line_stride + e;
-    ll.gstep = 4 * line_stride;
-    ll.soff_even = ln * 8 + (e ^ ln);
-    ll.soff_odd = ln * 8 + (e ^ (ln | 4));
-    ll.valid = 0;
+template <int RPT>
+struct LaneLines {
+    int64_t goff, gstep;
+    int soff[Lines<RPT>::KIN];
+    unsigned valid;
+    __device__ LaneLines(int warp, int lane, int n_tiles, int64_t line_stride) {
+        const int ln0 = lane >> 3, e = lane & 7;
+        goff = int64_t(warp * Lines<RPT>::LPW + ln0) * line_stride + e;
+        gstep = 4 * line_stride;
+        valid = 0;
 #pragma unroll
-    for (int k = 0; k < 8; ++k)
-        if (warp * 32 + 4 * k + ln < n_tiles) ll.valid |= 1u << k;
-    return ll;
-}
+        for (int k = 0; k < Lines<RPT>::KIN; ++k) {
+            const int ln = 4 * k + ln0;
+            soff[k] = ln * 8 + (e ^ Lines<RPT>::swz(ln));
+            if (warp * Lines<RPT>::LPW + ln < n_tiles) valid |= 1u << k;
+        }
+    }
+};
 
-__device__ __forceinline__ void stage_column(cplx* stage, const cplx* col_base, const LaneLines& ll) {
+template <int RPT>
+__device__ __forceinline__ void stage_column(cplx* stage, const cplx* col_base, const LaneLines<RPT>& ll) {
     const cplx* gp = col_base + ll.goff;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        cplx* d = stage + 32 * k + ((k & 1) ? ll.soff_odd : ll.soff_even);
-        if (ll.valid & (1u << k)) cp_async16(d, gp);
-        else *d = czero();
+    for (int k = 0; k < Lines<RPT>::KIN; ++k) {
+        if (ll.valid & (1u << k)) cp_async16(stage + ll.soff[k], gp);
+        else stage[ll.soff[k]] = czero();
         gp += ll.gstep;
     }
 }
 
-__device__ __forceinline__ void unstage_column(cplx* col_base, const cplx* stage, const LaneLines& ll) {
+template <int RPT>
+__device__ __forceinline__ void unstage_column(cplx* col_base, const cplx* stage, const LaneLines<RPT>& ll) {
     cplx* gp = col_base + ll.goff;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        if (ll.valid & (1u << k)) stc(gp, stage[32 * k + ((k & 1) ? ll.soff_odd : ll.soff_even)]);
+    for (int k = 0; k < Lines<RPT>::KIN; ++k) {
+        if (ll.valid & (1u << k)) stc(gp, stage[ll.soff[k]]);
         gp += ll.gstep;
     }
 }
 
-template <int MAXT> struct DepthCfg;
-template <> struct DepthCfg<128> { static constexpr int STAGES = 3, MINB = 3; static constexpr bool PRECOMP = true; };
-template <> struct DepthCfg<256> { static constexpr int STAGES = 2, MINB = 2; static constexpr bool PRECOMP = true; };
-template <> struct DepthCfg<512> { static constexpr int STAGES = 2, MINB = 1; static constexpr bool PRECOMP = false; };
+// Launch configurations: rows per thread, max threads, pipeline depth,
+// min CTAs per SM, and whether the scan multipliers live in shared memory.
+template <int RPT, int MAXT> struct DepthCfg;
+template <> struct DepthCfg<4, 256> { static constexpr int STAGES = 2, MINB = 3; static constexpr bool PRECOMP = true; };
+template <> struct DepthCfg<8, 128> { static constexpr int STAGES = 3, MINB = 3; static constexpr bool PRECOMP = true; };
+template <> struct DepthCfg<8, 256> { static constexpr int STAGES = 2, MINB = 2; static constexpr bool PRECOMP = true; };
+template <> struct DepthCfg<8, 512> { static constexpr int STAGES = 2, MINB = 1; static constexpr bool PRECOMP = false; };
 
-template <int MAXT>
+template <int RPT, int MAXT>
 __host__ __device__ constexpr size_t depth_smem_elems(int nthreads) {
-    return size_t(nthreads / 32) * DepthCfg<MAXT>::STAGES * 256 +
-           (DepthCfg<MAXT>::PRECOMP ? 12 * size_t(nthreads) : 0) + 5 * size_t(nthreads / 32);
+    return size_t(nthreads / 32) * DepthCfg<RPT, MAXT>::STAGES * (Lines<RPT>::LPW * 8) +
+           (DepthCfg<RPT, MAXT>::PRECOMP ? 10 * size_t(nthreads) : 0) + 5 * size_t(nthreads / 32);
 }
 
 // Persistent CTA over a contiguous run of global columns g = f*n_theta + m.
-// Thread t owns depth tile t (rows 8t..8t+7).  Registers hold the tile's
+// Thread t owns rows RPT*t .. RPT*t + RPT-1.  Registers hold the rows'
 // column-independent coefficients
-//   A_l = kappa (1 + cx_rhs local_l),  m_l,   (kappa = -1/off)
-// so that b_l = m_l (A_l x_l + beta d2_l) = inv_l rhs_l with
-// beta = kappa cx_rhs s_z.  The Kogge-Stone multipliers of the tile scans
-// (products of m_l over windows of tiles) are column independent too and,
-// for up to 256 threads, are computed once per frequency into shared memory
-// -- with zeros where a lane has no partner, so the scans are branch free.
-template <int MAXT>
-__global__ void __launch_bounds__(MAXT, DepthCfg<MAXT>::MINB)
+//   A'_l = kappa (1 + cx_rhs local_l) - 2 beta,  m_l,   (kappa = -1/off,
+//   beta = kappa cx_rhs s_z)
+// so that r'_l = A'_l x_l + beta (x_{l+1} + x_{l-1}) = kappa rhs_l and the
+// forward elimination is y_l = m_l (r'_l + y_{l-1}).  The Kogge-Stone
+// multipliers of the row-chunk scans (products of m_l over windows of
+// threads) are column independent and, except for the largest CTAs, are
+// computed once per frequency into shared memory -- zero where a lane has
+// no partner, so the scans are branch free.
+template <int RPT, int MAXT>
+__global__ void __launch_bounds__(MAXT, (DepthCfg<RPT, MAXT>::MINB))
 k_depth_scan(const cplx* __restrict__ src, cplx* __restrict__ dst, const cplx* __restrict__ loc_tab,
              const cplx* __restrict__ mul_tab, const FreqDev* __restrict__ fdev, int n_theta, int n_tiles,
              int64_t total_cols, int cols_per_cta, int sector) {
-    constexpr int STAGES = DepthCfg<MAXT>::STAGES;
-    constexpr bool PRECOMP = DepthCfg<MAXT>::PRECOMP;
+    constexpr int STAGES = DepthCfg<RPT, MAXT>::STAGES;
+    constexpr bool PRECOMP = DepthCfg<RPT, MAXT>::PRECOMP;
+    constexpr int SW = Lines<RPT>::LPW * 8;         // stage elements per warp per column
     extern __shared__ cplx smem[];
     const int nthreads = blockDim.x;
     const int nwarps = nthreads >> 5;
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    cplx* stage = smem + warp * (STAGES * 256);
-    cplx* mf = smem + nwarps * (STAGES * 256);      // [5][nthreads]   (PRECOMP)
-    cplx* mb = mf + (PRECOMP ? 5 * nthreads : 0);   // [5][nthreads]
-    cplx* pincf = mb + (PRECOMP ? 5 * nthreads : 0);
+    cplx* stage = smem + warp * (STAGES * SW);
+    cplx* mf = smem + nwarps * (STAGES * SW);       // [4][nthreads] forward multipliers, levels 1..4
+    cplx* mb = mf + (PRECOMP ? 4 * nthreads : 0);   // [4][nthreads] backward
+    cplx* pincf = mb + (PRECOMP ? 4 * nthreads : 0);
     cplx* pincb = pincf + (PRECOMP ? nthreads : 0);
     cplx* spw = pincb + (PRECOMP ? nthreads : 0);   // [nwarps] warp products
     cplx* sY = spw + nwarps;
@@ -150,18 +179,21 @@ k_depth_scan(const cplx* __restrict__ src, cplx* __restrict__ dst, const cplx* _
     const int64_t g1 = g0 + cols_per_cta < total_cols ? g0 + cols_per_cta : total_cols;
     if (g0 >= g1) return;
     const int n_cols = int(g1 - g0);
-    const bool active = t < n_tiles;
-    const int64_t nz8 = int64_t(n_tiles) * 8;
+    const int nz8 = n_tiles * 8;
+    const bool active = t * RPT < nz8;
     const int64_t line_stride = int64_t(n_theta) * 8;
     const int64_t freq_stride = int64_t(n_tiles) * line_stride;
-    const LaneLines ll = lane_lines(warp, lane, n_tiles, line_stride);
+    const LaneLines<RPT> ll(warp, lane, n_tiles, line_stride);
+    // this thread's rows inside its warp's stage: line, first element
+    const int my_line = lane * RPT / 8, my_e0 = (lane * RPT) & 7;
+    const int my_swz = Lines<RPT>::swz(my_line);
 
     // (frequency, column) of the next column to prefetch
     int pf = int(g0 / n_theta), pc = int(g0 - int64_t(pf) * n_theta);
 #pragma unroll
     for (int p = 0; p < STAGES - 1; ++p) {
         if (p < n_cols) {
-            stage_column(stage + p * 256, src + pf * freq_stride + int64_t(pc) * 8, ll);
+            stage_column<RPT>(stage + p * SW, src + pf * freq_stride + int64_t(pc) * 8, ll);
             if (++pc == n_theta) { pc = 0; ++pf; }
         }
         cp_async_commit();
@@ -169,8 +201,9 @@ k_depth_scan(const cplx* __restrict__ src, cplx* __restrict__ dst, const cplx* _
 
     int f = int(g0 / n_theta), col = int(g0 - int64_t(f) * n_theta);
     int cur_f = -1;
-    cplx A[8], M[8], beta = czero();
+    cplx A[RPT], M[RPT], beta = czero(), P0f = czero(), P0b = czero();
     int slot = 0;
+    PHASE_BEGIN
     for (int it = 0; it < n_cols; ++it) {
         if (f != cur_f) {
             // ---- per-frequency coefficients and scan multipliers
@@ -179,22 +212,23 @@ k_depth_scan(const cplx* __restrict__ src, cplx* __restrict__ dst, const cplx* _
             beta = cmul(kappa, crmul(fd.s_z, fd.cx_rhs));
             cplx P = cone();
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const cplx lc = active ? ldc(loc_tab + f * nz8 + 8 * t + i) : czero();
-                M[i] = active ? ldc(mul_tab + f * nz8 + 8 * t + i) : czero();
-                // A'_l = kappa (1 + cx_rhs local_l) - 2 beta  (the -2x of d2 folded in)
+            for (int i = 0; i < RPT; ++i) {
+                const cplx lc = active ? ldc(loc_tab + int64_t(f) * nz8 + RPT * t + i) : czero();
+                M[i] = active ? ldc(mul_tab + int64_t(f) * nz8 + RPT * t + i) : czero();
                 A[i] = csub(cmul(kappa, cadd(cone(), cmul(fd.cx_rhs, lc))), cadd(beta, beta));
                 P = cmul(M[i], P);
             }
             if (!active) P = cone();
             __syncthreads();                       // previous column done with the tables
+            P0f = lane >= 1 ? P : czero();         // level-0 multipliers (own tile product)
+            P0b = lane + 1 < 32 ? P : czero();
             cplx Pf = P, Pb = P;
 #pragma unroll
             for (int d = 0; d < 5; ++d) {
                 const int o = 1 << d;
-                if (PRECOMP) {
-                    mf[d * nthreads + t] = lane >= o ? Pf : czero();
-                    mb[d * nthreads + t] = lane + o < 32 ? Pb : czero();
+                if (PRECOMP && d > 0) {
+                    mf[(d - 1) * nthreads + t] = lane >= o ? Pf : czero();
+                    mb[(d - 1) * nthreads + t] = lane + o < 32 ? Pb : czero();
                 }
                 const cplx pu = shfl_up(Pf, o), pd = shfl_down(Pb, o);
                 if (lane >= o) Pf = cmul(Pf, pu);
@@ -204,58 +238,61 @@ k_depth_scan(const cplx* __restrict__ src, cplx* __restrict__ dst, const cplx* _
             if (lane == 31) spw[warp] = Pf;
             __syncthreads();
             cur_f = f;
+            PHASE(0);
         }
         // ---- prefetch column it + STAGES - 1, then wait for column it
         {
             const int ps = (slot + STAGES - 1) % STAGES;
             if (it + STAGES - 1 < n_cols) {
-                stage_column(stage + ps * 256, src + pf * freq_stride + int64_t(pc) * 8, ll);
+                stage_column<RPT>(stage + ps * SW, src + pf * freq_stride + int64_t(pc) * 8, ll);
                 if (++pc == n_theta) { pc = 0; ++pf; }
             }
             cp_async_commit();
+            PHASE(1);
             cp_async_wait<STAGES - 1>();
             __syncwarp();
+            PHASE(2);
         }
-        cplx* cur = stage + slot * 256;
-        const int sw = lane & 7;
-        cplx x[8];
+        cplx* cur = stage + slot * SW;
+        cplx x[RPT];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) x[i] = cur[lane * 8 + (i ^ sw)];
+        for (int i = 0; i < RPT; ++i) x[i] = cur[my_line * 8 + ((my_e0 + i) ^ my_swz)];
 
-        // ---- halos: last row of the tile above, first row of the tile below
-        cplx up = shfl_up(x[7], 1), dn = shfl_down(x[0], 1);
-        if (lane == 31) sUp[warp] = x[7];
+        // ---- halos: last row of the chunk above, first row of the chunk below
+        cplx up = shfl_up(x[RPT - 1], 1), dn = shfl_down(x[0], 1);
+        if (lane == 31) sUp[warp] = x[RPT - 1];
         if (lane == 0) sDn[warp] = x[0];
+        PHASE(3);
         __syncthreads();
+        PHASE(4);
         if (lane == 0) up = warp > 0 ? sUp[warp - 1] : czero();
         if (lane == 31) dn = warp < nwarps - 1 ? sDn[warp + 1] : czero();
         if (t == 0) up = czero();
-        if (t >= n_tiles - 1) dn = czero();
 
         // ---- r'_l = kappa rhs_l = A'_l x_l + beta (x_{l+1} + x_{l-1})
         //      (ref operators.py:115-121,139,210; marching.py:114: row 0 has m_0 = 0)
-        cplx b[8];
+        cplx b[RPT];
         if (sector && (col == 0 || col == n_theta - 1)) {       // uniform per CTA
 #pragma unroll
-            for (int i = 0; i < 8; ++i) b[i] = czero();
+            for (int i = 0; i < RPT; ++i) b[i] = czero();
         } else {
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
+            for (int i = 0; i < RPT; ++i) {
                 const cplx um = i ? x[i - 1] : up;
-                const cplx upp = i < 7 ? x[i + 1] : dn;
+                const cplx upp = i < RPT - 1 ? x[i + 1] : dn;
                 b[i] = cfma(A[i], x[i], cmul(beta, cadd(upp, um)));
             }
         }
 
         // ---- forward elimination y_l = m_l (r'_l + y_{l-1}): local chunk, scan, exact re-run
-        // (inactive threads have m = 0 and x = 0, hence Y = 0)
+        // (inactive threads have m = 0, hence Y = 0; pad rows have m = 0)
         cplx Y = czero();
 #pragma unroll
-        for (int i = 0; i < 8; ++i) Y = cmul(M[i], cadd(b[i], Y));
+        for (int i = 0; i < RPT; ++i) Y = cmul(M[i], cadd(b[i], Y));
         cplx Pacc = cone();
         if (!PRECOMP) {
 #pragma unroll
-            for (int i = 0; i < 8; ++i) Pacc = cmul(M[i], Pacc);
+            for (int i = 0; i < RPT; ++i) Pacc = cmul(M[i], Pacc);
             if (!active) Pacc = cone();
         }
 #pragma unroll
@@ -263,29 +300,31 @@ k_depth_scan(const cplx* __restrict__ src, cplx* __restrict__ dst, const cplx* _
             const int o = 1 << d;
             const cplx Yp = shfl_up(Y, o);
             if (PRECOMP) {
-                Y = cfma(mf[d * nthreads + t], Yp, Y);
+                Y = cfma(d == 0 ? P0f : mf[(d - 1) * nthreads + t], Yp, Y);
             } else {
                 const cplx Pp = shfl_up(Pacc, o);
                 if (lane >= o) { Y = cfma(Pacc, Yp, Y); Pacc = cmul(Pacc, Pp); }
             }
         }
         if (lane == 31) sY[warp] = Y;
+        PHASE(5);
         __syncthreads();
+        PHASE(6);
         cplx C = czero();
         for (int w = 0; w < warp; ++w) C = cfma(spw[w], C, sY[w]);
         cplx y = shfl_up(cfma(PRECOMP ? pincf[t] : Pacc, C, Y), 1);
         if (lane == 0) y = C;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) { y = cmul(M[i], cadd(b[i], y)); b[i] = y; }
+        for (int i = 0; i < RPT; ++i) { y = cmul(M[i], cadd(b[i], y)); b[i] = y; }
 
-        // ---- back substitution
+        // ---- back substitution x_l = y_l + m_l x_{l+1}
         cplx X = czero();
 #pragma unroll
-        for (int i = 7; i >= 0; --i) X = cfma(M[i], X, b[i]);
+        for (int i = RPT - 1; i >= 0; --i) X = cfma(M[i], X, b[i]);
         cplx Qacc = cone();
         if (!PRECOMP) {
 #pragma unroll
-            for (int i = 0; i < 8; ++i) Qacc = cmul(M[i], Qacc);
+            for (int i = 0; i < RPT; ++i) Qacc = cmul(M[i], Qacc);
             if (!active) Qacc = cone();
         }
 #pragma unroll
@@ -293,39 +332,272 @@ k_depth_scan(const cplx* __restrict__ src, cplx* __restrict__ dst, const cplx* _
             const int o = 1 << d;
             const cplx Xn = shfl_down(X, o);
             if (PRECOMP) {
-                X = cfma(mb[d * nthreads + t], Xn, X);
+                X = cfma(d == 0 ? P0b : mb[(d - 1) * nthreads + t], Xn, X);
             } else {
                 const cplx Qn = shfl_down(Qacc, o);
                 if (lane + o < 32) { X = cfma(Qacc, Xn, X); Qacc = cmul(Qacc, Qn); }
             }
         }
         if (lane == 0) sX[warp] = X;
+        PHASE(7);
         __syncthreads();
+        PHASE(8);
         cplx D = czero();
         for (int w = nwarps - 1; w > warp; --w) D = cfma(spw[w], D, sX[w]);
         cplx xv = shfl_down(cfma(PRECOMP ? pincb[t] : Qacc, D, X), 1);
         if (lane == 31) xv = D;
 #pragma unroll
-        for (int i = 7; i >= 0; --i) { xv = cfma(M[i], xv, b[i]); b[i] = xv; }
+        for (int i = RPT - 1; i >= 0; --i) { xv = cfma(M[i], xv, b[i]); b[i] = xv; }
+        PHASE(9);
 
         // ---- stage out through the same buffer, full-line stores
 #pragma unroll
-        for (int i = 0; i < 8; ++i) cur[lane * 8 + (i ^ sw)] = b[i];
+        for (int i = 0; i < RPT; ++i) cur[my_line * 8 + ((my_e0 + i) ^ my_swz)] = b[i];
         __syncwarp();
-        unstage_column(dst + f * freq_stride + int64_t(col) * 8, cur, ll);
+        unstage_column<RPT>(dst + f * freq_stride + int64_t(col) * 8, cur, ll);
         __syncwarp();
+        PHASE(10);
         if (++col == n_theta) { col = 0; ++f; }
         slot = (slot + 1 == STAGES) ? 0 : slot + 1;
     }
     cp_async_wait<0>();
 }
 
+// ------------------------------------------------------------- TMA variant
+// Same math as k_depth_scan<8, *>, but each warp's 32 column tiles move
+// through the Tensor Memory Accelerator: one 4-D tiled TMA load per warp and
+// column (box {16 doubles, 1 azimuth, 32 tiles, 1 frequency}, hardware
+// 128-B swizzle = the line swizzle the threads read with, zero fill past the
+// last tile), completion on a per-warp mbarrier, and one TMA bulk store of
+// the solved column from the same stage.  The warps issue no per-line
+// copies at all; a 3-deep per-warp stage ring keeps two columns in flight.
+template <int STAGES, int MINB>
+__global__ void __launch_bounds__(128, MINB)
+k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ CUtensorMap tm_dst,
+            const cplx* __restrict__ loc_tab, const cplx* __restrict__ mul_tab, const FreqDev* __restrict__ fdev,
+            int n_theta, int n_tiles, int64_t total_cols, int cols_per_cta, int sector) {
+    constexpr int RPT = 8;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    const int nthreads = blockDim.x;
+    const int nwarps = nthreads >> 5;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    // 1024-B aligned stage ring (128-B swizzle atoms), then barriers and tables
+    cplx* base = reinterpret_cast<cplx*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    cplx* stage = base + warp * (STAGES * 256);
+    cplx* mf = base + nwarps * (STAGES * 256);      // [4][nthreads]
+    cplx* mb = mf + 4 * nthreads;
+    cplx* pincf = mb + 4 * nthreads;
+    cplx* pincb = pincf + nthreads;
+    cplx* spw = pincb + nthreads;
+    cplx* sY = spw + nwarps;
+    cplx* sX = sY + nwarps;
+    cplx* sUp = sX + nwarps;
+    cplx* sDn = sUp + nwarps;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sDn + nwarps) + warp * STAGES;
+
+    const int64_t g0 = int64_t(blockIdx.x) * cols_per_cta;
+    const int64_t g1 = g0 + cols_per_cta < total_cols ? g0 + cols_per_cta : total_cols;
+    if (g0 >= g1) return;
+    const int n_cols = int(g1 - g0);
+    const int nz8 = n_tiles * 8;
+    const bool active = t * RPT < nz8;
+    const int tile0 = warp * 32;
+
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < STAGES; ++k) mbar_init(&bars[k], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+
+    int pf = int(g0 / n_theta), pc = int(g0 - int64_t(pf) * n_theta);
+    if (lane == 0) {
+#pragma unroll
+        for (int p = 0; p < STAGES - 1; ++p) {
+            if (p < n_cols) {
+                mbar_expect_tx(&bars[p], 32 * 128);
+                tma_load_4d(stage + p * 256, &tm_src, 0, pc, tile0, pf, &bars[p]);
+                if (++pc == n_theta) { pc = 0; ++pf; }
+            }
+        }
+    }
+
+    int f = int(g0 / n_theta), col = int(g0 - int64_t(f) * n_theta);
+    int cur_f = -1;
+    cplx A[RPT], M[RPT], beta = czero(), P0f = czero(), P0b = czero();
+    int slot = 0;
+    unsigned parity = 0;
+    for (int it = 0; it < n_cols; ++it) {
+        if (f != cur_f) {
+            const FreqDev fd = fdev[f];
+            const cplx kappa = crecip(cneg(fd.off_z));
+            beta = cmul(kappa, crmul(fd.s_z, fd.cx_rhs));
+            cplx P = cone();
+#pragma unroll
+            for (int i = 0; i < RPT; ++i) {
+                const cplx lc = active ? ldc(loc_tab + int64_t(f) * nz8 + RPT * t + i) : czero();
+                M[i] = active ? ldc(mul_tab + int64_t(f) * nz8 + RPT * t + i) : czero();
+                A[i] = csub(cmul(kappa, cadd(cone(), cmul(fd.cx_rhs, lc))), cadd(beta, beta));
+                P = cmul(M[i], P);
+            }
+            if (!active) P = cone();
+            __syncthreads();
+            P0f = lane >= 1 ? P : czero();
+            P0b = lane + 1 < 32 ? P : czero();
+            cplx Pf = P, Pb = P;
+#pragma unroll
+            for (int d = 0; d < 5; ++d) {
+                const int o = 1 << d;
+                if (d > 0) {
+                    mf[(d - 1) * nthreads + t] = lane >= o ? Pf : czero();
+                    mb[(d - 1) * nthreads + t] = lane + o < 32 ? Pb : czero();
+                }
+                const cplx pu = shfl_up(Pf, o), pd = shfl_down(Pb, o);
+                if (lane >= o) Pf = cmul(Pf, pu);
+                if (lane + o < 32) Pb = cmul(Pb, pd);
+            }
+            pincf[t] = Pf;
+            pincb[t] = Pb;
+            if (lane == 31) spw[warp] = Pf;
+            __syncthreads();
+            cur_f = f;
+        }
+        cplx* cur = stage + slot * 256;
+        mbar_wait(&bars[slot], parity);
+        const int sw = lane & 7;
+        cplx x[RPT];
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) x[i] = cur[lane * 8 + (i ^ sw)];
+
+        cplx up = shfl_up(x[RPT - 1], 1), dn = shfl_down(x[0], 1);
+        if (lane == 31) sUp[warp] = x[RPT - 1];
+        if (lane == 0) sDn[warp] = x[0];
+        __syncthreads();
+        if (lane == 0) up = warp > 0 ? sUp[warp - 1] : czero();
+        if (lane == 31) dn = warp < nwarps - 1 ? sDn[warp + 1] : czero();
+        if (t == 0) up = czero();
+
+        cplx b[RPT];
+        if (sector && (col == 0 || col == n_theta - 1)) {
+#pragma unroll
+            for (int i = 0; i < RPT; ++i) b[i] = czero();
+        } else {
+#pragma unroll
+            for (int i = 0; i < RPT; ++i) {
+                const cplx um = i ? x[i - 1] : up;
+                const cplx upp = i < RPT - 1 ? x[i + 1] : dn;
+                b[i] = cfma(A[i], x[i], cmul(beta, cadd(upp, um)));
+            }
+        }
+        cplx Y = czero();
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) Y = cmul(M[i], cadd(b[i], Y));
+#pragma unroll
+        for (int d = 0; d < 5; ++d) Y = cfma(d == 0 ? P0f : mf[(d - 1) * nthreads + t], shfl_up(Y, 1 << d), Y);
+        if (lane == 31) sY[warp] = Y;
+        __syncthreads();
+        cplx C = czero();
+        for (int w = 0; w < warp; ++w) C = cfma(spw[w], C, sY[w]);
+        cplx y = shfl_up(cfma(pincf[t], C, Y), 1);
+        if (lane == 0) y = C;
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) { y = cmul(M[i], cadd(b[i], y)); b[i] = y; }
+
+        cplx X = czero();
+#pragma unroll
+        for (int i = RPT - 1; i >= 0; --i) X = cfma(M[i], X, b[i]);
+#pragma unroll
+        for (int d = 0; d < 5; ++d) X = cfma(d == 0 ? P0b : mb[(d - 1) * nthreads + t], shfl_down(X, 1 << d), X);
+        if (lane == 0) sX[warp] = X;
+        __syncthreads();
+        cplx D = czero();
+        for (int w = nwarps - 1; w > warp; --w) D = cfma(spw[w], D, sX[w]);
+        cplx xv = shfl_down(cfma(pincb[t], D, X), 1);
+        if (lane == 31) xv = D;
+#pragma unroll
+        for (int i = RPT - 1; i >= 0; --i) { xv = cfma(M[i], xv, b[i]); b[i] = xv; }
+
+        // ---- solved column back through the stage, one TMA store per warp
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) cur[lane * 8 + (i ^ sw)] = b[i];
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+            tma_store_4d(&tm_dst, 0, col, tile0, f, cur);
+            bulk_commit();
+            bulk_wait_read<1>();            // the previous column's store has left its stage slot
+            if (it + STAGES - 1 < n_cols) {
+                const int ps = (slot + STAGES - 1) % STAGES;
+                mbar_expect_tx(&bars[ps], 32 * 128);
+                tma_load_4d(stage + ps * 256, &tm_src, 0, pc, tile0, pf, &bars[ps]);
+                if (++pc == n_theta) { pc = 0; ++pf; }
+            }
+        }
+        __syncwarp();
+        if (++col == n_theta) { col = 0; ++f; }
+        if (++slot == STAGES) { slot = 0; parity ^= 1u; }
+    }
+    if (lane == 0) bulk_wait_read<0>();
+    __syncwarp();
+}
+
 static int round32(int x) { return (x + 31) / 32 * 32; }
 
-cudaError_t launch_depth_scan(const LaunchCtx& c, const cplx* src, cplx* dst) {
-    const int nthreads = round32(c.n_tiles);
+// Host side of the TMA path: 4-D tiled tensor maps over the device field
+// (dims {16 doubles, n_theta, n_tiles, n_freq}).
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+static bool field_tensor_map(CUtensorMap* tm, const void* base, const LaunchCtx& c) {
+    auto enc = tensor_map_encoder();
+    if (!enc) return false;
+    const cuuint64_t dims[4] = {16, cuuint64_t(c.n_theta), cuuint64_t(c.n_tiles), cuuint64_t(c.n_freq)};
+    const cuuint64_t strides[3] = {128, cuuint64_t(c.n_theta) * 128, cuuint64_t(c.n_theta) * 128 * c.n_tiles};
+    const cuuint32_t box[4] = {16, 1, 32, 1};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<void*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static cudaError_t launch_depth_tma(const LaunchCtx& c, const cplx* src, cplx* dst) {
+    CUtensorMap tm_src, tm_dst;
+    if (!field_tensor_map(&tm_src, src, c) || !field_tensor_map(&tm_dst, dst, c)) return cudaErrorNotSupported;
+    const int nthreads = (c.n_tiles + 31) / 32 * 32;
+    const int nwarps = nthreads / 32;
+    constexpr int STAGES = 3;
+    const size_t bytes = 1024 + sizeof(cplx) * (size_t(nwarps) * STAGES * 256 + 10 * size_t(nthreads) + 5 * nwarps) +
+                         sizeof(uint64_t) * nwarps * STAGES;
+    auto kern = k_depth_tma<STAGES, 3>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+    if (e != cudaSuccess) return e;
     const int64_t total = int64_t(c.n_freq) * c.n_theta;
-    auto go = [&](auto kern, size_t elems, int per_sm) -> cudaError_t {
+    int per_sm = int((227 * 1024) / (bytes + 1024));
+    if (per_sm > 3) per_sm = 3;
+    if (per_sm < 1) per_sm = 1;
+    const int64_t ctas = int64_t(c.num_sms) * per_sm;
+    const int per = int((total + ctas - 1) / ctas);
+    const int grid = int((total + per - 1) / per);
+    kern<<<grid, nthreads, bytes, c.stream>>>(tm_src, tm_dst, c.loc_tab, c.mul_tab, c.fdev, c.n_theta, c.n_tiles,
+                                              total, per, c.sector);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_depth_scan(const LaunchCtx& c, const cplx* src, cplx* dst) {
+    const int64_t total = int64_t(c.n_freq) * c.n_theta;
+    const int nz8 = c.n_tiles * 8;
+    auto go = [&](auto kern, int nthreads, size_t elems, int per_sm) -> cudaError_t {
         const size_t sm = sizeof(cplx) * elems;
         if (sm > 48 * 1024) {
             cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
@@ -338,9 +610,19 @@ cudaError_t launch_depth_scan(const LaunchCtx& c, const cplx* src, cplx* dst) {
                                                per, c.sector);
         return cudaGetLastError();
     };
-    if (nthreads <= 128) return go(k_depth_scan<128>, depth_smem_elems<128>(nthreads), DepthCfg<128>::MINB);
-    if (nthreads <= 256) return go(k_depth_scan<256>, depth_smem_elems<256>(nthreads), DepthCfg<256>::MINB);
-    return go(k_depth_scan<512>, depth_smem_elems<512>(nthreads), DepthCfg<512>::MINB);
+    if (c.n_tiles <= 128 && !getenv("PE3D_DEPTH_NO_TMA")) {
+        cudaError_t e = launch_depth_tma(c, src, dst);
+        if (e != cudaErrorNotSupported) return e;
+    }
+    const bool rpt4 = getenv("PE3D_DEPTH_RPT4") != nullptr;
+    if (rpt4 && nz8 / 4 <= 256) {
+        const int nt = round32(nz8 / 4);
+        return go(k_depth_scan<4, 256>, nt, depth_smem_elems<4, 256>(nt), DepthCfg<4, 256>::MINB);
+    }
+    const int nt = round32(c.n_tiles);
+    if (nt <= 128) return go(k_depth_scan<8, 128>, nt, depth_smem_elems<8, 128>(nt), DepthCfg<8, 128>::MINB);
+    if (nt <= 256) return go(k_depth_scan<8, 256>, nt, depth_smem_elems<8, 256>(nt), DepthCfg<8, 256>::MINB);
+    return go(k_depth_scan<8, 512>, nt, depth_smem_elems<8, 512>(nt), DepthCfg<8, 512>::MINB);
 }
 
 cudaError_t launch_factor_depth(const LaunchCtx& c, const cplx* local, int64_t local_fstride, int step_for_error) {
