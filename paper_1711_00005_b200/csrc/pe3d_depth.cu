@@ -427,6 +427,7 @@ k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ 
     cplx A[RPT], M[RPT], beta = czero(), P0f = czero(), P0b = czero();
     int slot = 0;
     unsigned parity = 0;
+    PHASE_BEGIN
     for (int it = 0; it < n_cols; ++it) {
         if (f != cur_f) {
             const FreqDev fd = fdev[f];
@@ -461,9 +462,12 @@ k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ 
             if (lane == 31) spw[warp] = Pf;
             __syncthreads();
             cur_f = f;
+            PHASE(0);
         }
         cplx* cur = stage + slot * 256;
+        PHASE(1);
         mbar_wait(&bars[slot], parity);
+        PHASE(2);
         const int sw = lane & 7;
         cplx x[RPT];
 #pragma unroll
@@ -472,7 +476,9 @@ k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ 
         cplx up = shfl_up(x[RPT - 1], 1), dn = shfl_down(x[0], 1);
         if (lane == 31) sUp[warp] = x[RPT - 1];
         if (lane == 0) sDn[warp] = x[0];
+        PHASE(3);
         __syncthreads();
+        PHASE(4);
         if (lane == 0) up = warp > 0 ? sUp[warp - 1] : czero();
         if (lane == 31) dn = warp < nwarps - 1 ? sDn[warp + 1] : czero();
         if (t == 0) up = czero();
@@ -486,22 +492,24 @@ k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ 
             for (int i = 0; i < RPT; ++i) {
                 const cplx um = i ? x[i - 1] : up;
                 const cplx upp = i < RPT - 1 ? x[i + 1] : dn;
-                b[i] = cfma(A[i], x[i], cmul(beta, cadd(upp, um)));
+                b[i] = cmul(M[i], cfma(A[i], x[i], cmul(beta, cadd(upp, um))));   // m_l r'_l, off the chain
             }
         }
         cplx Y = czero();
 #pragma unroll
-        for (int i = 0; i < RPT; ++i) Y = cmul(M[i], cadd(b[i], Y));
+        for (int i = 0; i < RPT; ++i) Y = cfma(M[i], Y, b[i]);
 #pragma unroll
         for (int d = 0; d < 5; ++d) Y = cfma(d == 0 ? P0f : mf[(d - 1) * nthreads + t], shfl_up(Y, 1 << d), Y);
         if (lane == 31) sY[warp] = Y;
+        PHASE(5);
         __syncthreads();
+        PHASE(6);
         cplx C = czero();
         for (int w = 0; w < warp; ++w) C = cfma(spw[w], C, sY[w]);
         cplx y = shfl_up(cfma(pincf[t], C, Y), 1);
         if (lane == 0) y = C;
 #pragma unroll
-        for (int i = 0; i < RPT; ++i) { y = cmul(M[i], cadd(b[i], y)); b[i] = y; }
+        for (int i = 0; i < RPT; ++i) { y = cfma(M[i], y, b[i]); b[i] = y; }
 
         cplx X = czero();
 #pragma unroll
@@ -509,7 +517,9 @@ k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ 
 #pragma unroll
         for (int d = 0; d < 5; ++d) X = cfma(d == 0 ? P0b : mb[(d - 1) * nthreads + t], shfl_down(X, 1 << d), X);
         if (lane == 0) sX[warp] = X;
+        PHASE(7);
         __syncthreads();
+        PHASE(8);
         cplx D = czero();
         for (int w = nwarps - 1; w > warp; --w) D = cfma(spw[w], D, sX[w]);
         cplx xv = shfl_down(cfma(pincb[t], D, X), 1);
@@ -517,6 +527,7 @@ k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ 
 #pragma unroll
         for (int i = RPT - 1; i >= 0; --i) { xv = cfma(M[i], xv, b[i]); b[i] = xv; }
 
+        PHASE(9);
         // ---- solved column back through the stage, one TMA store per warp
 #pragma unroll
         for (int i = 0; i < RPT; ++i) cur[lane * 8 + (i ^ sw)] = b[i];
@@ -534,6 +545,7 @@ k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ 
             }
         }
         __syncwarp();
+        PHASE(10);
         if (++col == n_theta) { col = 0; ++f; }
         if (++slot == STAGES) { slot = 0; parity ^= 1u; }
     }
