@@ -125,6 +125,44 @@ PE3D_API int pe3d_march_device(void* handle, const pe3d_grid* grid, const pe3d_c
                       int64_t* d_clamped, void* stream, pe3d_error* err);
 
 /*
+ * Extended medium for on-device generation of the local term n^2 - 1
+ * (paper_1711_00005_b200/medium.py LayeredMedium; BASELINE cfg3): water
+ * profile (piecewise linear, clamped), fluid bottom below the bathymetry
+ * h(r, theta) = max(depth0 - r tan(slope) cos(theta), min_depth) blended by a
+ * tanh step of width interface_width, attenuation in dB per wavelength,
+ * absorbing layer over the last sponge_points rows, density through the
+ * effective-index term, and an optional perturbation lattice
+ * [lat_nx][lat_ny][lat_nz] (trilinear in x = r cos t, y = r sin t, z).
+ * All pointers are HOST pointers; the library uploads them.
+ */
+typedef struct {
+    double c0;
+    int32_t n_profile;
+    const double* profile_z;
+    const double* profile_c;
+    double water_density, water_alpha;
+    double bottom_speed, bottom_density, bottom_alpha;
+    double bathy_depth0, bathy_slope_deg, bathy_min_depth;
+    int32_t sponge_points;
+    double sponge_max_alpha;
+    double interface_width;
+    const double* lattice;          /* NULL: no perturbation */
+    int32_t lat_nx, lat_ny, lat_nz;
+    double lat_extent_h, lat_spacing_h, lat_spacing_v;
+} pe3d_medium;
+
+/*
+ * pe3d_march_medium_host -- run_frequency (ref marching.py:144-193) for
+ * media that vary with range and azimuth: the local term is generated on
+ * the device every step (at r_j for the explicit side, r_{j+1} for the
+ * implicit side, ref marching.py:110,116), and each depth column is
+ * factored per step.  Buffers as in pe3d_march_host (host pointers).
+ */
+PE3D_API int pe3d_march_medium_host(void* handle, const pe3d_grid* grid, const pe3d_coeffs* coeffs,
+                                    const pe3d_medium* medium, const pe3d_c128* u0, pe3d_c128* u_final,
+                                    double* tl, pe3d_c128* snapshots, int64_t* clamped, pe3d_error* err);
+
+/*
  * pe3d_step_general_host -- replaces range_step (ref marching.py:93-136)
  * for media that vary with range and azimuth: one step with explicit
  * per-point local terms at the old and the new range, host buffers.

@@ -28,7 +28,7 @@ FLAG_NO_GRAPH, FLAG_SERIAL, FLAG_PROFILE = 1, 2, 4
 EXPORTED_SYMBOLS = (
     "pe3d_abi_version", "pe3d_device_count", "pe3d_handle_create", "pe3d_handle_destroy",
     "pe3d_sample_count", "pe3d_march_host", "pe3d_march_device", "pe3d_step_general_host",
-    "pe3d_solve_batch_host", "pe3d_profile_last",
+    "pe3d_solve_batch_host", "pe3d_profile_last", "pe3d_march_medium_host",
 )
 
 
@@ -55,6 +55,17 @@ class Coeffs(C.Structure):
                 ("cy_rhs", C128)]
 
 
+class Medium(C.Structure):
+    _fields_ = [("c0", C.c_double), ("n_profile", C.c_int32), ("profile_z", C.c_void_p),
+                ("profile_c", C.c_void_p), ("water_density", C.c_double), ("water_alpha", C.c_double),
+                ("bottom_speed", C.c_double), ("bottom_density", C.c_double), ("bottom_alpha", C.c_double),
+                ("bathy_depth0", C.c_double), ("bathy_slope_deg", C.c_double), ("bathy_min_depth", C.c_double),
+                ("sponge_points", C.c_int32), ("sponge_max_alpha", C.c_double),
+                ("interface_width", C.c_double), ("lattice", C.c_void_p), ("lat_nx", C.c_int32),
+                ("lat_ny", C.c_int32), ("lat_nz", C.c_int32), ("lat_extent_h", C.c_double),
+                ("lat_spacing_h", C.c_double), ("lat_spacing_v", C.c_double)]
+
+
 class Strided(C.Structure):
     _fields_ = [("ptr", C.c_void_p), ("row_stride", C.c_int64), ("member_stride", C.c_int64)]
 
@@ -75,6 +86,8 @@ _SIGNATURES = {
     "pe3d_solve_batch_host": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, Strided, Strided, Strided,
                                         Strided, _P, C.POINTER(ErrorRecord)]),
     "pe3d_profile_last": (C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_int32)]),
+    "pe3d_march_medium_host": (C.c_int, [_P, C.POINTER(GridParams), C.POINTER(Coeffs), C.POINTER(Medium),
+                                         _P, _P, _P, _P, _P, C.POINTER(ErrorRecord)]),
 }
 
 _lib: Optional[C.CDLL] = None
@@ -154,3 +167,28 @@ def call(fn_name: str, *args) -> None:
     err = ErrorRecord()
     status = getattr(lib, fn_name)(*args, C.byref(err))
     raise_from_record(status, err)
+
+
+def make_medium(medium, keep_alive: list) -> Medium:
+    """pe3d_medium view of a :class:`~.medium.LayeredMedium` (arrays kept
+    alive in ``keep_alive`` for the duration of the call)."""
+    z = np.ascontiguousarray(medium.water.depths, dtype=np.float64)
+    c = np.ascontiguousarray(medium.water.speeds, dtype=np.float64)
+    keep_alive += [z, c]
+    b = medium.bottom
+    m = Medium(c0=medium.c0, n_profile=z.size, profile_z=z.ctypes.data, profile_c=c.ctypes.data,
+               water_density=medium.water_density, water_alpha=medium.water_alpha,
+               bottom_speed=b.speed, bottom_density=b.density, bottom_alpha=b.alpha,
+               bathy_depth0=b.bathymetry.depth0, bathy_slope_deg=b.bathymetry.slope_deg,
+               bathy_min_depth=b.bathymetry.min_depth,
+               sponge_points=medium.sponge.n_points if medium.sponge else 0,
+               sponge_max_alpha=medium.sponge.max_alpha if medium.sponge else 0.0,
+               interface_width=medium.interface_width)
+    p = medium.perturbation
+    if p is not None:
+        lat = np.ascontiguousarray(p.lattice, dtype=np.float64)
+        keep_alive.append(lat)
+        m.lattice = lat.ctypes.data
+        m.lat_nx, m.lat_ny, m.lat_nz = lat.shape
+        m.lat_extent_h, m.lat_spacing_h, m.lat_spacing_v = p.extent_h, p.spacing_h, p.spacing_v
+    return m

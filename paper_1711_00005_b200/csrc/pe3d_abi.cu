@@ -55,6 +55,8 @@ struct Handle {
     DevBuf h_local, h_local2, h_u0, h_final, h_tl, h_snap, h_clamped;
     // solve_batch
     DevBuf sb_in, sb_x, sb_cp, sb_inv, sb_y, sb_q;
+    // extended medium (profile, lattice, two local-term grids)
+    DevBuf med_prof, med_lat, med_local;
     // one cached step-loop graph (reused when a march repeats with identical arguments)
     std::vector<unsigned char> graph_key;
     cudaGraphExec_t graph_exec = nullptr;
@@ -212,7 +214,7 @@ cudaError_t enqueue_steps(Handle* h, const pe3d_grid* g, const MarchPlan& p, con
         const double r_new = g->r_start + j_new * g->delta_r;          // Grid3D.range_at
         cudaError_t e;
         if (p.serial) {
-            e = prof.run(0, [&] { return pe3d::launch_depth_serial(c, A, B, C, d_local, d_local, g->n_depth, 0,
+            e = prof.run(0, [&] { return pe3d::launch_depth_serial(c, A, B, C, d_local, d_local, g->n_depth, 0, 1,
                                                                    h->fail_row.as<int>(), h->fail_mag.as<double>()); });
             if (e == cudaSuccess)
                 e = prof.run(2, [&] { return pe3d::launch_reduce_failures(h->fail_row.as<int>(), h->fail_mag.as<double>(),
@@ -288,7 +290,7 @@ int pe3d_handle_destroy(void* handle) {
     for (DevBuf* b : {&h->field_a, &h->field_b, &h->field_c, &h->loc_tab, &h->mul_tab, &h->fdev, &h->w_abs, &h->err,
                       &h->az_cp, &h->az_inv, &h->az_q, &h->az_ring, &h->fail_row, &h->fail_mag, &h->ring_tab, &h->h_local,
                       &h->h_local2, &h->h_u0, &h->h_final, &h->h_tl, &h->h_snap, &h->h_clamped, &h->sb_in, &h->sb_x,
-                      &h->sb_cp, &h->sb_inv, &h->sb_y, &h->sb_q})
+                      &h->sb_cp, &h->sb_inv, &h->sb_y, &h->sb_q, &h->med_prof, &h->med_lat, &h->med_local})
         b->release();
     if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
     if (h->stream) cudaStreamDestroy(h->stream);
@@ -520,7 +522,7 @@ int pe3d_step_general_host(void* handle, const pe3d_grid* g, const pe3d_coeffs* 
     ea.w_abs = h->w_abs.as<double>();
     CK(pe3d::launch_finish(c, h->h_u0.as<cplx>(), 0, h->field_a.as<cplx>(), g->r_input, ea), "prepare");
     CK(pe3d::launch_depth_serial(c, h->field_a.as<cplx>(), h->field_b.as<cplx>(), h->field_c.as<cplx>(),
-                                 h->h_local.as<cplx>(), h->h_local2.as<cplx>(), slab, NZ, h->fail_row.as<int>(),
+                                 h->h_local.as<cplx>(), h->h_local2.as<cplx>(), slab, NZ, 1, h->fail_row.as<int>(),
                                  h->fail_mag.as<double>()),
        "depth");
     CK(pe3d::launch_reduce_failures(h->fail_row.as<int>(), h->fail_mag.as<double>(), F, NT, j_new, 0, -1, c.err, s),
@@ -566,7 +568,7 @@ int pe3d_solve_batch_host(void* handle, int32_t n, int32_t members, int32_t cycl
     const int64_t total = e_sub + e_main + e_sup + e_rhs;
     CK(h->sb_in.ensure(total * sizeof(cplx)), "alloc");
     CK(h->sb_x.ensure(int64_t(members) * n * sizeof(cplx)), "alloc");
-    for (DevBuf* b : {&h->sb_cp, &h->sb_inv, &h->sb_y, &h->sb_q}) CK(b->ensure(int64_t(members) * n * sizeof(cplx)), "alloc");
+    for (DevBuf* b : {&h->sb_cp, &h->sb_inv, &h->sb_y, &h->sb_q, &h->med_prof, &h->med_lat, &h->med_local}) CK(b->ensure(int64_t(members) * n * sizeof(cplx)), "alloc");
     CK(h->fail_row.ensure(int64_t(members) * sizeof(int)), "alloc");
     CK(h->fail_mag.ensure(int64_t(members) * sizeof(double)), "alloc");
     CK(h->err.ensure(sizeof(pe3d::DevError)), "alloc");
@@ -604,6 +606,159 @@ int pe3d_solve_batch_host(void* handle, int32_t n, int32_t members, int32_t cycl
         return st;
     }
     CK(cudaMemcpyAsync(x, h->sb_x.ptr, int64_t(members) * n * sizeof(cplx), cudaMemcpyDeviceToHost, s), "D2H");
+    CK(cudaStreamSynchronize(s), "sync");
+    return PE3D_OK;
+}
+
+int pe3d_march_medium_host(void* handle, const pe3d_grid* g, const pe3d_coeffs* coeffs, const pe3d_medium* md,
+                           const pe3d_c128* u0, pe3d_c128* u_final, double* tl, pe3d_c128* snapshots,
+                           int64_t* clamped, pe3d_error* err) {
+    Handle* h = static_cast<Handle*>(handle);
+    if (!h) return bad_arg(err, "null handle");
+    int st = check_grid(g, coeffs, err);
+    if (st != PE3D_OK) return st;
+    if (!md || !u0 || md->n_profile < 1 || !md->profile_z || !md->profile_c) return bad_arg(err, "medium / u0");
+    if (!(md->interface_width > 0)) return bad_arg(err, "interface_width > 0");
+    CK(cudaSetDevice(h->device), "cudaSetDevice");
+    cudaStream_t s = h->stream;
+    const int F = g->n_freq, NT = g->n_theta, NZ = g->n_depth, n_tiles = (NZ + 7) / 8;
+    const int64_t slab = int64_t(NT) * NZ, field = int64_t(F) * n_tiles * NT * 8;
+    const int S = pe3d_sample_count(g->n_steps, g->output_stride);
+    std::vector<pe3d::FreqDev> fd = freq_table(g, coeffs);
+    for (DevBuf* b : {&h->field_a, &h->field_b, &h->field_c}) CK(b->ensure(field * sizeof(cplx)), "alloc");
+    CK(h->fdev.ensure(F * sizeof(pe3d::FreqDev)), "alloc");
+    CK(h->err.ensure(sizeof(pe3d::DevError)), "alloc");
+    CK(h->w_abs.ensure(int64_t(S) * F * sizeof(double)), "alloc");
+    CK(h->az_cp.ensure(int64_t(F) * NT * sizeof(cplx)), "alloc");
+    CK(h->az_inv.ensure(int64_t(F) * NT * sizeof(cplx)), "alloc");
+    CK(h->az_q.ensure(int64_t(F) * NT * sizeof(cplx)), "alloc");
+    CK(h->az_ring.ensure(int64_t(F) * 2 * sizeof(cplx)), "alloc");
+    CK(h->fail_row.ensure(int64_t(F) * (NT > NZ ? NT : NZ) * sizeof(int)), "alloc");
+    CK(h->fail_mag.ensure(int64_t(F) * (NT > NZ ? NT : NZ) * sizeof(double)), "alloc");
+    CK(h->med_local.ensure(2 * int64_t(F) * slab * sizeof(cplx)), "alloc");
+    CK(h->med_prof.ensure(2 * md->n_profile * sizeof(double)), "alloc");
+    const int64_t n_lat = md->lattice ? int64_t(md->lat_nx) * md->lat_ny * md->lat_nz : 0;
+    if (n_lat) CK(h->med_lat.ensure(n_lat * sizeof(double)), "alloc");
+    CK(h->h_u0.ensure(F * slab * sizeof(cplx)), "alloc");
+    CK(h->h_clamped.ensure(F * sizeof(int64_t)), "alloc");
+    if (u_final) CK(h->h_final.ensure(F * slab * sizeof(cplx)), "alloc");
+    if (tl) CK(h->h_tl.ensure(int64_t(F) * S * slab * sizeof(double)), "alloc");
+    if (snapshots) CK(h->h_snap.ensure(int64_t(F) * S * slab * sizeof(cplx)), "alloc");
+
+    std::vector<double> wabs(int64_t(S) * F);
+    for (int k = 0; k < S; ++k) {
+        const double r = (k == 0) ? g->r_input : g->r_start + (g->first_index + int64_t(k) * g->output_stride) * g->delta_r;
+        for (int f = 0; f < F; ++f) wabs[int64_t(k) * F + f] = hankel_abs_host(coeffs[f].k0, r);
+    }
+    pe3d::DevError de0{NO_ERROR, 0, 0};
+    CK(cudaMemcpyAsync(h->fdev.ptr, fd.data(), F * sizeof(pe3d::FreqDev), cudaMemcpyHostToDevice, s), "H2D");
+    CK(cudaMemcpyAsync(h->w_abs.ptr, wabs.data(), wabs.size() * sizeof(double), cudaMemcpyHostToDevice, s), "H2D");
+    CK(cudaMemcpyAsync(h->err.ptr, &de0, sizeof(de0), cudaMemcpyHostToDevice, s), "H2D");
+    CK(cudaMemcpyAsync(h->med_prof.ptr, md->profile_z, md->n_profile * sizeof(double), cudaMemcpyHostToDevice, s), "H2D");
+    CK(cudaMemcpyAsync(h->med_prof.as<double>() + md->n_profile, md->profile_c, md->n_profile * sizeof(double),
+                       cudaMemcpyHostToDevice, s), "H2D");
+    if (n_lat) CK(cudaMemcpyAsync(h->med_lat.ptr, md->lattice, n_lat * sizeof(double), cudaMemcpyHostToDevice, s), "H2D");
+    CK(cudaMemcpyAsync(h->h_u0.ptr, u0, F * slab * sizeof(cplx), cudaMemcpyHostToDevice, s), "H2D");
+    CK(cudaMemsetAsync(h->h_clamped.ptr, 0, F * sizeof(int64_t), s), "memset");
+    cudaStreamSynchronize(s);   // host staging (vectors) must outlive the copies
+
+    pe3d::MediumDev M{};
+    M.c0 = md->c0;
+    M.n_prof = md->n_profile;
+    M.pz = h->med_prof.as<double>();
+    M.pc = h->med_prof.as<double>() + md->n_profile;
+    M.rho_w = md->water_density;
+    M.alpha_w = md->water_alpha;
+    M.c_b = md->bottom_speed;
+    M.rho_b = md->bottom_density;
+    M.alpha_b = md->bottom_alpha;
+    M.h0 = md->bathy_depth0;
+    M.tan_slope = std::tan(md->bathy_slope_deg * 3.141592653589793 / 180.0);
+    M.hmin = md->bathy_min_depth;
+    M.sponge_n = md->sponge_points;
+    M.sponge_max = md->sponge_max_alpha;
+    M.w = md->interface_width;
+    M.lat = n_lat ? h->med_lat.as<double>() : nullptr;
+    M.nx = md->lat_nx; M.ny = md->lat_ny; M.nz = md->lat_nz;
+    M.ext_h = md->lat_extent_h; M.dh = md->lat_spacing_h; M.dv = md->lat_spacing_v;
+    M.eta = 1.0 / (40.0 * 3.141592653589793 * std::log10(std::exp(1.0)));
+
+    pe3d::LaunchCtx c{};
+    c.n_freq = F; c.n_theta = NT; c.n_depth = NZ; c.n_tiles = n_tiles;
+    c.sector = g->topology == PE3D_SECTOR;
+    c.num_sms = h->num_sms;
+    c.delta_theta = g->delta_theta;
+    c.fdev = h->fdev.as<pe3d::FreqDev>();
+    c.err = h->err.as<pe3d::DevError>();
+    c.stream = s;
+    cplx* L[2] = {h->med_local.as<cplx>(), h->med_local.as<cplx>() + int64_t(F) * slab};
+    cplx* A = h->field_a.as<cplx>();
+    cplx* B = h->field_b.as<cplx>();
+    cplx* Cc = h->field_c.as<cplx>();
+    const bool periodic = g->topology == PE3D_PERIODIC;
+    cplx* d_final = u_final ? h->h_final.as<cplx>() : nullptr;
+    double* d_tl = tl ? h->h_tl.as<double>() : nullptr;
+    cplx* d_snap = snapshots ? h->h_snap.as<cplx>() : nullptr;
+    int64_t* d_cl = h->h_clamped.as<int64_t>();
+    if (periodic && g->n_steps > 0) {
+        const int64_t E = pe3d::ring_table_elems(NT);
+        CK(h->ring_tab.ensure(int64_t(g->n_steps) * F * E * sizeof(cplx)), "alloc ring table");
+        CK(pe3d::launch_ring_setup(c, h->ring_tab.as<cplx>(), g->n_steps, g->first_index, g->r_start, g->delta_r),
+           "ring setup");
+    }
+    // starter: local term at the input range, boundary, TL sample 0, first temp
+    CK(pe3d::launch_medium_local(c, M, L[0], g->delta_z, g->r_input), "medium");
+    pe3d::EpilogueArgs ea0{};
+    ea0.tl = d_tl;
+    ea0.snap = d_snap;
+    ea0.final_out = g->n_steps == 0 ? d_final : nullptr;
+    ea0.clamped = d_cl;
+    ea0.w_abs = h->w_abs.as<double>();
+    ea0.n_samples = S;
+    ea0.sample = 0;
+    ea0.periodic = periodic;
+    ea0.write_temp = g->n_steps > 0;
+    CK(pe3d::launch_finish(c, h->h_u0.as<cplx>(), 0, A, g->r_input, ea0), "prepare");
+    const int64_t E = periodic ? pe3d::ring_table_elems(NT) : 0;
+    for (int k = 0; k < g->n_steps; ++k) {
+        const int j_new = g->first_index + k + 1;
+        const double r_new = g->r_start + j_new * g->delta_r;
+        cplx* now = L[k & 1];
+        cplx* nxt = L[(k + 1) & 1];
+        CK(pe3d::launch_medium_local(c, M, nxt, g->delta_z, r_new), "medium");
+        CK(pe3d::launch_depth_serial(c, A, B, Cc, now, nxt, int64_t(NZ) * NT, 1, NT, h->fail_row.as<int>(),
+                                     h->fail_mag.as<double>()),
+           "depth");
+        CK(pe3d::launch_reduce_failures(h->fail_row.as<int>(), h->fail_mag.as<double>(), F, NT, j_new, 0, -1, c.err, s),
+           "reduce");
+        pe3d::EpilogueArgs ea{};
+        const bool record = ((k + 1) % g->output_stride) == 0;
+        ea.tl = record ? d_tl : nullptr;
+        ea.snap = record ? d_snap : nullptr;
+        ea.final_out = (k == g->n_steps - 1) ? d_final : nullptr;
+        ea.clamped = d_cl;
+        ea.n_samples = S;
+        ea.sample = (k + 1) / g->output_stride;
+        ea.w_abs = h->w_abs.as<double>() + int64_t(ea.sample) * F;
+        ea.periodic = periodic;
+        ea.write_temp = (k < g->n_steps - 1);
+        if (periodic) {
+            CK(pe3d::launch_azimuth_scan(c, B, A, h->ring_tab.as<cplx>() + int64_t(k) * F * E, r_new, ea), "azimuth");
+        } else {
+            CK(pe3d::launch_azimuth_serial(c, B, Cc, h->az_cp.as<cplx>(), h->az_inv.as<cplx>(), h->az_q.as<cplx>(),
+                                           h->az_ring.as<cplx>(), r_new, j_new),
+               "azimuth");
+            CK(pe3d::launch_finish(c, Cc, 1, A, r_new, ea), "finish");
+        }
+    }
+    st = decode_error(h, s, err);
+    if (st != PE3D_OK) return st;
+    if (u_final) CK(cudaMemcpyAsync(u_final, h->h_final.ptr, F * slab * sizeof(cplx), cudaMemcpyDeviceToHost, s), "D2H");
+    if (tl) CK(cudaMemcpyAsync(tl, h->h_tl.ptr, int64_t(F) * S * slab * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
+    if (snapshots)
+        CK(cudaMemcpyAsync(snapshots, h->h_snap.ptr, int64_t(F) * S * slab * sizeof(cplx), cudaMemcpyDeviceToHost, s),
+           "D2H");
+    if (clamped) CK(cudaMemcpyAsync(clamped, h->h_clamped.ptr, F * sizeof(int64_t), cudaMemcpyDeviceToHost, s), "D2H");
     CK(cudaStreamSynchronize(s), "sync");
     return PE3D_OK;
 }

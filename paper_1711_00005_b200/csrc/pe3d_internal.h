@@ -29,6 +29,23 @@ struct EpilogueArgs {
     int write_temp;
 };
 
+// Device view of an extended medium (pe3d_medium in the public header).
+struct MediumDev {
+    double c0;
+    int n_prof;
+    const double* pz;
+    const double* pc;
+    double rho_w, alpha_w, c_b, rho_b, alpha_b;
+    double h0, tan_slope, hmin;
+    int sponge_n;
+    double sponge_max;
+    double w;
+    const double* lat;
+    int nx, ny, nz;
+    double ext_h, dh, dv;
+    double eta;
+};
+
 struct LaunchCtx {
     int n_freq, n_theta, n_depth, n_tiles;
     int sector;
@@ -52,8 +69,9 @@ cudaError_t launch_azimuth_scan(const LaunchCtx& c, const cplx* src, cplx* dst, 
 cudaError_t launch_finish(const LaunchCtx& c, const cplx* src, int src_tiled, cplx* dst, double r,
                           const EpilogueArgs& ea);
 cudaError_t launch_depth_serial(const LaunchCtx& c, const cplx* src, cplx* dst, cplx* scratch, const cplx* local_now,
-                                const cplx* local_new, int64_t fstride, int64_t mstride, int* fail_row,
+                                const cplx* local_new, int64_t fstride, int64_t mstride, int64_t lstride, int* fail_row,
                                 double* fail_mag);
+cudaError_t launch_medium_local(const LaunchCtx& c, const MediumDev& M, cplx* local, double dz, double r);
 cudaError_t launch_azimuth_serial(const LaunchCtx& c, const cplx* src, cplx* dst, cplx* cp, cplx* inv, cplx* qv,
                                   cplx* ring, double r_new, int step_for_error);
 cudaError_t launch_solve_batch(int n, int members, int cyclic, StridedC sub, StridedC mainv, StridedC sup,

@@ -20,7 +20,8 @@ namespace pe3d {
 // x is written to dst (device tiles), cp to `scratch` (device tiles).
 __global__ void k_depth_serial(const cplx* __restrict__ src, cplx* __restrict__ dst, cplx* __restrict__ scratch,
                                const cplx* __restrict__ local_now, const cplx* __restrict__ local_new,
-                               int64_t local_fstride, int64_t local_mstride, const FreqDev* __restrict__ fdev,
+                               int64_t local_fstride, int64_t local_mstride, int64_t local_lstride,
+                               const FreqDev* __restrict__ fdev,
                                int n_freq, int n_theta, int n_tiles, int n_depth, int sector,
                                int* __restrict__ fail_row, double* __restrict__ fail_mag) {
     const int gid = blockIdx.x * blockDim.x + threadIdx.x;
@@ -42,10 +43,10 @@ __global__ void k_depth_serial(const cplx* __restrict__ src, cplx* __restrict__ 
         if (l == 0) d2 = csub(t_next, crmul(2.0, t_cur));
         else if (l == n_depth - 1) d2 = csub(t_prev, crmul(2.0, t_cur));
         else d2 = cadd(csub(t_next, crmul(2.0, t_cur)), t_prev);
-        const cplx xt = cadd(cmul(ln[l], t_cur), crmul(fd.s_z, d2));
+        const cplx xt = cadd(cmul(ln[l * local_lstride], t_cur), crmul(fd.s_z, d2));
         cplx rhs = cadd(t_cur, cmul(fd.cx_rhs, xt));
         if (l == 0 || zero_col) rhs = czero();
-        const cplx loc = lw[l];
+        const cplx loc = lw[l * local_lstride];
         const cplx main_l = (l == 0) ? cone() : cadd(cone(), cmul(fd.cx_lhs, mk(loc.re - two_s, loc.im)));
         const cplx denom = (l == 0) ? main_l : csub(main_l, cmul(fd.off_z, cp_prev));
         if (failed_row == 0x7fffffff && cabs(denom) < PIVOT_FLOOR) { failed_row = l; failed_mag = cabs(denom); }
@@ -300,10 +301,10 @@ __global__ void k_zero(cplx* p, int64_t n) {
 // ------------------------------------------------------------ launchers
 
 cudaError_t launch_depth_serial(const LaunchCtx& c, const cplx* src, cplx* dst, cplx* scratch, const cplx* local_now,
-                                const cplx* local_new, int64_t fstride, int64_t mstride, int* fail_row,
+                                const cplx* local_new, int64_t fstride, int64_t mstride, int64_t lstride, int* fail_row,
                                 double* fail_mag) {
     const int total = c.n_freq * c.n_theta;
-    k_depth_serial<<<(total + 127) / 128, 128, 0, c.stream>>>(src, dst, scratch, local_now, local_new, fstride, mstride,
+    k_depth_serial<<<(total + 127) / 128, 128, 0, c.stream>>>(src, dst, scratch, local_now, local_new, fstride, mstride, lstride,
                                                               c.fdev, c.n_freq, c.n_theta, c.n_tiles, c.n_depth,
                                                               c.sector, fail_row, fail_mag);
     return cudaGetLastError();

@@ -102,6 +102,12 @@ def _grid_params(grid: Grid3D, n_freq: int, n_steps: int, stride: int, first_ind
         grid.delta_r, grid.delta_theta, grid.delta_z, grid.r_start, r_input)
 
 
+def _device_medium(env) -> bool:
+    """The medium can be generated on the device (a LayeredMedium)."""
+    from .medium import LayeredMedium
+    return isinstance(getattr(env, "medium", None), LayeredMedium)
+
+
 def _local_column(env, grid: Grid3D, r: float, k0: float) -> np.ndarray:
     """n^2 - 1 over depth for a range-independent medium."""
     return np.ascontiguousarray(local_term_grid(env, grid, r, k0)[0])
@@ -130,6 +136,11 @@ def range_step(state: MarchState, device: int = 0) -> MarchState:
         g = _grid_params(grid, 1, 1, 1, j, slab.range_m)
         _native.call("pe3d_march_host", h, g, coeffs, _native.ptr(local), _native.ptr(u_in),
                      _native.ptr(u_out), None, None, None)
+    elif _device_medium(env):
+        keep: list = []
+        g = _grid_params(grid, 1, 1, 1, j, slab.range_m)
+        _native.call("pe3d_march_medium_host", h, g, coeffs, _native.make_medium(env.medium, keep),
+                     _native.ptr(u_in), _native.ptr(u_out), None, None, None)
     else:
         now = np.ascontiguousarray(local_term_grid(env, grid, slab.range_m, k0))
         new = np.ascontiguousarray(local_term_grid(env, grid, r_new, k0))
@@ -192,6 +203,13 @@ def march_frequencies(config, frequencies: Sequence[float], n_steps: Optional[in
                          _native.ptr(final[lo:hi]), _native.ptr(tl[lo:hi]),
                          _native.ptr(snaps[lo:hi]) if keep_snapshots else None,
                          _native.ptr(clamped[lo:hi]))
+    elif _device_medium(env):
+        keep: list = []
+        med = _native.make_medium(env.medium, keep)
+        g = _grid_params(grid, F, steps, stride, 0, grid.r_start, flags)
+        cf = _native.make_coeffs(k0s, coeffs)
+        _native.call("pe3d_march_medium_host", h, g, cf, med, _native.ptr(u0), _native.ptr(final),
+                     _native.ptr(tl), _native.ptr(snaps) if keep_snapshots else None, _native.ptr(clamped))
     else:
         _march_general(config, k0s, coeffs, u0, steps, stride, tl, snaps, final, clamped, h)
 
