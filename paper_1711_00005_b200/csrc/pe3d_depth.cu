@@ -382,7 +382,8 @@ k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ 
     const int nwarps = nthreads >> 5;
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     // 1024-B aligned stage ring (128-B swizzle atoms), then barriers and tables
-    cplx* base = reinterpret_cast<cplx*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // offset arithmetic on the shared array keeps the shared address space (LDS/STS, not generic LD/ST)
+    cplx* base = reinterpret_cast<cplx*>(smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u));
     cplx* stage = base + warp * (STAGES * 256);
     cplx* mf = base + nwarps * (STAGES * 256);      // [4][nthreads]
     cplx* mb = mf + 4 * nthreads;
