@@ -195,6 +195,31 @@ PE3D_API int pe3d_solve_batch_host(void* handle, int32_t n, int32_t members, int
                           pe3d_strided rhs, pe3d_c128* x, pe3d_error* err);
 
 /*
+ * Slab-decomposed march of ONE large grid over nranks GPUs (SURVEY.md §8(e),
+ * BASELINE cfg5): the depth sweep runs on azimuth slabs (nranks column
+ * ranges), the azimuth sweep on depth slabs (nranks tile ranges), joined
+ * twice per step by an equal-split all-to-all (NCCL send/recv pairs), with
+ * the ring sweep reading/writing the rank-chunked layout the all-to-all
+ * delivers (no pack/unpack kernels).  No reference counterpart: the
+ * reference never splits one frequency's grid.
+ *
+ * nccl_id == NULL: nranks VIRTUAL ranks driven by this process on its one
+ *   device (device-to-device copies as the transport); u0 / u_final are full
+ *   [n_theta][n_depth] slabs and tl is [S][n_theta][n_depth].
+ * nccl_id != NULL: this process is rank `rank` of nranks (one GPU each; id
+ *   from pe3d_slab_unique_id on rank 0, broadcast by the caller); u0 /
+ *   u_final are this rank's depth slab [n_theta][n_depth/nranks] and tl is
+ *   [S][n_theta][n_depth/nranks].
+ * Requirements: n_freq == 1, periodic, n_theta % nranks == 0,
+ * n_depth % (8*nranks) == 0.  *ms_steps receives the device time of the
+ * step loop (CUDA events), for measurement.
+ */
+PE3D_API int pe3d_slab_unique_id(void* out, int32_t bytes);
+PE3D_API int pe3d_march_slab(void* handle, const pe3d_grid* grid, const pe3d_coeffs* coeffs, int32_t nranks,
+                             int32_t rank, const void* nccl_id, const pe3d_c128* local, const pe3d_c128* u0,
+                             pe3d_c128* u_final, double* tl, int64_t* clamped, double* ms_steps, pe3d_error* err);
+
+/*
  * pe3d_profile_last -- kernel timings of the last march run with
  * PE3D_FLAG_PROFILE on this handle: ms[k] is the summed CUDA-event time and
  * launches[k] the launch count of kernel class k (0 depth sweep, 1 azimuth

@@ -40,6 +40,7 @@ from .parallel import (
     FarmFailure, FarmReport, block_ranges, distributed_frequency_farm, frequency_farm, rank_frequencies,
     static_assignment,
 )
+from .slab import SlabResult, distributed_slab_march, slab_march
 from .tridiag import CYCLIC, OPEN, SolveBatch, TriDiagSystem, solve_batch, solve_cyclic, solve_thomas
 
 __all__ = [name for name in dir() if not name.startswith("_")]

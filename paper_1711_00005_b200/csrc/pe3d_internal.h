@@ -27,7 +27,21 @@ struct EpilogueArgs {
     int sample;
     int periodic;
     int write_temp;
+    // Slab march: the ring tiles of this rank hold global
+    // rows row_offset + l, and rings may be stored rank-chunked: element m of
+    // the ring of (f, tile) is at ring_base + m*8 + (m / chunk_cols)*chunk_gap.
+    // Standard layout: row_offset 0, chunk_cols = n_theta, chunk_gap = 0.
+    int row_offset;
+    int chunk_cols;
+    int64_t chunk_gap;
 };
+
+__host__ __device__ __forceinline__ int64_t ring_base(int f, int tile, int n_tiles, int n_theta, int chunk_cols) {
+    return (int64_t(f) * n_tiles * n_theta + int64_t(tile) * chunk_cols) * 8;
+}
+__host__ __device__ __forceinline__ int64_t ring_off(int m, int chunk_cols, int64_t chunk_gap) {
+    return int64_t(m) * 8 + (chunk_gap ? int64_t(m / chunk_cols) * chunk_gap : 0);
+}
 
 // Device view of an extended medium (pe3d_medium in the public header).
 struct MediumDev {

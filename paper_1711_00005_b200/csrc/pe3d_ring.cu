@@ -176,7 +176,8 @@ __device__ __forceinline__ void ring_epilogue(cplx (&u)[RT][L], int q, int n_chu
             if (k >= nvalid) break;
             const cplx um = k ? u[h][k - 1] : prev;
             const cplx up = (k + 1 < L && k < nvalid - 1) ? u[h][(k + 1) % L] : next;
-            stc_stream(dst_row + int64_t(m0 + k) * 8, cfma(b1, u[h][k], cmul(b2, cadd(up, um))));
+            stc_stream(dst_row + ring_off(m0 + k, ea.chunk_cols, ea.chunk_gap),
+                       cfma(b1, u[h][k], cmul(b2, cadd(up, um))));
         }
     }
 }
@@ -408,7 +409,7 @@ k_azimuth_pipe(const cplx* __restrict__ src, cplx* __restrict__ dst, const cplx*
 #pragma unroll
         for (int h = 0; h < RT; ++h) {
             const int l = l0 + i + h * RWT;
-            if (l == 0 || l >= n_depth) {
+            if (l + ea.row_offset == 0 || l >= n_depth) {
 #pragma unroll
                 for (int k = 0; k < L; ++k) v[h][k] = czero();
             }
@@ -458,13 +459,19 @@ k_azimuth_warp(const cplx* __restrict__ src, cplx* __restrict__ dst, const cplx*
     const int64_t it0 = int64_t(blockIdx.x) * items_per_cta;
     const int64_t it1 = it0 + items_per_cta < total_items ? it0 + items_per_cta : total_items;
     if (it0 >= it1) return;
+    const int C = ea.chunk_cols ? ea.chunk_cols : NT;   // 0: standard layout
+    const int64_t gap = ea.chunk_gap;
+    auto item_base = [&](int64_t item) {
+        const int fi = int(item / n_tiles);
+        return ring_base(fi, int(item - int64_t(fi) * n_tiles), n_tiles, NT, C);
+    };
     auto fetch = [&](int64_t item, int st) {
-        const cplx* g = src + item * ITEM;
+        const cplx* g = src + item_base(item);
         cplx* d = smem + st * ITEM;
 #pragma unroll
         for (int j = 0; j < PER; ++j) {
             const int e = j * NTHR + tid;
-            cp_async16(d + ring_slot<L>(e >> 3, e & 7), g + e);
+            cp_async16(d + ring_slot<L>(e >> 3, e & 7), g + e + (gap ? int64_t((e >> 3) / C) * gap : 0));
         }
     };
 #pragma unroll
@@ -561,7 +568,7 @@ k_azimuth_warp(const cplx* __restrict__ src, cplx* __restrict__ dst, const cplx*
 #pragma unroll
         for (int h = 0; h < RT; ++h) {
             const int l = l0 + h;
-            if (l == 0 || l >= n_depth) {
+            if (l + ea.row_offset == 0 || l >= n_depth) {
 #pragma unroll
                 for (int k = 0; k < L; ++k) v[h][k] = czero();
             }
@@ -598,11 +605,11 @@ k_azimuth_warp(const cplx* __restrict__ src, cplx* __restrict__ dst, const cplx*
         }
         if (ea.write_temp) {
             __syncthreads();                        // every warp's rows written
-            cplx* g = dst + item * ITEM;
+            cplx* g = dst + item_base(item);
 #pragma unroll
             for (int j = 0; j < PER; ++j) {
                 const int e = j * NTHR + tid;
-                stc_stream(g + e, stg[ring_slot<L>(e >> 3, e & 7)]);
+                stc_stream(g + e + (gap ? int64_t((e >> 3) / C) * gap : 0), stg[ring_slot<L>(e >> 3, e & 7)]);
             }
         }
         if (++tile == n_tiles) { tile = 0; ++f; }
@@ -630,18 +637,20 @@ k_azimuth_direct(const cplx* __restrict__ src, cplx* __restrict__ dst, const cpl
     const int f = blockIdx.y;
     const int m0 = q * L;
     const int nvalid = in_range ? min(L, n_theta - m0) : 0;
-    cplx* tile_base = dst + (int64_t(f) * n_tiles + tile) * n_theta * 8;
-    const cplx* src_tile = src + (int64_t(f) * n_tiles + tile) * n_theta * 8 + row0 + i;
+    const int64_t rb = ring_base(f, tile, n_tiles, n_theta, ea.chunk_cols ? ea.chunk_cols : n_theta);
+    cplx* tile_base = dst + rb;
+    const cplx* src_tile = src + rb + row0 + i;
     cplx v[1][L];
 #pragma unroll
-    for (int k = 0; k < L; ++k) v[0][k] = (k < nvalid) ? ldc_stream(src_tile + int64_t(m0 + k) * 8) : czero();
+    for (int k = 0; k < L; ++k)
+        v[0][k] = (k < nvalid) ? ldc_stream(src_tile + ring_off(m0 + k, ea.chunk_cols, ea.chunk_gap)) : czero();
     cplx* T = smem + lay.table;
     for (int e = t; e < E; e += blockDim.x) T[e] = table[int64_t(f) * E + e];
     __syncthreads();
     ring_solve<L, RW, 1, false>(v, T, q, i, lane, warp, nwarps, n_theta, nvalid, smem + lay.sW, smem + lay.sV,
                                 smem + lay.sTot);
     const int l = tile * 8 + row0 + i;
-    if (l == 0 || l >= n_depth) {
+    if (l + ea.row_offset == 0 || l >= n_depth) {
 #pragma unroll
         for (int k = 0; k < L; ++k) v[0][k] = czero();
     }
@@ -673,16 +682,16 @@ k_finish(const cplx* __restrict__ src, int src_tiled, cplx* __restrict__ dst, co
     const double s = azimuth_scale(fd.k0, r, delta_theta);
     const int m0 = q * L;
     const int nvalid = in_range ? min(L, n_theta - m0) : 0;
-    const int64_t tile_off = (int64_t(f) * n_tiles + tile) * n_theta * 8;
+    const int64_t tile_off = ring_base(f, tile, n_tiles, n_theta, ea.chunk_cols ? ea.chunk_cols : n_theta);
     cplx u[1][L];
 #pragma unroll
     for (int k = 0; k < L; ++k) {
         cplx v = czero();
         const int m = m0 + k;
         if (k < nvalid && l < n_depth) {
-            v = src_tiled ? ldc(src + tile_off + int64_t(m) * 8 + row0 + i)
+            v = src_tiled ? ldc(src + tile_off + ring_off(m, ea.chunk_cols, ea.chunk_gap) + row0 + i)
                           : ldc(src + (int64_t(f) * n_theta + m) * n_depth + l);
-            if (l == 0 || (!ea.periodic && (m == 0 || m == n_theta - 1))) v = czero();
+            if (l + ea.row_offset == 0 || (!ea.periodic && (m == 0 || m == n_theta - 1))) v = czero();
         }
         u[0][k] = v;
     }
@@ -783,7 +792,7 @@ cudaError_t launch_azimuth_scan(const LaunchCtx& c, const cplx* src, cplx* dst, 
     const RingLayout rl = plan.lay;
     const int nthreads = round32(RW * rl.n_chunks);
     const size_t stage_bytes = sizeof(cplx) * size_t(RW) * c.n_theta;
-    if (RW == 8 && 2 * stage_bytes <= 110 * 1024) {
+    if (RW == 8 && 2 * stage_bytes <= 110 * 1024 && ea.chunk_gap == 0) {
         const int stages = (3 * stage_bytes <= 72 * 1024) ? 3 : 2;
         const int64_t items = int64_t(c.n_freq) * c.n_tiles;
         constexpr int RT = 2;

@@ -65,3 +65,57 @@ def test_gloo_two_ranks_static_blocks(fail_freq):
         else:
             assert results[i][1] == f and results[i][2] == (0 if i < 4 else 1)
     assert failures == ([] if fail_freq is None else [(freqs.index(fail_freq), fail_freq)])
+
+
+def _slab_worker(rank, world, port, queue):
+    import numpy as np
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1711_00005_b200 import configs, slab
+    seen = {}
+
+    def fake_call(name, handle, g, coeffs, nranks, rnk, id_buf, local, u0, final, tl, clamped, ms):
+        seen.update(name=name, nranks=nranks, rank=rnk, id=bytes(id_buf), n_depth=g.n_depth)
+
+    slab.new_nccl_id = lambda: bytes(range(128))
+    slab._native.call = fake_call
+    slab._native.handle = lambda device=0: None
+    cfg = configs.build("cfg5", n_range=3)
+    res = slab.distributed_slab_march(cfg, 500.0, device=0, n_steps=2)
+    queue.put((rank, seen, res.final.shape, res.tl_field.shape))
+    dist.destroy_process_group()
+
+
+def test_gloo_slab_march_id_broadcast_and_slabs():
+    ctx = mp.get_context("spawn")
+    queue = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_slab_worker, args=(r, 2, port, queue)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = dict((lambda t: (t[0], t[1:]))(queue.get(timeout=180)) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank in (0, 1):
+        seen, final_shape, tl_shape = out[rank]
+        assert seen["name"] == "pe3d_march_slab" and seen["nranks"] == 2 and seen["rank"] == rank
+        assert seen["id"] == bytes(range(128))            # rank 0's NCCL id reached every rank
+        assert final_shape == (4096, 2048)                 # this rank's depth slab
+        assert tl_shape == (2, 4096, 2048)
+
+
+def test_slab_shape_rules():
+    import math
+    from paper_1711_00005_b200.environment import Grid3D
+    from paper_1711_00005_b200.errors import InvariantError
+    from paper_1711_00005_b200.slab import check_slab_shape, depth_slab
+    import numpy as np
+    g = Grid3D(3, 64, 256, 1.0, 2 * math.pi / 64, 1.0, 1.0)
+    check_slab_shape(g, 4)
+    with pytest.raises(InvariantError):
+        check_slab_shape(g, 3)
+    v = np.arange(64 * 256).reshape(64, 256)
+    parts = [depth_slab(v, 4, r) for r in range(4)]
+    assert np.array_equal(np.concatenate(parts, axis=1), v)
