@@ -103,7 +103,7 @@ def test_gloo_slab_march_id_broadcast_and_slabs():
         assert seen["name"] == "pe3d_march_slab" and seen["nranks"] == 2 and seen["rank"] == rank
         assert seen["id"] == bytes(range(128))            # rank 0's NCCL id reached every rank
         assert final_shape == (4096, 2048)                 # this rank's depth slab
-        assert tl_shape == (2, 4096, 2048)
+        assert tl_shape == (1, 4096, 2048)                 # stride 100: starter sample only
 
 
 def test_slab_shape_rules():
