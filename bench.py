@@ -338,11 +338,48 @@ def run_gpu_arm(a, rank, world, local):
         torch.distributed.destroy_process_group()
 
 
+def run_slab_arm(a, rank, world, local):
+    """cfg5 on N GPUs: one grid, slab-decomposed (NCCL all-to-all transposes)."""
+    import torch
+    import torch.distributed as dist
+    from paper_1711_00005_b200 import slab
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = workload(a.workload, max(a.steps, a.warmup))
+    grid = cfg.grid
+    f = cfg.source.frequencies[0]
+    slab.distributed_slab_march(cfg, f, device=local, n_steps=a.warmup)
+    dist.barrier()
+    with ClockSampler(local) as clocks:
+        res = slab.distributed_slab_march(cfg, f, device=local, n_steps=a.steps)
+    t = torch.tensor([res.step_ms], device="cuda", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    value = grid.n_azimuth * grid.n_depth * a.steps / (ms / 1e3)
+    if rank == 0:
+        peak, kind = peaks()
+        print(json.dumps({
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "c128", "data": "synthetic",
+            "config": {"workload": a.workload, "frequencies": 1, "n_theta": grid.n_azimuth, "n_depth": grid.n_depth,
+                       "parallelism": f"slab x{world}: depth sweep on azimuth slabs, azimuth sweep on depth slabs, "
+                                      "2 NCCL all-to-all per step"},
+            "roofline": {"bound": "hbm+nvlink", "achieved": STEP_BYTES_PER_POINT * value / world / 1e9, "peak": peak,
+                         "unit": "GB/s", "frac": STEP_BYTES_PER_POINT * value / world / 1e9 / peak,
+                         "peak_source": kind, "traffic": None},
+            "cpu_baseline": None, "e2e": None, "gpu_launches": None, "clocks": clocks.summary()}), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     a = parse()
     rank, world, local = dist_env()
     if a.impl == "reference":
         run_reference_arm(a, rank, world)
+        return
+    if a.workload == "cfg5" and world > 1:
+        run_slab_arm(a, rank, world, local)
         return
     run_gpu_arm(a, rank, world, local)
 
