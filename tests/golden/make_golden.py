@@ -174,12 +174,34 @@ def full_size_fixture(name, frequency, n_steps):
     print(f"{name} f={frequency}: {wall / n_steps:.2f} s/step (reference)")
 
 
+def output_fixture():
+    """TL files written by the reference's own writers (ref output.py:60-122)
+    for a fixed small result, plus the inputs that produced them."""
+    import math as _m
+    import pe3d.output as ref_out
+    out = HERE / "output"
+    out.mkdir(exist_ok=True)
+    grid = pe3d.Grid3D(10, 4, 5, 5.0, 2 * _m.pi / 4, 3.0, 5.0)
+    rng = np.random.default_rng(77)
+    tl = 40.0 + 30.0 * rng.random((3, 4, 5))
+    tl[1, 2, 3] = 300.0
+    final = rng.standard_normal((4, 5)) + 1j * rng.standard_normal((4, 5))
+    res = pe3d.FrequencyResult(frequency=63.5, ranges=np.array([5.0, 15.0, 25.0]), tl_field=tl, clamped_samples=1,
+                               final_slab=pe3d.FieldSlab(final, 25.0), output_stride=2, wall_seconds=0.5)
+    ref_out.write_tl_csv(out / "ref_tl.csv", res, grid)
+    ref_out.write_tl_binary(out / "ref_tl.bin", res, grid)
+    ref_out.write_manifest(out, {"command": "run", "frequencies": [{"frequency_hz": 63.5, "sha256": "x"}],
+                                 "grid": {"n_range": 10}})
+    np.savez_compressed(out / "inputs.npz", tl=tl, ranges=res.ranges)
+
+
 def main(which=None):
     jobs = {
         "tridiag": tridiag_fixture,
         "dense": dense_step_fixture,
         "small": lambda: (small_march_fixture("periodic"), small_march_fixture("sector")),
         "cfg1": cfg1_full_fixture,
+        "output": output_fixture,
         "cfg2": lambda: full_size_fixture("cfg2", 100.0, 20),
         "cfg3": lambda: full_size_fixture("cfg3", 25.0, 20),
         "cfg4": lambda: (full_size_fixture("cfg4", 50.0, 10), full_size_fixture("cfg4", 500.0, 10)),
