@@ -638,7 +638,7 @@ int pe3d_march_medium_host(void* handle, const pe3d_grid* g, const pe3d_coeffs* 
     CK(h->az_ring.ensure(int64_t(F) * 2 * sizeof(cplx)), "alloc");
     CK(h->fail_row.ensure(int64_t(F) * (NT > NZ ? NT : NZ) * sizeof(int)), "alloc");
     CK(h->fail_mag.ensure(int64_t(F) * (NT > NZ ? NT : NZ) * sizeof(double)), "alloc");
-    CK(h->med_local.ensure(2 * int64_t(F) * slab * sizeof(cplx)), "alloc");
+    CK(h->med_local.ensure(2 * field * sizeof(cplx)), "alloc");      // >= 2 slabs; tile layout for the scan path
     CK(h->med_prof.ensure(2 * md->n_profile * sizeof(double)), "alloc");
     const int64_t n_lat = md->lattice ? int64_t(md->lat_nx) * md->lat_ny * md->lat_nz : 0;
     if (n_lat) CK(h->med_lat.ensure(n_lat * sizeof(double)), "alloc");
@@ -694,7 +694,7 @@ int pe3d_march_medium_host(void* handle, const pe3d_grid* g, const pe3d_coeffs* 
     c.fdev = h->fdev.as<pe3d::FreqDev>();
     c.err = h->err.as<pe3d::DevError>();
     c.stream = s;
-    cplx* L[2] = {h->med_local.as<cplx>(), h->med_local.as<cplx>() + int64_t(F) * slab};
+    cplx* L[2] = {h->med_local.as<cplx>(), h->med_local.as<cplx>() + field};
     cplx* A = h->field_a.as<cplx>();
     cplx* B = h->field_b.as<cplx>();
     cplx* Cc = h->field_c.as<cplx>();
@@ -710,7 +710,9 @@ int pe3d_march_medium_host(void* handle, const pe3d_grid* g, const pe3d_coeffs* 
            "ring setup");
     }
     // starter: local term at the input range, boundary, TL sample 0, first temp
-    CK(pe3d::launch_medium_local(c, M, L[0], g->delta_z, g->r_input), "medium");
+    const bool scan_path = !(g->flags & PE3D_FLAG_SERIAL) && n_tiles <= 512;
+    if (scan_path) CK(pe3d::launch_medium_local_tiles(c, M, L[0], g->delta_z, g->r_input), "medium");
+    else CK(pe3d::launch_medium_local(c, M, L[0], g->delta_z, g->r_input), "medium");
     pe3d::EpilogueArgs ea0{};
     ea0.tl = d_tl;
     ea0.snap = d_snap;
@@ -728,10 +730,16 @@ int pe3d_march_medium_host(void* handle, const pe3d_grid* g, const pe3d_coeffs* 
         const double r_new = g->r_start + j_new * g->delta_r;
         cplx* now = L[k & 1];
         cplx* nxt = L[(k + 1) & 1];
-        CK(pe3d::launch_medium_local(c, M, nxt, g->delta_z, r_new), "medium");
-        CK(pe3d::launch_depth_serial(c, A, B, Cc, now, nxt, int64_t(NZ) * NT, 1, NT, h->fail_row.as<int>(),
-                                     h->fail_mag.as<double>()),
-           "depth");
+        if (scan_path) {
+            CK(pe3d::launch_depth_medium_scan(c, M, A, B, now, nxt, g->delta_z, r_new, h->fail_row.as<int>(),
+                                              h->fail_mag.as<double>()),
+               "depth");
+        } else {
+            CK(pe3d::launch_medium_local(c, M, nxt, g->delta_z, r_new), "medium");
+            CK(pe3d::launch_depth_serial(c, A, B, Cc, now, nxt, int64_t(NZ) * NT, 1, NT, h->fail_row.as<int>(),
+                                         h->fail_mag.as<double>()),
+               "depth");
+        }
         CK(pe3d::launch_reduce_failures(h->fail_row.as<int>(), h->fail_mag.as<double>(), F, NT, j_new, 0, -1, c.err, s),
            "reduce");
         pe3d::EpilogueArgs ea{};
