@@ -21,6 +21,8 @@
 #include "pe3d_device.cuh"
 #include "pe3d_internal.h"
 
+#include <cooperative_groups.h>
+
 #include <cstdlib>
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -371,8 +373,8 @@ k_depth_scan(const cplx* __restrict__ src, cplx* __restrict__ dst, const cplx* _
 // last tile), completion on a per-warp mbarrier, and one TMA bulk store of
 // the solved column from the same stage.  The warps issue no per-line
 // copies at all; a 3-deep per-warp stage ring keeps two columns in flight.
-template <int STAGES, int MINB>
-__global__ void __launch_bounds__(128, MINB)
+template <int STAGES, int MINB, int MAXT>
+__global__ void __launch_bounds__(MAXT, MINB)
 k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ CUtensorMap tm_dst,
             const cplx* __restrict__ loc_tab, const cplx* __restrict__ mul_tab, const FreqDev* __restrict__ fdev,
             int n_theta, int n_tiles, int64_t total_cols, int cols_per_cta, int sector) {
@@ -554,6 +556,273 @@ k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ 
     __syncwarp();
 }
 
+// Long columns (cfg5: 4096 rows): a thread-block cluster of CL CTAs per
+// column, CTA s solving rows [s*R, (s+1)*R) (R = 8*tiles_per_cta <= 1024)
+// with exactly the 128-thread k_depth_tma scheme above, so the SM runs three
+// such CTAs like the cfg4 column kernel instead of one 16-warp CTA.  The
+// sub-columns are chained by the scan structure of the substitutions:
+//   forward  y entering CTA s = sum_{s'<s} (prod_{s'<u<s} P_u) Ytot_s'
+//   backward x entering from below = sum_{s'>s} (prod_{s<u<s'} P_u) Xtot_s'
+// with Ytot/Xtot the CTA's zero-carry totals and P_u the product of its
+// multipliers; each thread adds (prefix product before it) x carry.  The
+// totals travel by st.async into every peer's double-buffered table
+// (mbarrier transaction counts, no cluster barrier in the loop).  The depth
+// stencil's halo rows across sub-column edges are plain global loads of the
+// (read-only) input.
+template <int STAGES, int MINB>
+__global__ void __launch_bounds__(128, MINB)
+k_depth_tma_cluster(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ CUtensorMap tm_dst,
+                    const cplx* __restrict__ src_raw, const cplx* __restrict__ loc_tab,
+                    const cplx* __restrict__ mul_tab, const FreqDev* __restrict__ fdev, int n_theta, int n_tiles,
+                    int64_t total_cols, int cols_per_cluster, int sector) {
+    constexpr int RPT = 8;
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int CL = int(cluster.num_blocks());
+    const int s = int(cluster.block_rank());
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    const int nthreads = blockDim.x;                // = 32 * tiles per CTA / 32 ... one tile per thread
+    const int nwarps = nthreads >> 5;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    cplx* base = reinterpret_cast<cplx*>(smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u));
+    cplx* stage = base + warp * (STAGES * 256);
+    cplx* mf = base + nwarps * (STAGES * 256);      // [4][nthreads]
+    cplx* mb = mf + 4 * nthreads;
+    cplx* pincf = mb + 4 * nthreads;
+    cplx* pincb = pincf + nthreads;
+    cplx* pexc = pincb + nthreads;                  // product of the CTA's multipliers before thread t
+    cplx* psuf = pexc + nthreads;                   // ... after thread t
+    cplx* spw = psuf + nthreads;
+    cplx* sY = spw + nwarps;
+    cplx* sX = sY + nwarps;
+    cplx* sUp = sX + nwarps;
+    cplx* sDn = sUp + nwarps;
+    cplx* xF = sDn + nwarps;                        // [2][16][2]: (Ytot, P) of every CTA
+    cplx* xB = xF + 2 * 16 * 2;                     // [2][16]: Xtot, then [2][2] halo rows
+    uint64_t* xbar = reinterpret_cast<uint64_t*>(xB + 2 * 16 + 4);   // [0..1] forward, [2..3] backward
+    uint64_t* bars = xbar + 4 + warp * STAGES;
+
+    const int tpc = n_tiles / CL;                   // tiles per CTA (= nthreads)
+    const int row0 = s * tpc * 8;
+    const int64_t g0 = int64_t(blockIdx.x / CL) * cols_per_cluster;
+    const int64_t g1 = g0 + cols_per_cluster < total_cols ? g0 + cols_per_cluster : total_cols;
+    if (g0 >= g1) return;                           // uniform over the cluster
+    const int n_cols = int(g1 - g0);
+    const int nz8 = n_tiles * 8;
+    const int tile0 = s * tpc + warp * 32;
+
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < STAGES; ++k) mbar_init(&bars[k], 1);
+    }
+    if (t == 0) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) mbar_init(&xbar[k], 1);
+    }
+    if (lane == 0) mbar_fence_init();
+    cluster_barrier();                              // every peer's barriers initialised
+
+    int pf = int(g0 / n_theta), pc = int(g0 - int64_t(pf) * n_theta);
+    if (lane == 0) {
+#pragma unroll
+        for (int p = 0; p < STAGES - 1; ++p) {
+            if (p < n_cols) {
+                mbar_expect_tx(&bars[p], 32 * 128);
+                tma_load_4d(stage + p * 256, &tm_src, 0, pc, tile0, pf, &bars[p]);
+                if (++pc == n_theta) { pc = 0; ++pf; }
+            }
+        }
+    }
+
+    int f = int(g0 / n_theta), col = int(g0 - int64_t(f) * n_theta);
+    int cur_f = -1;
+    // thread 0 keeps the row above the sub-column, the last thread the row below
+    const bool halo_thread = (t == 0 && s > 0) || (t == nthreads - 1 && s < CL - 1);
+    cplx* halo = xB + 2 * 16 + (t == 0 ? 0 : 2);    // [2] per edge thread
+    auto halo_src = [&](int hf, int hc) -> const cplx* {
+        return t == 0 ? src_raw + ((int64_t(hf) * n_tiles + (row0 >> 3) - 1) * n_theta + hc) * 8 + 7
+                      : src_raw + ((int64_t(hf) * n_tiles + (row0 >> 3) + tpc) * n_theta + hc) * 8;
+    };
+    if (halo_thread) {
+        cp_async16(&halo[0], halo_src(f, col));
+        cp_async_commit();
+    }
+    cplx A[RPT], M[RPT], beta = czero(), P0f = czero(), P0b = czero(), Pcta = czero();
+    int slot = 0;
+    unsigned parity = 0;
+    for (int it = 0; it < n_cols; ++it) {
+        const int buf = it & 1;
+        const unsigned xpar = unsigned(it >> 1) & 1u;
+        cplx* tF = xF + buf * 32;
+        cplx* tB = xB + buf * 16;
+        if (t == 0) {
+            mbar_expect_tx(&xbar[buf], unsigned(CL) * 2 * sizeof(cplx));
+            mbar_expect_tx(&xbar[2 + buf], unsigned(CL) * sizeof(cplx));
+        }
+        // halo rows across the sub-column edges (input is read-only here),
+        // copied one column ahead by the two edge threads (cp.async into shared)
+        cplx up_g = czero(), dn_g = czero();
+        if (halo_thread) {
+            cp_async_wait<0>();
+            const cplx h = halo[buf];
+            if (t == 0) up_g = h; else dn_g = h;
+            if (it + 1 < n_cols) {
+                const int nf = col + 1 == n_theta ? f + 1 : f, nc = col + 1 == n_theta ? 0 : col + 1;
+                cp_async16(&halo[buf ^ 1], halo_src(nf, nc));
+                cp_async_commit();
+            }
+        }
+        if (f != cur_f) {
+            const FreqDev fd = fdev[f];
+            const cplx kappa = crecip(cneg(fd.off_z));
+            beta = cmul(kappa, crmul(fd.s_z, fd.cx_rhs));
+            cplx P = cone();
+#pragma unroll
+            for (int i = 0; i < RPT; ++i) {
+                const int64_t o = int64_t(f) * nz8 + row0 + RPT * t + i;
+                const cplx lc = ldc(loc_tab + o);
+                M[i] = ldc(mul_tab + o);
+                A[i] = csub(cmul(kappa, cadd(cone(), cmul(fd.cx_rhs, lc))), cadd(beta, beta));
+                P = cmul(M[i], P);
+            }
+            __syncthreads();
+            P0f = lane >= 1 ? P : czero();
+            P0b = lane + 1 < 32 ? P : czero();
+            cplx Pf = P, Pb = P;
+#pragma unroll
+            for (int d = 0; d < 5; ++d) {
+                const int o = 1 << d;
+                if (d > 0) {
+                    mf[(d - 1) * nthreads + t] = lane >= o ? Pf : czero();
+                    mb[(d - 1) * nthreads + t] = lane + o < 32 ? Pb : czero();
+                }
+                const cplx pu = shfl_up(Pf, o), pd = shfl_down(Pb, o);
+                if (lane >= o) Pf = cmul(Pf, pu);
+                if (lane + o < 32) Pb = cmul(Pb, pd);
+            }
+            pincf[t] = Pf;
+            pincb[t] = Pb;
+            if (lane == 31) spw[warp] = Pf;
+            __syncthreads();
+            {
+                cplx before = cone(), after = cone();
+                Pcta = cone();
+                for (int w = 0; w < nwarps; ++w) {
+                    if (w < warp) before = cmul(before, spw[w]);
+                    if (w > warp) after = cmul(after, spw[w]);
+                    Pcta = cmul(Pcta, spw[w]);
+                }
+                pexc[t] = lane > 0 ? cmul(before, pincf[t - 1]) : before;
+                psuf[t] = lane < 31 ? cmul(after, pincb[t + 1]) : after;
+            }
+            cur_f = f;
+        }
+        cplx* cur = stage + slot * 256;
+        mbar_wait(&bars[slot], parity);
+        const int sw = lane & 7;
+        cplx x[RPT];
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) x[i] = cur[lane * 8 + (i ^ sw)];
+
+        cplx up = shfl_up(x[RPT - 1], 1), dn = shfl_down(x[0], 1);
+        if (lane == 31) sUp[warp] = x[RPT - 1];
+        if (lane == 0) sDn[warp] = x[0];
+        __syncthreads();
+        if (lane == 0) up = warp > 0 ? sUp[warp - 1] : up_g;
+        if (lane == 31) dn = warp < nwarps - 1 ? sDn[warp + 1] : dn_g;
+
+        cplx b[RPT];
+        if (sector && (col == 0 || col == n_theta - 1)) {
+#pragma unroll
+            for (int i = 0; i < RPT; ++i) b[i] = czero();
+        } else {
+#pragma unroll
+            for (int i = 0; i < RPT; ++i) {
+                const cplx um = i ? x[i - 1] : up;
+                const cplx upp = i < RPT - 1 ? x[i + 1] : dn;
+                b[i] = cmul(M[i], cfma(A[i], x[i], cmul(beta, cadd(upp, um))));   // m_l r'_l, off the chain
+            }
+        }
+        cplx Y = czero();
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) Y = cfma(M[i], Y, b[i]);
+#pragma unroll
+        for (int d = 0; d < 5; ++d) Y = cfma(d == 0 ? P0f : mf[(d - 1) * nthreads + t], shfl_up(Y, 1 << d), Y);
+        if (lane == 31) sY[warp] = Y;
+        __syncthreads();
+        cplx C = czero();
+        for (int w = 0; w < warp; ++w) C = cfma(spw[w], C, sY[w]);
+        const cplx yinc = cfma(pincf[t], C, Y);         // y at this thread's last row, zero CTA carry
+        // forward totals to every peer: (Ytot, P) from the CTA's last thread
+        if (warp == nwarps - 1) {
+            const cplx ytot = shfl_idx(yinc, 31);
+            if (lane < CL) {
+                const unsigned rb = mapa_shared(smem_addr(&xbar[buf]), lane);
+                st_async_cplx(mapa_shared(smem_addr(tF + 2 * s), lane), ytot, rb);
+                st_async_cplx(mapa_shared(smem_addr(tF + 2 * s + 1), lane), Pcta, rb);
+            }
+        }
+        cplx y = shfl_up(yinc, 1);
+        if (lane == 0) y = C;
+        mbar_wait(&xbar[buf], xpar);
+        {
+            cplx cin = czero();
+            for (int u = 0; u < s; ++u) cin = cfma(tF[2 * u + 1], cin, tF[2 * u]);
+            y = cfma(pexc[t], cin, y);                  // + carry entering the CTA, propagated
+        }
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) { y = cfma(M[i], y, b[i]); b[i] = y; }
+
+        cplx X = czero();
+#pragma unroll
+        for (int i = RPT - 1; i >= 0; --i) X = cfma(M[i], X, b[i]);
+#pragma unroll
+        for (int d = 0; d < 5; ++d) X = cfma(d == 0 ? P0b : mb[(d - 1) * nthreads + t], shfl_down(X, 1 << d), X);
+        if (lane == 0) sX[warp] = X;
+        __syncthreads();
+        cplx D = czero();
+        for (int w = nwarps - 1; w > warp; --w) D = cfma(spw[w], D, sX[w]);
+        const cplx xinc = cfma(pincb[t], D, X);         // x at this thread's first row, zero carry from below
+        if (warp == 0) {
+            const cplx xtot = shfl_idx(xinc, 0);
+            if (lane < CL)
+                st_async_cplx(mapa_shared(smem_addr(tB + s), lane), xtot, mapa_shared(smem_addr(&xbar[2 + buf]), lane));
+        }
+        cplx xv = shfl_down(xinc, 1);
+        if (lane == 31) xv = D;
+        mbar_wait(&xbar[2 + buf], xpar);
+        {
+            cplx din = czero();
+            for (int u = CL - 1; u > s; --u) din = cfma(tF[2 * u + 1], din, tB[u]);
+            xv = cfma(psuf[t], din, xv);
+        }
+#pragma unroll
+        for (int i = RPT - 1; i >= 0; --i) { xv = cfma(M[i], xv, b[i]); b[i] = xv; }
+
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) cur[lane * 8 + (i ^ sw)] = b[i];
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+            tma_store_4d(&tm_dst, 0, col, tile0, f, cur);
+            bulk_commit();
+            bulk_wait_read<1>();
+            if (it + STAGES - 1 < n_cols) {
+                const int ps = (slot + STAGES - 1) % STAGES;
+                mbar_expect_tx(&bars[ps], 32 * 128);
+                tma_load_4d(stage + ps * 256, &tm_src, 0, pc, tile0, pf, &bars[ps]);
+                if (++pc == n_theta) { pc = 0; ++pf; }
+            }
+        }
+        __syncwarp();
+        if (++col == n_theta) { col = 0; ++f; }
+        if (++slot == STAGES) { slot = 0; parity ^= 1u; }
+    }
+    if (lane == 0) bulk_wait_read<0>();
+    __syncwarp();
+    cluster_barrier();                              // no CTA leaves while peers may still address it
+}
+
 static int round32(int x) { return (x + 31) / 32 * 32; }
 
 // Host side of the TMA path: 4-D tiled tensor maps over the device field
@@ -584,20 +853,21 @@ static bool field_tensor_map(CUtensorMap* tm, const void* base, const LaunchCtx&
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-static cudaError_t launch_depth_tma(const LaunchCtx& c, const cplx* src, cplx* dst) {
+template <int STAGES, int MINB, int MAXT>
+static cudaError_t launch_depth_tma_cfg(const LaunchCtx& c, const cplx* src, cplx* dst) {
     CUtensorMap tm_src, tm_dst;
     if (!field_tensor_map(&tm_src, src, c) || !field_tensor_map(&tm_dst, dst, c)) return cudaErrorNotSupported;
     const int nthreads = (c.n_tiles + 31) / 32 * 32;
     const int nwarps = nthreads / 32;
-    constexpr int STAGES = 3;
     const size_t bytes = 1024 + sizeof(cplx) * (size_t(nwarps) * STAGES * 256 + 10 * size_t(nthreads) + 5 * nwarps) +
                          sizeof(uint64_t) * nwarps * STAGES;
-    auto kern = k_depth_tma<STAGES, 3>;
+    if (bytes > 227 * 1024) return cudaErrorNotSupported;
+    auto kern = k_depth_tma<STAGES, MINB, MAXT>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
     if (e != cudaSuccess) return e;
     const int64_t total = int64_t(c.n_freq) * c.n_theta;
     int per_sm = int((227 * 1024) / (bytes + 1024));
-    if (per_sm > 3) per_sm = 3;
+    if (per_sm > MINB) per_sm = MINB;
     if (per_sm < 1) per_sm = 1;
     const int64_t ctas = int64_t(c.num_sms) * per_sm;
     const int per = int((total + ctas - 1) / ctas);
@@ -605,6 +875,57 @@ static cudaError_t launch_depth_tma(const LaunchCtx& c, const cplx* src, cplx* d
     kern<<<grid, nthreads, bytes, c.stream>>>(tm_src, tm_dst, c.loc_tab, c.mul_tab, c.fdev, c.n_theta, c.n_tiles,
                                               total, per, c.sector);
     return cudaGetLastError();
+}
+
+static cudaError_t launch_depth_tma_cluster(const LaunchCtx& c, const cplx* src, cplx* dst, int CL) {
+    CUtensorMap tm_src, tm_dst;
+    if (!field_tensor_map(&tm_src, src, c) || !field_tensor_map(&tm_dst, dst, c)) return cudaErrorNotSupported;
+    constexpr int STAGES = 3, MINB = 3;
+    const int nthreads = c.n_tiles / CL;
+    const int nwarps = nthreads / 32;
+    const size_t bytes = 1024 + sizeof(cplx) * (size_t(nwarps) * STAGES * 256 + 12 * size_t(nthreads) + 5 * nwarps +
+                                                2 * 16 * 2 + 2 * 16 + 4) +
+                         sizeof(uint64_t) * (4 + nwarps * STAGES);
+    auto kern = k_depth_tma_cluster<STAGES, MINB>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.blockDim = dim3(nthreads);
+    cfg.dynamicSmemBytes = bytes;
+    cfg.stream = c.stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    static int resident[17] = {0};                  // co-resident clusters, per cluster size
+    if (resident[CL] == 0) {
+        cfg.gridDim = dim3(CL * c.num_sms);
+        int n = 0;
+        e = cudaOccupancyMaxActiveClusters(&n, kern, &cfg);
+        if (e != cudaSuccess) return e;
+        if (n < 1) return cudaErrorInvalidConfiguration;
+        resident[CL] = n;
+    }
+    const int64_t total = int64_t(c.n_freq) * c.n_theta;
+    const int per = int((total + resident[CL] - 1) / resident[CL]);
+    const int clusters = int((total + per - 1) / per);
+    cfg.gridDim = dim3(clusters * CL);
+    return cudaLaunchKernelEx(&cfg, kern, tm_src, tm_dst, src, c.loc_tab, c.mul_tab, c.fdev, c.n_theta, c.n_tiles,
+                              total, per, c.sector);
+}
+
+// Columns of up to 128 tiles: 128-thread CTAs, 3 stages, 3 CTAs per SM.
+// Longer columns split into CL = n_tiles/128 sub-columns of 128 tiles, one
+// per CTA of a cluster (cfg5: 4096 rows, CL = 4); otherwise one 512-thread
+// CTA per SM.
+static cudaError_t launch_depth_tma(const LaunchCtx& c, const cplx* src, cplx* dst) {
+    if (c.n_tiles <= 128) return launch_depth_tma_cfg<3, 3, 128>(c, src, dst);
+    if (c.n_tiles % 128 == 0 && c.n_tiles / 128 <= 8 && !getenv("PE3D_DEPTH_NO_CLUSTER"))
+        return launch_depth_tma_cluster(c, src, dst, c.n_tiles / 128);
+    return launch_depth_tma_cfg<2, 1, 512>(c, src, dst);
 }
 
 cudaError_t launch_depth_scan(const LaunchCtx& c, const cplx* src, cplx* dst) {
@@ -623,7 +944,7 @@ cudaError_t launch_depth_scan(const LaunchCtx& c, const cplx* src, cplx* dst) {
                                                per, c.sector);
         return cudaGetLastError();
     };
-    if (c.n_tiles <= 128 && !getenv("PE3D_DEPTH_NO_TMA")) {
+    if (c.n_tiles <= 512 && !getenv("PE3D_DEPTH_NO_TMA") && !(c.n_tiles > 128 && getenv("PE3D_DEPTH_WIDE_SCAN"))) {
         cudaError_t e = launch_depth_tma(c, src, dst);
         if (e != cudaErrorNotSupported) return e;
     }

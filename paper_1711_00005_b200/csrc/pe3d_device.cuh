@@ -83,6 +83,9 @@ __device__ __forceinline__ cplx shfl_up(cplx v, int d) {
 __device__ __forceinline__ cplx shfl_down(cplx v, int d) {
     return mk(__shfl_down_sync(0xffffffffu, v.re, d), __shfl_down_sync(0xffffffffu, v.im, d));
 }
+__device__ __forceinline__ cplx shfl_xor(cplx v, int m) {
+    return mk(__shfl_xor_sync(0xffffffffu, v.re, m), __shfl_xor_sync(0xffffffffu, v.im, m));
+}
 __device__ __forceinline__ cplx shfl_idx(cplx v, int src) {
     return mk(__shfl_sync(0xffffffffu, v.re, src), __shfl_sync(0xffffffffu, v.im, src));
 }
@@ -171,6 +174,37 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
         "}\n" ::"r"(smem_addr(bar)),
         "r"(parity)
         : "memory");
+}
+// Wait for a phase completed by st.async writes of other CTAs of the cluster
+// (distributed shared memory).  The writes land in this CTA's shared memory
+// and are counted on this CTA's mbarrier as transaction bytes, exactly like a
+// TMA load, so the CTA-scope acquire of the default try_wait suffices.
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAITC_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAITC_%=;\n"
+        "}\n" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+// Address of the same shared-memory object in CTA `rank` of the cluster.
+__device__ __forceinline__ unsigned mapa_shared(unsigned addr, unsigned rank) {
+    unsigned r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+// 16-byte asynchronous store into a cluster peer's shared memory; completion
+// (and visibility) is signalled on the peer's mbarrier as transaction bytes.
+__device__ __forceinline__ void st_async_cplx(unsigned raddr, cplx v, unsigned rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];\n" ::"r"(raddr),
+                 "d"(v.re), "d"(v.im), "r"(rbar)
+                 : "memory");
+}
+__device__ __forceinline__ void cluster_barrier() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 // 4-D tiled TMA load global -> shared, completion counted on `bar`.
 __device__ __forceinline__ void tma_load_4d(void* smem_dst, const void* tmap, int c0, int c1, int c2, int c3,

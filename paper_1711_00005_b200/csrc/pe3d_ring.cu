@@ -19,6 +19,8 @@
 #include "pe3d_device.cuh"
 #include "pe3d_internal.h"
 
+#include <cooperative_groups.h>
+#include <cstdio>
 #include <cstdlib>
 
 namespace pe3d {
@@ -618,6 +620,326 @@ k_azimuth_warp(const cplx* __restrict__ src, cplx* __restrict__ dst, const cplx*
     cp_async_wait<0>();
 }
 
+// Wide rings (n_theta = CL * 32L, CL = 2..16): one thread-block cluster per
+// (frequency, depth tile) item.  CTA s of the cluster stages the contiguous
+// segment of azimuths [s*32L, (s+1)*32L) of the item's 8 rows (coalesced
+// cp.async into the swizzled stage of k_azimuth_warp) and runs the same
+// ring-per-warp solve on it with zero carry-in.  The segments are joined by
+// two DSMEM exchanges of per-row segment totals, combined with Horner in
+// R = rho^(32L):
+//   forward  w entering segment s = sum_{s'<s} R^(s-1-s') W_s'
+//                                  + R^s * (sum_s' R^(CL-1-s') W_s') / (1 - rho^N)
+//   backward x entering from the right = sum_{s'>s} R^(s'-s-1) X_s'
+//                                  + R^(CL-1-s) * (sum_s' R^s' X_s') / (1 - rho^N)
+// and the epilogue's neighbours across segment edges follow from the
+// recurrences themselves: x_(m-1) = w_(m-1) + rho x_m, x_(m+32L) = the right
+// carry.  The totals are pushed with st.async into every peer's table and
+// counted on the peer's mbarrier (no cluster-wide barrier, hence no GPU-scope
+// fence behind the streaming stores, inside the item loop); the tables are
+// double-buffered by item parity, which is race free because a CTA can only
+// start item i+2 after every peer has sent its item i+1 totals, i.e. after
+// every peer has finished reading item i.  Persistent: every CTA of a
+// cluster walks the same item range.
+template <int L, int RT, int STAGES>
+__global__ void __launch_bounds__(32 * 8 / RT, (L == 8 ? 3 : 1))
+k_azimuth_cluster(const cplx* __restrict__ src, cplx* __restrict__ dst, const cplx* __restrict__ table, int E,
+                  const FreqDev* __restrict__ fdev, int n_theta, int n_tiles, int n_depth, int64_t total_items,
+                  int items_per_cluster, double r_new, double delta_theta, EpilogueArgs ea) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int CL = int(cluster.num_blocks());
+    const int s = int(cluster.block_rank());
+    constexpr int NS = 32 * L;                      // segment length
+    constexpr int ITEM = NS * 8;                    // elements per segment of an item
+    constexpr int NTHR = 32 * 8 / RT;
+    constexpr int PER = ITEM / NTHR;
+    constexpr int TE = 4 + (L + 1) + 33;            // table entries used: header, rho^0..L, R^0..32
+    extern __shared__ cplx smem[];
+    cplx* T = smem + STAGES * ITEM;
+    cplx* segW = T + TE;                            // [2][16][8] forward totals of every segment
+    cplx* segX = segW + 2 * 16 * 8;                 // [2][16][8] backward totals
+    cplx* Rp = segX + 2 * 16 * 8;                   // [17] R^k, k = 0..16
+    uint64_t* bars = reinterpret_cast<uint64_t*>(Rp + 17);   // [0..1] forward, [2..3] backward
+    const cplx* pw = T + 4;
+    const cplx* qp = pw + L + 1;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int q = lane, swz = q & 7;
+    const int m0 = q * L;
+    const int mseg = s * NS;
+
+    const int64_t it0 = int64_t(blockIdx.x / CL) * items_per_cluster;
+    const int64_t it1 = it0 + items_per_cluster < total_items ? it0 + items_per_cluster : total_items;
+    if (it0 >= it1) return;                         // uniform over the cluster
+    if (tid == 0) {
+#pragma unroll
+        for (int b = 0; b < 4; ++b) mbar_init(&bars[b], 1);
+        mbar_fence_init();
+    }
+    cluster_barrier();                              // peers' barriers initialised before any st.async
+    const unsigned exch_bytes = unsigned(CL) * 8 * sizeof(cplx);
+    // push this segment's per-row value to table[buf][s][row] of every peer (lane j -> rank j)
+    auto push = [&](cplx* table_, uint64_t* bar, int row, cplx val) {
+        if (lane < CL) st_async_cplx(mapa_shared(smem_addr(table_ + s * 8 + row), lane), val,
+                                     mapa_shared(smem_addr(bar), lane));
+    };
+    const int C = ea.chunk_cols ? ea.chunk_cols : n_theta;
+    const int64_t gap = ea.chunk_gap;
+    auto item_base = [&](int64_t item) {
+        const int fi = int(item / n_tiles);
+        return ring_base(fi, int(item - int64_t(fi) * n_tiles), n_tiles, n_theta, C);
+    };
+    auto goff = [&](int e) -> int64_t {
+        const int ge = s * ITEM + e;
+        return ge + (gap ? int64_t((ge >> 3) / C) * gap : 0);
+    };
+    auto fetch = [&](int64_t item, int st) {
+        cplx* d = smem + st * ITEM;
+        if (gap == 0) {                             // standard layout: the segment is contiguous
+            const cplx* g = src + item_base(item) + s * ITEM + tid;
+#pragma unroll
+            for (int j = 0; j < PER; ++j) {
+                const int e = j * NTHR + tid;
+                cp_async16(d + ring_slot<L>(e >> 3, e & 7), g + j * NTHR);
+            }
+        } else {
+            const cplx* g = src + item_base(item);
+#pragma unroll
+            for (int j = 0; j < PER; ++j) {
+                const int e = j * NTHR + tid;
+                cp_async16(d + ring_slot<L>(e >> 3, e & 7), g + goff(e));
+            }
+        }
+    };
+#pragma unroll
+    for (int p = 0; p < STAGES - 1; ++p) {
+        if (it0 + p < it1) fetch(it0 + p, p);
+        cp_async_commit();
+    }
+    int f = int(it0 / n_tiles), tile = int(it0 - int64_t(f) * n_tiles);
+    int cur_f = -1;
+    int slot = 0;
+    cplx rho = czero(), R = czero(), inv_wrap = czero(), scale = czero(), b1 = czero(), b2 = czero();
+    cplx Rs = cone(), Rr = cone();                  // R^s, R^(CL-1-s)
+    bool diagonal = false;
+    for (int64_t item = it0; item < it1; ++item) {
+        const int kk = int(item - it0);
+        const int buf = kk & 1;
+        const unsigned par = unsigned(kk >> 1) & 1u;
+        cplx* tW = segW + buf * 128;
+        cplx* tX = segX + buf * 128;
+        __syncthreads();                            // previous item's stage fully stored
+        if (tid == 0) {
+            mbar_expect_tx(&bars[buf], exch_bytes);
+            mbar_expect_tx(&bars[2 + buf], exch_bytes);
+        }
+        if (f != cur_f) {
+            for (int e = tid; e < TE; e += NTHR) T[e] = table[int64_t(f) * E + e];
+            __syncthreads();
+            cur_f = f;
+            rho = T[0];
+            scale = T[1];
+            inv_wrap = T[2];
+            diagonal = T[3].re != 0.0;
+            R = qp[32];
+            if (tid == 0) {
+                cplx p = cone();
+                for (int k = 0; k <= 16; ++k) { Rp[k] = p; p = cmul(p, R); }
+            }
+            __syncthreads();
+            Rs = Rp[s];
+            Rr = Rp[CL - 1 - s];
+            const FreqDev fd = fdev[f];
+            const cplx alpha = crmul(azimuth_scale(fd.k0, r_new, delta_theta), fd.cy_rhs);
+            b2 = cmul(scale, alpha);
+            b1 = csub(scale, cadd(b2, b2));
+        }
+        {
+            const int64_t ip = item + STAGES - 1;
+            if (ip < it1) fetch(ip, (slot + STAGES - 1) % STAGES);
+            cp_async_commit();
+            cp_async_wait<STAGES - 1>();
+        }
+        __syncthreads();                            // item's lines visible to every warp
+        cplx* stg = smem + slot * ITEM;
+        cplx v[RT][L];
+#pragma unroll
+        for (int h = 0; h < RT; ++h)
+#pragma unroll
+            for (int k = 0; k < L; ++k) v[h][k] = stg[(m0 + k) * 8 + ((warp * RT + h) ^ swz)];
+
+        cplx prev_edge[RT], next_edge[RT];         // x at mseg-1 and mseg+NS (cyclic)
+        if (!diagonal) {
+            // ---- forward recurrence w_m = v_m + rho w_{m-1} on the segment, zero carry-in
+            cplx Y[RT];
+#pragma unroll
+            for (int h = 0; h < RT; ++h) {
+                Y[h] = czero();
+#pragma unroll
+                for (int k = 0; k < L; ++k) { Y[h] = cfma(rho, Y[h], v[h][k]); v[h][k] = Y[h]; }
+            }
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const cplx m = lane >= d ? qp[d] : czero();
+#pragma unroll
+                for (int h = 0; h < RT; ++h) Y[h] = cfma(m, shfl_up(Y[h], d), Y[h]);
+            }
+#pragma unroll
+            for (int h = 0; h < RT; ++h) push(tW, &bars[buf], warp * RT + h, shfl_idx(Y[h], 31));
+            mbar_wait_cluster(&bars[buf], par);     // every segment's forward totals
+            // half-warp hh = lane/16 serves row warp*RT+hh; its lane j < CL weighs
+            // segment j's total by its power of R; a 4-level butterfly sums
+            cplx carry_w[RT];
+            {
+                const int hh = lane >> 4, j = lane & 15;
+                const bool use = j < CL && hh < RT;
+                const cplx w = use ? tW[j * 8 + warp * RT + (hh < RT ? hh : 0)] : czero();
+                cplx cin = (use && j < s) ? cmul(Rp[j < s ? s - 1 - j : 0], w) : czero();
+                cplx wend = use ? cmul(Rp[j < CL ? CL - 1 - j : 0], w) : czero();
+#pragma unroll
+                for (int o = 1; o < 16; o <<= 1) {
+                    cin = cadd(cin, shfl_xor(cin, o));
+                    wend = cadd(wend, shfl_xor(wend, o));
+                }
+                const cplx cw = cfma(Rs, cmul(wend, inv_wrap), cin);      // w_(mseg-1), cyclic
+#pragma unroll
+                for (int h = 0; h < RT; ++h) carry_w[h] = shfl_idx(cw, 16 * h);
+            }
+            const cplx qpq = qp[q];
+#pragma unroll
+            for (int h = 0; h < RT; ++h) {
+                cplx ex = shfl_up(Y[h], 1);
+                if (lane == 0) ex = czero();
+                const cplx c_in = cfma(qpq, carry_w[h], ex);
+#pragma unroll
+                for (int k = 0; k < L; ++k) v[h][k] = cfma(pw[k + 1], c_in, v[h][k]);
+            }
+            // ---- backward recurrence x_m = w_m + rho x_{m+1}, zero carry-in
+            cplx X[RT];
+#pragma unroll
+            for (int h = 0; h < RT; ++h) {
+                X[h] = czero();
+#pragma unroll
+                for (int k = L - 1; k >= 0; --k) { X[h] = cfma(rho, X[h], v[h][k]); v[h][k] = X[h]; }
+            }
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const cplx m = lane + d < 32 ? qp[d] : czero();
+#pragma unroll
+                for (int h = 0; h < RT; ++h) X[h] = cfma(m, shfl_down(X[h], d), X[h]);
+            }
+#pragma unroll
+            for (int h = 0; h < RT; ++h) push(tX, &bars[2 + buf], warp * RT + h, shfl_idx(X[h], 0));
+            mbar_wait_cluster(&bars[2 + buf], par);
+            const cplx qup = qp[31 - q];
+            cplx carry_xr[RT];
+            {
+                const int hh = lane >> 4, j = lane & 15;
+                const bool use = j < CL && hh < RT;
+                const cplx xs = use ? tX[j * 8 + warp * RT + (hh < RT ? hh : 0)] : czero();
+                cplx dn = (use && j > s) ? cmul(Rp[(j > s && j < CL) ? j - s - 1 : 0], xs) : czero();
+                cplx x0 = use ? cmul(Rp[j < CL ? j : 0], xs) : czero();
+#pragma unroll
+                for (int o = 1; o < 16; o <<= 1) {
+                    dn = cadd(dn, shfl_xor(dn, o));
+                    x0 = cadd(x0, shfl_xor(x0, o));
+                }
+                const cplx cx = cfma(Rr, cmul(x0, inv_wrap), dn);         // x_(mseg+NS), cyclic
+#pragma unroll
+                for (int h = 0; h < RT; ++h) carry_xr[h] = shfl_idx(cx, 16 * h);
+            }
+#pragma unroll
+            for (int h = 0; h < RT; ++h) {
+                const cplx carry_x = carry_xr[h];
+                cplx nx = shfl_down(X[h], 1);
+                if (lane == 31) nx = czero();
+                const cplx c_up = cfma(qup, carry_x, nx);
+#pragma unroll
+                for (int k = 0; k < L; ++k) v[h][k] = cfma(pw[L - k], c_up, v[h][k]);
+                next_edge[h] = carry_x;
+                prev_edge[h] = cfma(rho, shfl_idx(v[h][0], 0), carry_w[h]);   // x_(mseg-1) = w + rho x_mseg
+            }
+        } else {
+            // off == 0 (B = diag I): x = v; the edges are the neighbours' raw values
+#pragma unroll
+            for (int h = 0; h < RT; ++h) {
+                push(tW, &bars[buf], warp * RT + h, shfl_idx(v[h][L - 1], 31));
+                push(tX, &bars[2 + buf], warp * RT + h, shfl_idx(v[h][0], 0));
+            }
+            mbar_wait_cluster(&bars[buf], par);
+            mbar_wait_cluster(&bars[2 + buf], par);
+#pragma unroll
+            for (int h = 0; h < RT; ++h) {
+                prev_edge[h] = tW[((s + CL - 1) % CL) * 8 + warp * RT + h];
+                next_edge[h] = tX[((s + 1) % CL) * 8 + warp * RT + h];
+            }
+        }
+        // ---- boundary (surface and pad rows), TL / snapshot / final, next temp
+        const int l0 = tile * 8 + warp * RT;
+#pragma unroll
+        for (int h = 0; h < RT; ++h) {
+            const int l = l0 + h;
+            if (l + ea.row_offset == 0 || l >= n_depth) {
+#pragma unroll
+                for (int k = 0; k < L; ++k) v[h][k] = czero();
+                prev_edge[h] = czero();
+                next_edge[h] = czero();
+            }
+            if (l < n_depth && (ea.tl || ea.snap || ea.final_out)) {
+                long long zeros = 0;
+#pragma unroll
+                for (int k = 0; k < L; ++k) {
+                    const int m = mseg + m0 + k;
+                    const cplx uf = cmul(scale, v[h][k]);
+                    const int64_t so = (int64_t(f) * ea.n_samples + ea.sample) * n_theta * n_depth +
+                                       (int64_t(m) * n_depth + l);
+                    if (ea.tl) {
+                        const double mag = cabs(uf) * ea.w_abs[f];
+                        if (mag == 0.0) ++zeros;
+                        ea.tl[so] = (mag == 0.0) ? TL_FLOOR_DB : -20.0 * log10(mag);
+                    }
+                    if (ea.snap) stc(ea.snap + so, uf);
+                    if (ea.final_out) stc(ea.final_out + (int64_t(f) * n_theta + m) * n_depth + l, uf);
+                }
+                if (ea.tl && zeros) atomicAdd(reinterpret_cast<unsigned long long*>(ea.clamped + f), (unsigned long long)zeros);
+            }
+            if (ea.write_temp) {
+                cplx prev = shfl_up(v[h][L - 1], 1), next = shfl_down(v[h][0], 1);
+                if (lane == 0) prev = prev_edge[h];
+                if (lane == 31) next = next_edge[h];
+                const int r = (warp * RT + h) ^ swz;
+#pragma unroll
+                for (int k = 0; k < L; ++k) {
+                    const cplx um = k ? v[h][k - 1] : prev;
+                    const cplx up = (k + 1 < L) ? v[h][(k + 1) % L] : next;
+                    stg[(m0 + k) * 8 + r] = cfma(b1, v[h][k], cmul(b2, cadd(up, um)));   // own slots only
+                }
+            }
+        }
+        if (ea.write_temp) {
+            __syncthreads();                        // every warp's rows written
+            if (gap == 0) {
+                cplx* g = dst + item_base(item) + s * ITEM + tid;
+#pragma unroll
+                for (int j = 0; j < PER; ++j) {
+                    const int e = j * NTHR + tid;
+                    stc_stream(g + j * NTHR, stg[ring_slot<L>(e >> 3, e & 7)]);
+                }
+            } else {
+                cplx* g = dst + item_base(item);
+#pragma unroll
+                for (int j = 0; j < PER; ++j) {
+                    const int e = j * NTHR + tid;
+                    stc_stream(g + goff(e), stg[ring_slot<L>(e >> 3, e & 7)]);
+                }
+            }
+        }
+        if (++tile == n_tiles) { tile = 0; ++f; }
+        slot = (slot + 1 == STAGES) ? 0 : slot + 1;
+    }
+    cp_async_wait<0>();
+    cluster_barrier();                              // no CTA leaves while peers may still address it
+}
+
 // Direct variant (one CTA per (frequency, row group), registers only) for
 // rings too wide for a shared-memory stage (RW < 8).
 template <int L, int RW>
@@ -720,13 +1042,27 @@ struct RingPlan {
     RingLayout lay;
 };
 
+static int cluster_chunk() {
+    static const int L = getenv("PE3D_CLUSTER_L") ? atoi(getenv("PE3D_CLUSTER_L")) : 8;
+    return L == 16 ? 16 : 8;
+}
+
 static RingPlan ring_plan(int n_theta) {
     RingPlan p;
-    if (n_theta % 32 == 0 && n_theta / 32 >= 2 && n_theta / 32 <= 16 && !(getenv("PE3D_RING_BLOCK"))) {
+    const bool block = getenv("PE3D_RING_BLOCK") != nullptr;
+    if (n_theta % 32 == 0 && n_theta / 32 >= 2 && n_theta / 32 <= 16 && !block) {
         p.kind = 0;
         p.L = n_theta / 32;
         p.RW = 1;
         p.lay = ring_layout(n_theta, p.L, 1);     // 32 chunks, qp[0..32]
+        return p;
+    }
+    const int cl_L = cluster_chunk();
+    if (n_theta % (32 * cl_L) == 0 && n_theta / (32 * cl_L) >= 2 && n_theta / (32 * cl_L) <= 16 && !block) {
+        p.kind = 2;                               // cluster of n_theta/(32L) segments
+        p.L = cl_L;
+        p.RW = 1;
+        p.lay = ring_layout(n_theta, p.L, 1);     // qp[0..32] leads the R^j run
         return p;
     }
     p.kind = 1;
@@ -773,9 +1109,57 @@ static cudaError_t launch_warp_ring(const LaunchCtx& c, const cplx* src, cplx* d
     return cudaGetLastError();
 }
 
+template <int L, int RT, int STAGES>
+static cudaError_t launch_cluster_ring(const LaunchCtx& c, const cplx* src, cplx* dst, const cplx* table_step, int E,
+                                       double r_new, const EpilogueArgs& ea) {
+    auto kern = k_azimuth_cluster<L, RT, STAGES>;
+    constexpr int NS = 32 * L;
+    const int CL = c.n_theta / NS;
+    const int nthr = 32 * 8 / RT;
+    const size_t bytes = sizeof(cplx) * (size_t(STAGES) * NS * 8 + 4 + (L + 1) + 33 + 4 * 128 + 17) + 4 * sizeof(uint64_t);
+    cudaError_t e = set_smem(kern, bytes);
+    if (e != cudaSuccess) return e;
+    if (CL > 8) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return e;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.blockDim = dim3(nthr);
+    cfg.dynamicSmemBytes = bytes;
+    cfg.stream = c.stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    // persistent: as many clusters as can be co-resident (queried once per cluster size)
+    static int resident[17] = {0};
+    if (resident[CL] == 0) {
+        cfg.gridDim = dim3(CL * c.num_sms);
+        int n = 0;
+        e = cudaOccupancyMaxActiveClusters(&n, kern, &cfg);
+        if (e != cudaSuccess) return e;
+        if (n < 1) return cudaErrorInvalidConfiguration;
+        resident[CL] = n;
+        if (getenv("PE3D_DEBUG_CLUSTER")) fprintf(stderr, "pe3d: cluster ring L=%d CL=%d resident clusters=%d\n", L, CL, n);
+    }
+    const int64_t items = int64_t(c.n_freq) * c.n_tiles;
+    const int per = int((items + resident[CL] - 1) / resident[CL]);
+    const int clusters = int((items + per - 1) / per);
+    cfg.gridDim = dim3(clusters * CL);
+    return cudaLaunchKernelEx(&cfg, kern, src, dst, table_step, E, c.fdev, c.n_theta, c.n_tiles, c.n_depth, items, per,
+                              r_new, c.delta_theta, ea);
+}
+
 cudaError_t launch_azimuth_scan(const LaunchCtx& c, const cplx* src, cplx* dst, const cplx* table_step, double r_new,
                                 const EpilogueArgs& ea) {
     const RingPlan plan = ring_plan(c.n_theta);
+    if (plan.kind == 2 && ea.periodic) {
+        if (plan.L == 16) return launch_cluster_ring<16, 1, 2>(c, src, dst, table_step, plan.lay.E, r_new, ea);
+        return launch_cluster_ring<8, 2, 2>(c, src, dst, table_step, plan.lay.E, r_new, ea);
+    }
     if (plan.kind == 0 && ea.periodic) {
         const int E = plan.lay.E;
         const int stages = getenv("PE3D_RING_STAGES") ? atoi(getenv("PE3D_RING_STAGES")) : 2;

@@ -239,6 +239,66 @@ def test_batch_equals_single_and_rerun_bitwise():
         assert x.final_slab.values.tobytes() == y.final_slab.values.tobytes()
 
 
+@pytest.mark.parametrize("n_azimuth", [1024, 2048, 4096])
+def test_cluster_ring_matches_direct_ring(monkeypatch, n_azimuth):
+    """Wide rings: the thread-block-cluster azimuth sweep (segments of 256
+    azimuths joined over DSMEM, cluster sizes 4/8/16) against the one-CTA
+    direct kernel (PE3D_RING_BLOCK) on the same march, and both against the
+    oracle on a short run."""
+    cfg = configs.build("cfg5", n_range=4, output_stride=2)
+    grid = cfg.grid
+    small = Config(Grid3D(4, n_azimuth, 128, grid.delta_r, 2 * math.pi / n_azimuth, grid.delta_z, grid.r_start),
+                   cfg.environment, SourceSpec((500.0,), 30.0), RunOptions(output_stride=2))
+    monkeypatch.delenv("PE3D_RING_BLOCK", raising=False)
+    got = march_frequencies(small, [500.0], flags=_native.FLAG_NO_GRAPH)[0]
+    monkeypatch.setenv("PE3D_RING_BLOCK", "1")
+    ref = march_frequencies(small, [500.0], flags=_native.FLAG_NO_GRAPH)[0]
+    # different (both exact) summation orders; near r = 0 the rings are
+    # ill-conditioned (rho -> 1), so allow rounding growth well inside 1e-9
+    assert rel_l2(got.final_slab.values, ref.final_slab.values) <= 1e-10
+    assert tl_err(got.tl_field, ref.tl_field) <= 1e-8
+    if n_azimuth == 1024:
+        orc = O.run_frequency(small, 500.0)
+        assert rel_l2(got.final_slab.values, orc.final) <= 1e-9
+        assert tl_err(got.tl_field, orc.tl_field) <= 1e-4
+
+
+@pytest.mark.parametrize("n_depth,topology", [(2048, PERIODIC), (4096, PERIODIC), (4096, SECTOR)])
+def test_cluster_depth_sweep_matches_single_cta(monkeypatch, n_depth, topology):
+    """Long columns: the depth sweep split over a cluster of 1024-row
+    sub-columns (carries over DSMEM, halo rows from global) against the
+    one-CTA-per-column kernel, and against the oracle."""
+    cfg = configs.build("cfg5", n_range=4, output_stride=2)
+    grid = cfg.grid
+    small = Config(Grid3D(4, 64, n_depth, grid.delta_r, 2 * math.pi / 64, grid.delta_z, grid.r_start,
+                          azimuth_topology=topology),
+                   cfg.environment, SourceSpec((500.0,), 600.0), RunOptions(output_stride=2))
+    monkeypatch.delenv("PE3D_DEPTH_NO_CLUSTER", raising=False)
+    got = march_frequencies(small, [500.0], flags=_native.FLAG_NO_GRAPH)[0]
+    monkeypatch.setenv("PE3D_DEPTH_NO_CLUSTER", "1")
+    ref = march_frequencies(small, [500.0], flags=_native.FLAG_NO_GRAPH)[0]
+    assert rel_l2(got.final_slab.values, ref.final_slab.values) <= 1e-12
+    assert tl_err(got.tl_field, ref.tl_field) <= 1e-9
+    orc = O.run_frequency(small, 500.0)
+    assert rel_l2(got.final_slab.values, orc.final) <= FIELD_TOL
+    assert tl_err(got.tl_field, orc.tl_field) <= TL_TOL
+
+
+@pytest.mark.parametrize("nranks", [2, 4])
+def test_cluster_ring_slab_layout(nranks):
+    """The cluster kernel on rank-chunked depth slabs (virtual ranks) equals
+    the undecomposed march with the same kernel."""
+    from paper_1711_00005_b200 import slab_march
+    cfg = configs.build("cfg5", n_range=4, output_stride=2)
+    grid = cfg.grid
+    small = Config(Grid3D(4, 2048, 256, grid.delta_r, 2 * math.pi / 2048, grid.delta_z, grid.r_start),
+                   cfg.environment, SourceSpec((500.0,), 30.0), RunOptions(output_stride=2))
+    ref = march_frequencies(small, [500.0])[0]
+    got = slab_march(small, 500.0, nranks)
+    assert got.final.tobytes() == ref.final_slab.values.tobytes()
+    assert got.tl_field.tobytes() == ref.tl_field.tobytes()
+
+
 def test_run_frequency_contract():
     grid = make_grid(n_range=10, delta_r=5.0, r_start=5.0)
     env = make_env(grid)
