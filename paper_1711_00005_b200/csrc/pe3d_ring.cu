@@ -441,7 +441,9 @@ k_azimuth_pipe(const cplx* __restrict__ src, cplx* __restrict__ dst, const cplx*
 template <int L>
 __device__ __forceinline__ int ring_slot(int m, int r) { return m * 8 + (r ^ ((m / L) & 7)); }
 
-template <int L, int RT, int STAGES>
+// CHUNKED: rank-chunked ring layout of the slab march (ea.chunk_cols /
+// chunk_gap); the standard march compiles the plain contiguous addressing.
+template <int L, int RT, int STAGES, bool CHUNKED>
 __global__ void __launch_bounds__(32 * 8 / RT)
 k_azimuth_warp(const cplx* __restrict__ src, cplx* __restrict__ dst, const cplx* __restrict__ table, int E,
                const FreqDev* __restrict__ fdev, int n_tiles, int n_depth, int64_t total_items, int items_per_cta,
@@ -461,8 +463,8 @@ k_azimuth_warp(const cplx* __restrict__ src, cplx* __restrict__ dst, const cplx*
     const int64_t it0 = int64_t(blockIdx.x) * items_per_cta;
     const int64_t it1 = it0 + items_per_cta < total_items ? it0 + items_per_cta : total_items;
     if (it0 >= it1) return;
-    const int C = ea.chunk_cols ? ea.chunk_cols : NT;   // 0: standard layout
-    const int64_t gap = ea.chunk_gap;
+    const int C = CHUNKED ? ea.chunk_cols : NT;
+    const int64_t gap = CHUNKED ? ea.chunk_gap : 0;
     auto item_base = [&](int64_t item) {
         const int fi = int(item / n_tiles);
         return ring_base(fi, int(item - int64_t(fi) * n_tiles), n_tiles, NT, C);
@@ -473,7 +475,7 @@ k_azimuth_warp(const cplx* __restrict__ src, cplx* __restrict__ dst, const cplx*
 #pragma unroll
         for (int j = 0; j < PER; ++j) {
             const int e = j * NTHR + tid;
-            cp_async16(d + ring_slot<L>(e >> 3, e & 7), g + e + (gap ? int64_t((e >> 3) / C) * gap : 0));
+            cp_async16(d + ring_slot<L>(e >> 3, e & 7), g + e + (CHUNKED ? int64_t((e >> 3) / C) * gap : 0));
         }
     };
 #pragma unroll
@@ -611,7 +613,7 @@ k_azimuth_warp(const cplx* __restrict__ src, cplx* __restrict__ dst, const cplx*
 #pragma unroll
             for (int j = 0; j < PER; ++j) {
                 const int e = j * NTHR + tid;
-                stc_stream(g + e + (gap ? int64_t((e >> 3) / C) * gap : 0), stg[ring_slot<L>(e >> 3, e & 7)]);
+                stc_stream(g + e + (CHUNKED ? int64_t((e >> 3) / C) * gap : 0), stg[ring_slot<L>(e >> 3, e & 7)]);
             }
         }
         if (++tile == n_tiles) { tile = 0; ++f; }
@@ -641,7 +643,7 @@ k_azimuth_warp(const cplx* __restrict__ src, cplx* __restrict__ dst, const cplx*
 // every peer has finished reading item i.  Persistent: every CTA of a
 // cluster walks the same item range.
 template <int L, int RT, int STAGES>
-__global__ void __launch_bounds__(32 * 8 / RT, (L == 8 ? 3 : 1))
+__global__ void __launch_bounds__(32 * 8 / RT, (L == 8 ? 3 : 2))
 k_azimuth_cluster(const cplx* __restrict__ src, cplx* __restrict__ dst, const cplx* __restrict__ table, int E,
                   const FreqDev* __restrict__ fdev, int n_theta, int n_tiles, int n_depth, int64_t total_items,
                   int items_per_cluster, double r_new, double delta_theta, EpilogueArgs ea) {
@@ -1042,9 +1044,13 @@ struct RingPlan {
     RingLayout lay;
 };
 
-static int cluster_chunk() {
-    static const int L = getenv("PE3D_CLUSTER_L") ? atoi(getenv("PE3D_CLUSTER_L")) : 8;
-    return L == 16 ? 16 : 8;
+// Segment chunk of the cluster ring kernel: 16 (segments of 512 azimuths,
+// one 8-warp CTA per SM, measured faster at cfg5) when n_theta allows it,
+// else 8 (segments of 256, three 4-warp CTAs per SM).  PE3D_CLUSTER_L forces.
+static int cluster_chunk(int n_theta) {
+    const char* env = getenv("PE3D_CLUSTER_L");
+    if (env) return atoi(env) == 16 ? 16 : 8;
+    return (n_theta % 512 == 0 && n_theta / 512 >= 2) ? 16 : 8;
 }
 
 static RingPlan ring_plan(int n_theta) {
@@ -1057,7 +1063,7 @@ static RingPlan ring_plan(int n_theta) {
         p.lay = ring_layout(n_theta, p.L, 1);     // 32 chunks, qp[0..32]
         return p;
     }
-    const int cl_L = cluster_chunk();
+    const int cl_L = cluster_chunk(n_theta);
     if (n_theta % (32 * cl_L) == 0 && n_theta / (32 * cl_L) >= 2 && n_theta / (32 * cl_L) <= 16 && !block) {
         p.kind = 2;                               // cluster of n_theta/(32L) segments
         p.L = cl_L;
@@ -1092,7 +1098,8 @@ static cudaError_t set_smem(K kern, size_t bytes) {
 template <int L, int RT, int STAGES>
 static cudaError_t launch_warp_ring(const LaunchCtx& c, const cplx* src, cplx* dst, const cplx* table_step, int E,
                                    double r_new, const EpilogueArgs& ea) {
-    auto kern = k_azimuth_warp<L, RT, STAGES>;
+    const bool chunked = ea.chunk_gap != 0 || (ea.chunk_cols != 0 && ea.chunk_cols != c.n_theta);
+    auto kern = chunked ? k_azimuth_warp<L, RT, STAGES, true> : k_azimuth_warp<L, RT, STAGES, false>;
     const int nthr = 32 * 8 / RT;
     const size_t bytes = sizeof(cplx) * (size_t(STAGES) * 32 * L * 8 + E);
     cudaError_t e = set_smem(kern, bytes);
@@ -1157,7 +1164,10 @@ cudaError_t launch_azimuth_scan(const LaunchCtx& c, const cplx* src, cplx* dst, 
                                 const EpilogueArgs& ea) {
     const RingPlan plan = ring_plan(c.n_theta);
     if (plan.kind == 2 && ea.periodic) {
-        if (plan.L == 16) return launch_cluster_ring<16, 1, 2>(c, src, dst, table_step, plan.lay.E, r_new, ea);
+        // 512-azimuth segments: single-stage CTAs (64 KB, 128 registers), two per
+        // SM, so the second CTA hides the first one's loads (measured faster at
+        // cfg5 than one double-buffered CTA per SM)
+        if (plan.L == 16) return launch_cluster_ring<16, 1, 1>(c, src, dst, table_step, plan.lay.E, r_new, ea);
         return launch_cluster_ring<8, 2, 2>(c, src, dst, table_step, plan.lay.E, r_new, ea);
     }
     if (plan.kind == 0 && ea.periodic) {

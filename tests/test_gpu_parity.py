@@ -239,10 +239,10 @@ def test_batch_equals_single_and_rerun_bitwise():
         assert x.final_slab.values.tobytes() == y.final_slab.values.tobytes()
 
 
-@pytest.mark.parametrize("n_azimuth", [1024, 2048, 4096])
-def test_cluster_ring_matches_direct_ring(monkeypatch, n_azimuth):
-    """Wide rings: the thread-block-cluster azimuth sweep (segments of 256
-    azimuths joined over DSMEM, cluster sizes 4/8/16) against the one-CTA
+@pytest.mark.parametrize("n_azimuth,chunk", [(768, None), (1024, None), (2048, None), (4096, None), (4096, "8")])
+def test_cluster_ring_matches_direct_ring(monkeypatch, n_azimuth, chunk):
+    """Wide rings: the thread-block-cluster azimuth sweep (segments of 512 or
+    256 azimuths joined over DSMEM, cluster sizes 2..16) against the one-CTA
     direct kernel (PE3D_RING_BLOCK) on the same march, and both against the
     oracle on a short run."""
     cfg = configs.build("cfg5", n_range=4, output_stride=2)
@@ -250,6 +250,8 @@ def test_cluster_ring_matches_direct_ring(monkeypatch, n_azimuth):
     small = Config(Grid3D(4, n_azimuth, 128, grid.delta_r, 2 * math.pi / n_azimuth, grid.delta_z, grid.r_start),
                    cfg.environment, SourceSpec((500.0,), 30.0), RunOptions(output_stride=2))
     monkeypatch.delenv("PE3D_RING_BLOCK", raising=False)
+    if chunk:
+        monkeypatch.setenv("PE3D_CLUSTER_L", chunk)
     got = march_frequencies(small, [500.0], flags=_native.FLAG_NO_GRAPH)[0]
     monkeypatch.setenv("PE3D_RING_BLOCK", "1")
     ref = march_frequencies(small, [500.0], flags=_native.FLAG_NO_GRAPH)[0]
