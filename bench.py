@@ -57,6 +57,9 @@ def parse():
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--shard-of", type=int, default=0,
+                   help="diagnostic: march only rank 0's frequency block of an N-way split on this one GPU "
+                        "(value then counts only that block's points)")
     return p.parse_args()
 
 
@@ -207,7 +210,8 @@ def run_gpu_arm(a, rank, world, local):
     cfg = workload(a.workload, max(a.steps, a.warmup))
     grid, env, source, _ = cfg
     all_freqs = list(source.frequencies)
-    mine = parallel.rank_frequencies(all_freqs, rank, world)
+    shard_world = a.shard_of if (a.shard_of and world == 1) else world
+    mine = parallel.rank_frequencies(all_freqs, rank, shard_world)
     F, NT, NZ = len(mine), grid.n_azimuth, grid.n_depth
     k0s = [wavenumber(f, env.c0) for f in mine]
     coeffs = _native.make_coeffs(k0s, [StepCoefficients.for_step(k0, grid.delta_r) for k0 in k0s])
@@ -259,7 +263,7 @@ def run_gpu_arm(a, rank, world, local):
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
-    total_points = len(all_freqs) * NT * NZ * a.steps
+    total_points = (len(all_freqs) if shard_world == world else F) * NT * NZ * a.steps
     value = total_points / (ms / 1e3)
 
     # ---- per-kernel timing: the same K-step march with events per launch
@@ -321,6 +325,7 @@ def run_gpu_arm(a, rank, world, local):
             "vs_baseline": None, "dtype": "c128", "data": "synthetic",
             "config": {"workload": a.workload, "frequencies": len(all_freqs), "frequencies_per_gpu": F,
                        "n_theta": NT, "n_depth": NZ, "delta_r": grid.delta_r, "parallelism": f"frequency-shard x{world}",
+                       **({"emulated_shard_of": shard_world} if shard_world != world else {}),
                        "l2": "inputs larger than L2 (field 256 MiB per buffer at N=1)" if a.workload in ("cfg4", "cfg5")
                        else "field L2-resident", "march": f"one graph of {a.steps} steps"},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -66,6 +66,10 @@ struct Handle {
     // PE3D_FLAG_PROFILE accounting
     double prof_ms[3] = {0, 0, 0};
     int32_t prof_n[3] = {0, 0, 0};
+    // concurrent step-loop chains over disjoint frequency groups
+    static constexpr int MAX_CHAINS = 4;
+    cudaStream_t chain_stream[MAX_CHAINS] = {};
+    cudaEvent_t chain_fork = nullptr, chain_join[MAX_CHAINS] = {};
 };
 
 // Launch wrapper: in profile mode, bracket each launch with events.
@@ -203,6 +207,61 @@ struct MarchPlan {
     int n_samples;
 };
 
+// Number of concurrent step-loop chains.  Frequencies are independent, so a
+// march runs two disjoint frequency groups as parallel graph branches: each
+// chain's launch ramp, pipeline fill and tail are filled by the other chain's
+// CTAs.  Measured on cfg4 (per-GPU step, 1 -> 2 chains): 64 frequencies
+// 216 -> 208 us, 32: 119 -> 105, 16: 66 -> 57, 8: 39 -> 34.5; four chains
+// are worse.  PE3D_CHAINS overrides.
+int step_chains(const pe3d::LaunchCtx& c, bool profiling) {
+    if (profiling || c.n_freq < 2) return 1;
+    const char* env = getenv("PE3D_CHAINS");
+    int n = env ? atoi(env) : 2;
+    if (n > Handle::MAX_CHAINS) n = Handle::MAX_CHAINS;
+    if (n > c.n_freq) n = c.n_freq;
+    return n < 1 ? 1 : n;
+}
+
+// Step loop of the parallel (scan) path for frequencies [f0, f0 + nf) on
+// stream `st`; all pointers are offset to the group.
+cudaError_t enqueue_group(Handle* h, const pe3d_grid* g, const MarchPlan& p, int f0, int nf, cudaStream_t st,
+                          double* d_tl, cplx* d_snap, cplx* d_final, int64_t* d_clamped, const double* d_wabs,
+                          Prof& prof) {
+    const pe3d::LaunchCtx& c = p.ctx;
+    const int E = pe3d::ring_table_elems(c.n_theta);
+    const int64_t fe = int64_t(c.n_tiles) * c.n_theta * 8;     // field elements per frequency
+    const int64_t oe = int64_t(c.n_theta) * g->n_depth;         // output elements per frequency and sample
+    pe3d::LaunchCtx cg = c;
+    cg.n_freq = nf;
+    cg.fdev = c.fdev + f0;
+    cg.loc_tab = c.loc_tab + int64_t(f0) * c.n_tiles * 8;
+    cg.mul_tab = c.mul_tab + int64_t(f0) * c.n_tiles * 8;
+    cg.stream = st;
+    cplx* A = h->field_a.as<cplx>() + f0 * fe;
+    cplx* B = h->field_b.as<cplx>() + f0 * fe;
+    for (int s = 0; s < g->n_steps; ++s) {
+        const int j_new = g->first_index + s + 1;
+        const double r_new = g->r_start + j_new * g->delta_r;      // Grid3D.range_at
+        cudaError_t e = prof.run(0, [&] { return pe3d::launch_depth_scan(cg, A, B); });
+        if (e != cudaSuccess) return e;
+        pe3d::EpilogueArgs ea{};
+        const bool record = ((s + 1) % g->output_stride) == 0;
+        ea.n_samples = p.n_samples;
+        ea.tl = record && d_tl ? d_tl + int64_t(f0) * p.n_samples * oe : nullptr;
+        ea.snap = record && d_snap ? d_snap + int64_t(f0) * p.n_samples * oe : nullptr;
+        ea.final_out = (s == g->n_steps - 1) && d_final ? d_final + f0 * oe : nullptr;
+        ea.clamped = d_clamped ? d_clamped + f0 : nullptr;
+        ea.sample = (s + 1) / g->output_stride;
+        ea.w_abs = d_wabs + int64_t(ea.sample) * g->n_freq + f0;
+        ea.periodic = true;
+        ea.write_temp = (s < g->n_steps - 1);
+        const cplx* tab = h->ring_tab.as<cplx>() + (int64_t(s) * c.n_freq + f0) * E;
+        e = prof.run(1, [&] { return pe3d::launch_azimuth_scan(cg, B, A, tab, r_new, ea); });
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
 // Enqueue the step loop (the body graphed by pe3d_march_device).
 cudaError_t enqueue_steps(Handle* h, const pe3d_grid* g, const MarchPlan& p, const cplx* d_local,
                           double* d_tl, cplx* d_snap, cplx* d_final, int64_t* d_clamped,
@@ -212,6 +271,29 @@ cudaError_t enqueue_steps(Handle* h, const pe3d_grid* g, const MarchPlan& p, con
     cplx* B = h->field_b.as<cplx>();
     cplx* C = h->field_c.as<cplx>();
     const bool periodic = g->topology == PE3D_PERIODIC;
+    if (periodic && !p.serial) {
+        const int chains = step_chains(c, prof.on);
+        if (chains == 1)
+            return enqueue_group(h, g, p, 0, c.n_freq, c.stream, d_tl, d_snap, d_final, d_clamped, d_wabs, prof);
+        cudaError_t e = cudaSuccess;
+        if (!h->chain_fork) e = cudaEventCreateWithFlags(&h->chain_fork, cudaEventDisableTiming);
+        for (int k = 0; k < chains && e == cudaSuccess; ++k) {
+            if (!h->chain_stream[k]) e = cudaStreamCreateWithFlags(&h->chain_stream[k], cudaStreamNonBlocking);
+            if (e == cudaSuccess && !h->chain_join[k])
+                e = cudaEventCreateWithFlags(&h->chain_join[k], cudaEventDisableTiming);
+        }
+        if (e == cudaSuccess) e = cudaEventRecord(h->chain_fork, c.stream);
+        for (int k = 0; k < chains && e == cudaSuccess; ++k) {
+            const int f0 = int(int64_t(c.n_freq) * k / chains), f1 = int(int64_t(c.n_freq) * (k + 1) / chains);
+            e = cudaStreamWaitEvent(h->chain_stream[k], h->chain_fork, 0);
+            if (e == cudaSuccess)
+                e = enqueue_group(h, g, p, f0, f1 - f0, h->chain_stream[k], d_tl, d_snap, d_final, d_clamped, d_wabs,
+                                  prof);
+            if (e == cudaSuccess) e = cudaEventRecord(h->chain_join[k], h->chain_stream[k]);
+            if (e == cudaSuccess) e = cudaStreamWaitEvent(c.stream, h->chain_join[k], 0);
+        }
+        return e;
+    }
     for (int s = 0; s < g->n_steps; ++s) {
         const int j_new = g->first_index + s + 1;
         const double r_new = g->r_start + j_new * g->delta_r;          // Grid3D.range_at
@@ -238,15 +320,10 @@ cudaError_t enqueue_steps(Handle* h, const pe3d_grid* g, const MarchPlan& p, con
         ea.w_abs = d_wabs + int64_t(ea.sample) * g->n_freq;
         ea.periodic = periodic;
         ea.write_temp = (s < g->n_steps - 1);
-        if (periodic && !p.serial) {
-            const cplx* tab = h->ring_tab.as<cplx>() + int64_t(s) * c.n_freq * pe3d::ring_table_elems(c.n_theta);
-            e = prof.run(1, [&] { return pe3d::launch_azimuth_scan(c, B, A, tab, r_new, ea); });
-        } else {
-            e = prof.run(1, [&] { return pe3d::launch_azimuth_serial(c, B, C, h->az_cp.as<cplx>(), h->az_inv.as<cplx>(),
-                                                                     h->az_q.as<cplx>(), h->az_ring.as<cplx>(), r_new,
-                                                                     j_new); });
-            if (e == cudaSuccess) e = prof.run(2, [&] { return pe3d::launch_finish(c, C, 1, A, r_new, ea); });
-        }
+        e = prof.run(1, [&] { return pe3d::launch_azimuth_serial(c, B, C, h->az_cp.as<cplx>(), h->az_inv.as<cplx>(),
+                                                                 h->az_q.as<cplx>(), h->az_ring.as<cplx>(), r_new,
+                                                                 j_new); });
+        if (e == cudaSuccess) e = prof.run(2, [&] { return pe3d::launch_finish(c, C, 1, A, r_new, ea); });
         if (e != cudaSuccess) return e;
     }
     return cudaSuccess;
@@ -296,6 +373,11 @@ int pe3d_handle_destroy(void* handle) {
                       &h->sb_cp, &h->sb_inv, &h->sb_y, &h->sb_q, &h->med_prof, &h->med_lat, &h->med_local})
         b->release();
     if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
+    for (int k = 0; k < Handle::MAX_CHAINS; ++k) {
+        if (h->chain_stream[k]) cudaStreamDestroy(h->chain_stream[k]);
+        if (h->chain_join[k]) cudaEventDestroy(h->chain_join[k]);
+    }
+    if (h->chain_fork) cudaEventDestroy(h->chain_fork);
     if (h->stream) cudaStreamDestroy(h->stream);
     delete h;
     return PE3D_OK;
@@ -406,6 +488,8 @@ int pe3d_march_device(void* handle, const pe3d_grid* g, const pe3d_coeffs* coeff
         add(&stream, sizeof(stream));
         const void* tabs[5] = {h->w_abs.ptr, h->fdev.ptr, h->loc_tab.ptr, h->err.ptr, h->ring_tab.ptr};
         add(tabs, sizeof(tabs));
+        const int chains = step_chains(p.ctx, false);
+        add(&chains, sizeof(chains));
         if (!(h->graph_exec && key == h->graph_key)) {
             if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
             h->graph_exec = nullptr;

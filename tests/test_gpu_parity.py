@@ -301,6 +301,24 @@ def test_cluster_ring_slab_layout(nranks):
     assert got.tl_field.tobytes() == ref.tl_field.tobytes()
 
 
+@pytest.mark.parametrize("chains", ["2", "3"])
+def test_concurrent_chains_bitwise_equal_to_one_chain(monkeypatch, chains):
+    """Disjoint frequency groups marched as concurrent graph branches
+    (PE3D_CHAINS) give bitwise the single-chain results: TL at every output
+    range, clamped counts and final slabs, with uneven groups (5 = 2+3 or
+    1+2+2 frequencies)."""
+    freqs = (50.0, 90.0, 150.0, 300.0, 500.0)
+    cfg = configs.build("cfg4", n_range=8, frequencies=freqs, output_stride=2)
+    monkeypatch.setenv("PE3D_CHAINS", "1")
+    ref = march_frequencies(cfg, list(freqs))
+    monkeypatch.setenv("PE3D_CHAINS", chains)
+    got = march_frequencies(cfg, list(freqs))
+    for x, y in zip(ref, got):
+        assert x.tl_field.tobytes() == y.tl_field.tobytes()
+        assert x.final_slab.values.tobytes() == y.final_slab.values.tobytes()
+        assert x.clamped_samples == y.clamped_samples
+
+
 def test_run_frequency_contract():
     grid = make_grid(n_range=10, delta_r=5.0, r_start=5.0)
     env = make_env(grid)
