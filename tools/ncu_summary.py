@@ -1,46 +1,87 @@
-"""Summarise an ncu report (details + raw pages) into a short text table."""
+"""Summarise an ncu --set full report into the text kept under profiles/.
+
+usage: python tools/ncu_summary.py REPORT.ncu-rep [--traffic OUT.json KEY=regex ...]
+Prints, per kernel: duration, DRAM bytes read/written and throughput, L2 hit
+rate, occupancy, issue rate, IPC, registers, top stall reasons (per issued
+instruction) and the dynamic instruction mix (from the SASS source page).
+"""
+import collections
 import csv
+import io
+import json
+import re
 import subprocess
 import sys
 
-WANT = ['Duration', 'Memory Throughput', 'DRAM Throughput', 'Compute (SM) Throughput', 'Achieved Occupancy',
-        'Theoretical Occupancy', 'Registers Per Thread', 'L1/TEX Hit Rate', 'L2 Hit Rate',
-        'Issued Warp Per Scheduler', 'No Eligible', 'Eligible Warps Per Scheduler', 'Dynamic Shared Memory Per Block',
-        'Executed Ipc Active', 'Grid Size', 'Block Size']
-RAW = ['dram__bytes_read.sum', 'dram__bytes_write.sum', 'smsp__inst_executed.sum',
-       'sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active',
-       'l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum', 'gpu__time_duration.sum']
+DETAILS = ["Duration", "DRAM Throughput", "Memory Throughput", "L2 Hit Rate", "Issued Warp Per Scheduler",
+           "Executed Ipc Active", "Achieved Occupancy", "Theoretical Occupancy", "Registers Per Thread",
+           "Grid Size", "Block Size", "Cluster Size", "Dynamic Shared Memory Per Block"]
+RAW = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "smsp__inst_executed.sum",
+       "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"]
 
 
-def run(rep):
-    out = subprocess.run(['ncu', '-i', rep, '--page', 'details', '--csv'], capture_output=True, text=True).stdout
-    rows = list(csv.reader(out.splitlines()))
+def ncu(*args):
+    return subprocess.run(["ncu", *args], capture_output=True, text=True, check=True).stdout
+
+
+def main():
+    rep = sys.argv[1]
+    out = {}
+    rows = list(csv.reader(io.StringIO(ncu("-i", rep, "--page", "details", "--csv"))))
     h = rows[0]
-    ki, mi, vi, ui = h.index('Kernel Name'), h.index('Metric Name'), h.index('Metric Value'), h.index('Metric Unit')
+    ik, im, iv, iu = (h.index(x) for x in ("Kernel Name", "Metric Name", "Metric Value", "Metric Unit"))
+    kernels = []
     for r in rows[1:]:
-        if r[mi] in WANT:
-            print(f"{r[ki][:28]:28s} | {r[mi]:32s} = {r[vi]} {r[ui]}")
-    out = subprocess.run(['ncu', '-i', rep, '--page', 'raw', '--csv'], capture_output=True, text=True).stdout
-    rows = list(csv.reader(out.splitlines()))
-    h = rows[0]
-    units = rows[1]
-    for r in rows[2:]:
-        name = r[h.index('Kernel Name')][:28]
-        for k in RAW:
-            if k in h:
-                print(f"{name:28s} | {k:32s} = {r[h.index(k)]} {units[h.index(k)]}")
-        stalls = []
-        for i, k in enumerate(h):
-            if k.startswith('smsp__average_warps_issue_stalled_') and k.endswith('_per_issue_active.ratio'):
-                try:
-                    v = float(r[i])
-                except ValueError:
-                    continue
-                if v > 0.1:
-                    stalls.append((v, k[len('smsp__average_warps_issue_stalled_'):-len('_per_issue_active.ratio')]))
-        stalls.sort(reverse=True)
-        print(f"{name:28s} | stalls: " + ", ".join(f"{n} {v:.2f}" for v, n in stalls[:8]))
+        name = r[ik].split("(")[0]
+        if name not in out:
+            out[name] = {}
+            kernels.append(name)
+        if r[im] in DETAILS:
+            out[name][r[im]] = f"{r[iv]} {r[iu]}".strip()
+    raw = list(csv.reader(io.StringIO(ncu("-i", rep, "--page", "raw", "--csv", "--metrics", ",".join(RAW)))))
+    hr = raw[0]
+    for r in raw[2:]:
+        name = r[hr.index("Kernel Name")].split("(")[0]
+        for m in RAW:
+            out[name][m] = r[hr.index(m)] + " " + raw[1][hr.index(m)]
+    for name in kernels:
+        base = re.search(r"(k_\w+)", name).group(1)
+        src = list(csv.reader(io.StringIO(ncu("-i", rep, "--page", "source", "--csv", "--print-source", "sass",
+                                              "--kernel-name", "regex:" + base + "(<|$)"))))
+        hdr, data = src[1], src[2:]
+        iE = hdr.index("Instructions Executed")
+        names = [x for x in hdr if x.startswith("stall_") and "(Not" not in x]
+        idx = {n: hdr.index(n) for n in names}
+        tot_s = sum(int(r[idx[n]] or 0) for r in data for n in names) or 1
+        stalls = sorted(((n[6:], sum(int(r[idx[n]] or 0) for r in data)) for n in names), key=lambda t: -t[1])
+        mix = collections.Counter()
+        for r in data:
+            op = r[1].strip().split()
+            if op:
+                o = op[1] if op[0].startswith("@") else op[0]
+                mix[o.split(".")[0]] += int(r[iE] or 0)
+        tot_i = sum(mix.values()) or 1
+        out[name]["stall samples (share)"] = ", ".join(f"{n} {100 * v / tot_s:.1f}%" for n, v in stalls[:8])
+        out[name]["instruction mix"] = ", ".join(f"{o} {100 * v / tot_i:.1f}%" for o, v in mix.most_common(12))
+    for name in kernels:
+        print(name)
+        for k, v in out[name].items():
+            print(f"  {k:62s} {v}")
+    if "--traffic" in sys.argv:
+        i = sys.argv.index("--traffic")
+        path, pairs = sys.argv[i + 1], sys.argv[i + 2:]
+        traffic = {}
+        for p in pairs:
+            key, pat = p.split("=")
+            for name in kernels:
+                if pat in name:
+                    rd = float(out[name]["dram__bytes_read.sum"].split()[0])
+                    wr = float(out[name]["dram__bytes_write.sum"].split()[0])
+                    unit = out[name]["dram__bytes_read.sum"].split()[1]
+                    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[unit]
+                    traffic[key] = (rd + wr) * scale
+        json.dump(traffic, open(path, "w"), indent=1)
 
 
-if __name__ == '__main__':
-    run(sys.argv[1])
+if __name__ == "__main__":
+    main()
