@@ -959,7 +959,14 @@ cudaError_t launch_depth_scan(const LaunchCtx& c, const cplx* src, cplx* dst) {
     return go(k_depth_scan<8, 512>, nt, depth_smem_elems<8, 512>(nt), DepthCfg<8, 512>::MINB);
 }
 
+// Factor tables once per march: the parallel continuant scan (pe3d_medium.cu)
+// for columns of up to 4096 rows; the reference-order single-thread
+// recurrence when PE3D_FACTOR_SERIAL is set (it was 0.46 ms per cfg4 march).
 cudaError_t launch_factor_depth(const LaunchCtx& c, const cplx* local, int64_t local_fstride, int step_for_error) {
+    if (!getenv("PE3D_FACTOR_SERIAL")) {
+        const cudaError_t e = launch_factor_depth_scan(c, local, local_fstride, step_for_error);
+        if (e != cudaErrorNotSupported) return e;
+    }
     k_factor_depth<<<c.n_freq, 1, 0, c.stream>>>(local, local_fstride, c.loc_tab, c.mul_tab, c.fdev, c.n_depth,
                                                  c.n_tiles * 8, step_for_error, c.err);
     return cudaGetLastError();

@@ -75,6 +75,7 @@ struct LaunchCtx {
 void ring_shape(int n_theta, int* L, int* RW);
 int ring_table_elems(int n_theta);   // complex entries per (step, frequency) ring table
 cudaError_t launch_factor_depth(const LaunchCtx& c, const cplx* local, int64_t local_fstride, int step_for_error);
+cudaError_t launch_factor_depth_scan(const LaunchCtx& c, const cplx* local, int64_t local_fstride, int step_for_error);
 cudaError_t launch_depth_scan(const LaunchCtx& c, const cplx* src, cplx* dst);
 cudaError_t launch_ring_setup(const LaunchCtx& c, cplx* table, int n_steps, int first_index, double r_start,
                               double delta_r);

@@ -293,6 +293,85 @@ cudaError_t launch_depth_medium_scan(const LaunchCtx& c, const MediumDev& M, con
     return cudaGetLastError();
 }
 
+// Range-independent depth factorization (tables of K1), one CTA per
+// frequency, thread t owning depth tile t: the same continuant scan as above
+// replaces the single-thread Thomas recurrence of k_factor_depth (ref
+// tridiag.py:151-167): d_l = p_l / p_(l-1), m_l = -off / d_l, loc_tab = the
+// local term, pads zero; the first pivot below the floor is reported with
+// the reference's (row, member) convention.
+__global__ void __launch_bounds__(512)
+k_factor_depth_scan(const cplx* __restrict__ local, int64_t local_fstride, cplx* __restrict__ loc_tab,
+                    cplx* __restrict__ mul_tab, const FreqDev* __restrict__ fdev, int n_depth, int n_tiles,
+                    int step_for_error, DevError* err) {
+    __shared__ M2 sM[16];
+    __shared__ int sFail;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int f = blockIdx.x;
+    const bool active = t < n_tiles;
+    const FreqDev fd = fdev[f];
+    const int nz8 = n_tiles * 8;
+    if (t == 0) sFail = 0x7fffffff;
+    const cplx off2 = cmul(fd.off_z, fd.off_z);
+    const double two_s = 2.0 * fd.s_z;
+    cplx mainv[8];
+    M2 T{cone(), czero(), czero(), cone()};
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int l = 8 * t + i;
+        const bool real_row = active && l < n_depth;
+        const cplx loc = real_row ? ldc(local + f * local_fstride + l) : czero();
+        if (active) stc(loc_tab + int64_t(f) * nz8 + l, loc);
+        mainv[i] = cadd(cone(), cmul(fd.cx_lhs, mk(loc.re - two_s, loc.im)));
+        M2 Ml;
+        if (l == 0 || !real_row) Ml = M2{cone(), czero(), czero(), cone()};   // surface / pads: identity
+        else Ml = M2{mainv[i], cneg(l == 1 ? czero() : off2), cone(), czero()};
+        T = m2norm(m2mul(Ml, T));
+    }
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const M2 Tp = shfl_up_m2(T, d);
+        if (lane >= d) T = m2norm(m2mul(T, Tp));
+    }
+    if (lane == 31) sM[warp] = T;
+    __syncthreads();
+    M2 Cw{cone(), czero(), czero(), cone()};
+    for (int w = 0; w < warp; ++w) Cw = m2norm(m2mul(sM[w], Cw));
+    M2 Tin = shfl_up_m2(m2norm(m2mul(T, Cw)), 1);
+    if (lane == 0) Tin = Cw;
+    cplx pa = Tin.a, pb = Tin.c;
+    int my_fail = 0x7fffffff;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int l = 8 * t + i;
+        cplx mult = czero();
+        if (l == 0) {
+            pa = cone(); pb = czero();                      // d_0 = main_0 = 1 (surface row)
+        } else if (active && l < n_depth) {
+            const cplx na = csub(cmul(mainv[i], pa), cmul(l == 1 ? czero() : off2, pb));
+            const cplx d = cdiv(na, pa);                    // d_l = p_l / p_(l-1)
+            if (my_fail == 0x7fffffff && cabs(d) < PIVOT_FLOOR) my_fail = l;
+            pb = pa;
+            pa = na;
+            const double sc = fmax(fabs(pa.re), fabs(pa.im));
+            if (sc > 0.0 && isfinite(sc)) { pa = crmul(1.0 / sc, pa); pb = crmul(1.0 / sc, pb); }
+            mult = cneg(cmul(fd.off_z, crecip(d)));
+        }
+        if (active) stc(mul_tab + int64_t(f) * nz8 + l, mult);
+    }
+    if (my_fail != 0x7fffffff) atomicMin(&sFail, my_fail);
+    __syncthreads();
+    if (t == 0 && sFail != 0x7fffffff) report_failure(err, fail_key(step_for_error, 0, f, 0), sFail, 0);
+}
+
+cudaError_t launch_factor_depth_scan(const LaunchCtx& c, const cplx* local, int64_t local_fstride,
+                                     int step_for_error) {
+    const int nthreads = (c.n_tiles + 31) / 32 * 32;
+    if (nthreads > 512) return cudaErrorNotSupported;
+    k_factor_depth_scan<<<c.n_freq, nthreads, 0, c.stream>>>(local, local_fstride, c.loc_tab, c.mul_tab, c.fdev,
+                                                             c.n_depth, c.n_tiles, step_for_error, c.err);
+    return cudaGetLastError();
+}
+
 // local term in the device tile layout (the starter range of the scan path)
 __global__ void k_medium_local_tiles(MediumDev M, const FreqDev* __restrict__ fdev, cplx* __restrict__ local,
                                      int n_freq, int n_theta, int n_tiles, int n_depth, double delta_theta, double dz,

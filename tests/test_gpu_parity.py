@@ -319,6 +319,19 @@ def test_concurrent_chains_bitwise_equal_to_one_chain(monkeypatch, chains):
         assert x.clamped_samples == y.clamped_samples
 
 
+def test_parallel_factorization_matches_reference_recurrence(monkeypatch):
+    """The depth tables from the continuant scan (one CTA per frequency)
+    against the reference-order single-thread Thomas recurrence."""
+    cfg = configs.build("cfg4", n_range=10, frequencies=(50.0, 120.0, 500.0), output_stride=5)
+    monkeypatch.setenv("PE3D_FACTOR_SERIAL", "1")
+    ref = march_frequencies(cfg, [50.0, 120.0, 500.0], flags=_native.FLAG_NO_GRAPH)
+    monkeypatch.delenv("PE3D_FACTOR_SERIAL")
+    got = march_frequencies(cfg, [50.0, 120.0, 500.0], flags=_native.FLAG_NO_GRAPH)
+    for x, y in zip(ref, got):
+        assert rel_l2(y.final_slab.values, x.final_slab.values) <= 1e-12
+        assert tl_err(y.tl_field, x.tl_field) <= 1e-9
+
+
 def test_run_frequency_contract():
     grid = make_grid(n_range=10, delta_r=5.0, r_start=5.0)
     env = make_env(grid)
