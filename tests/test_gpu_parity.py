@@ -394,6 +394,27 @@ def test_criterion_06_convergence_order():
     assert math.log2(e1 / e2) >= 1.0
 
 
+@pytest.mark.parametrize("chains", ["1", "2"])
+def test_criterion_07_executor_invariance(monkeypatch, chains):
+    """Reference criterion 7 (tests/test_acceptance.py): TL digests are
+    bitwise identical for every executor configuration.  Here: workers,
+    schedule and intra_threads of frequency_farm, and the number of
+    concurrent step chains."""
+    import hashlib
+    from paper_1711_00005_b200 import frequency_farm
+    monkeypatch.setenv("PE3D_CHAINS", chains)
+    cfg = configs.build("cfg1", n_range=40, frequencies=(50.0, 65.0, 80.0), output_stride=10)
+    digests = set()
+    for workers, schedule, intra in [(1, "static", 1), (2, "static", 1), (4, "dynamic", 2), (3, "dynamic", 8)]:
+        rep = frequency_farm(cfg, [50.0, 65.0, 80.0], workers=workers, schedule=schedule, intra_threads=intra)
+        assert not rep.failures
+        h = hashlib.sha256()
+        for r in rep.results:
+            h.update(np.ascontiguousarray(r.tl_field).tobytes())
+        digests.add(h.hexdigest())
+    assert len(digests) == 1
+
+
 def O_local(env, grid, k0):
     from paper_1711_00005_b200.environment import local_term_grid
     return local_term_grid(env, grid, grid.r_start, k0)[0]
