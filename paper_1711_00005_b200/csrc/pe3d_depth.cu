@@ -948,11 +948,6 @@ cudaError_t launch_depth_scan(const LaunchCtx& c, const cplx* src, cplx* dst) {
         cudaError_t e = launch_depth_tma(c, src, dst);
         if (e != cudaErrorNotSupported) return e;
     }
-    const bool rpt4 = getenv("PE3D_DEPTH_RPT4") != nullptr;
-    if (rpt4 && nz8 / 4 <= 256) {
-        const int nt = round32(nz8 / 4);
-        return go(k_depth_scan<4, 256>, nt, depth_smem_elems<4, 256>(nt), DepthCfg<4, 256>::MINB);
-    }
     const int nt = round32(c.n_tiles);
     if (nt <= 128) return go(k_depth_scan<8, 128>, nt, depth_smem_elems<8, 128>(nt), DepthCfg<8, 128>::MINB);
     if (nt <= 256) return go(k_depth_scan<8, 256>, nt, depth_smem_elems<8, 256>(nt), DepthCfg<8, 256>::MINB);
