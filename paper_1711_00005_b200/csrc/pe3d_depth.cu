@@ -930,7 +930,6 @@ static cudaError_t launch_depth_tma(const LaunchCtx& c, const cplx* src, cplx* d
 
 cudaError_t launch_depth_scan(const LaunchCtx& c, const cplx* src, cplx* dst) {
     const int64_t total = int64_t(c.n_freq) * c.n_theta;
-    const int nz8 = c.n_tiles * 8;
     auto go = [&](auto kern, int nthreads, size_t elems, int per_sm) -> cudaError_t {
         const size_t sm = sizeof(cplx) * elems;
         if (sm > 48 * 1024) {
