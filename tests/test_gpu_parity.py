@@ -465,6 +465,30 @@ def test_slab_march_matches_single_gpu_march(nranks):
     assert got.clamped_samples == ref.clamped_samples
 
 
+def test_slab_march_real_nccl_one_rank():
+    """The NCCL transport of the slab march (dlopen'd libnccl, unique id
+    broadcast through torch.distributed, ncclCommInitRank, grouped
+    send/recv) with a single rank on one GPU: bitwise the plain march."""
+    import torch.distributed as dist
+    from paper_1711_00005_b200 import slab
+    cfg = configs.build("cfg5", n_range=4, output_stride=2)
+    grid = cfg.grid
+    small = Config(Grid3D(4, 256, 512, grid.delta_r, 2 * math.pi / 256, grid.delta_z, grid.r_start),
+                   cfg.environment, SourceSpec((500.0,), 100.0), RunOptions(output_stride=2))
+    ref = march_frequencies(small, [500.0])[0]
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        got = slab.distributed_slab_march(small, 500.0, device=0)
+    finally:
+        dist.destroy_process_group()
+    assert got.final.tobytes() == ref.final_slab.values.tobytes()
+    assert got.tl_field.tobytes() == ref.tl_field.tobytes()
+
+
 def test_slab_march_cfg5_full_size_vs_reference(golden):
     from paper_1711_00005_b200 import slab_march
     fx = golden("cfg5_f500_3steps.npz")
