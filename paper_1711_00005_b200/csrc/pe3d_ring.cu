@@ -1023,6 +1023,77 @@ k_finish(const cplx* __restrict__ src, int src_tiled, cplx* __restrict__ dst, co
                         cone(), fd.cy_rhs, s, sFirst, sLast, dst + tile_off, in_range);
 }
 
+// March prologue from the reference layout u0 [f][m][l] (depth fastest):
+// boundary, the starting TL sample / snapshot, and the first temp = [1 +
+// cy_rhs Y] u in the device tiles.  A CTA owns 32 azimuths x 64 depths of
+// one frequency and stages them (plus one azimuth of halo either side) in
+// shared memory, so u0 is read as 1 KB runs, TL is written as depth runs and
+// the tiles as 4 KB runs.  Same arithmetic as ring_epilogue with scale 1.
+constexpr int PREP_MB = 32, PREP_DB = 64;
+__global__ void __launch_bounds__(256)
+k_prepare(const cplx* __restrict__ u0, cplx* __restrict__ dst, const FreqDev* __restrict__ fdev, int n_theta,
+          int n_tiles, int n_depth, double r, double delta_theta, EpilogueArgs ea) {
+    __shared__ cplx sx[PREP_MB + 2][PREP_DB];
+    __shared__ unsigned long long szeros;
+    const int f = blockIdx.z;
+    const int m0 = blockIdx.x * PREP_MB, l0 = blockIdx.y * PREP_DB;
+    const int tid = threadIdx.x;
+    const bool periodic = ea.periodic;
+    if (tid == 0) szeros = 0;
+    // stage azimuths m0-1 .. m0+MB (periodic wrap, zero exterior for a sector)
+    for (int e = tid; e < (PREP_MB + 2) * PREP_DB; e += blockDim.x) {
+        const int a = e / PREP_DB, dl = e % PREP_DB;
+        int m = m0 - 1 + a;
+        const int l = l0 + dl;
+        bool ok = l < n_depth && l + ea.row_offset != 0;
+        if (m < 0 || m >= n_theta) {
+            if (periodic) m = (m + n_theta) % n_theta;
+            else ok = false;
+        }
+        if (!periodic && (m == 0 || m == n_theta - 1)) ok = false;    // sector edges (marching.py:87-89)
+        sx[a][dl] = ok ? ldc(u0 + (int64_t(f) * n_theta + m) * n_depth + l) : czero();
+    }
+    __syncthreads();
+    const FreqDev fd = fdev[f];
+    const double s = azimuth_scale(fd.k0, r, delta_theta);
+    const cplx b2 = crmul(s, fd.cy_rhs);                     // scale 1: b2 = alpha, b1 = 1 - 2 alpha
+    const cplx b1 = csub(cone(), cadd(b2, b2));
+    // TL / snapshot / final in the reference layout: depth-fastest runs
+    if (ea.tl || ea.snap || ea.final_out) {
+        unsigned long long zeros = 0;
+        for (int e = tid; e < PREP_MB * PREP_DB; e += blockDim.x) {
+            const int a = e / PREP_DB, dl = e % PREP_DB;
+            const int m = m0 + a, l = l0 + dl;
+            if (l >= n_depth) continue;
+            const cplx uf = sx[a + 1][dl];
+            const int64_t so = (int64_t(f) * ea.n_samples + ea.sample) * n_theta * n_depth + (int64_t(m) * n_depth + l);
+            if (ea.tl) {
+                const double mag = cabs(uf) * ea.w_abs[f];
+                if (mag == 0.0) ++zeros;
+                ea.tl[so] = (mag == 0.0) ? TL_FLOOR_DB : -20.0 * log10(mag);
+            }
+            if (ea.snap) stc(ea.snap + so, uf);
+            if (ea.final_out) stc(ea.final_out + (int64_t(f) * n_theta + m) * n_depth + l, uf);
+        }
+        if (ea.tl && zeros) atomicAdd(&szeros, zeros);
+    }
+    // next temp into the device tiles: tile-major, 32 azimuths x 8 rows = 4 KB runs
+    if (ea.write_temp) {
+        cplx* base = dst + ring_base(f, 0, n_tiles, n_theta, n_theta);
+        for (int e = tid; e < PREP_MB * PREP_DB; e += blockDim.x) {
+            const int tl = e / (PREP_MB * 8), rem = e % (PREP_MB * 8);
+            const int a = rem / 8, rr = rem % 8;
+            const int dl = tl * 8 + rr;
+            const int tile = (l0 + dl) >> 3;
+            if (tile >= n_tiles) continue;
+            const cplx um = sx[a][dl], uc = sx[a + 1][dl], up = sx[a + 2][dl];
+            stc_stream(base + (int64_t(tile) * n_theta + m0 + a) * 8 + rr, cfma(b1, uc, cmul(b2, cadd(up, um))));
+        }
+    }
+    __syncthreads();
+    if (tid == 0 && szeros) atomicAdd(reinterpret_cast<unsigned long long*>(ea.clamped + f), szeros);
+}
+
 // ------------------------------------------------------------ launchers
 
 static int round32(int x) { return (x + 31) / 32 * 32; }
@@ -1237,6 +1308,12 @@ cudaError_t launch_azimuth_scan(const LaunchCtx& c, const cplx* src, cplx* dst, 
 
 cudaError_t launch_finish(const LaunchCtx& c, const cplx* src, int src_tiled, cplx* dst, double r,
                           const EpilogueArgs& ea) {
+    const bool standard = ea.chunk_gap == 0 && (ea.chunk_cols == 0 || ea.chunk_cols == c.n_theta);
+    if (!src_tiled && standard && c.n_theta % PREP_MB == 0 && !getenv("PE3D_PREPARE_RINGS")) {
+        dim3 grid(c.n_theta / PREP_MB, (c.n_tiles * 8 + PREP_DB - 1) / PREP_DB, c.n_freq);
+        k_prepare<<<grid, 256, 0, c.stream>>>(src, dst, c.fdev, c.n_theta, c.n_tiles, c.n_depth, r, c.delta_theta, ea);
+        return cudaGetLastError();
+    }
     int L, RW;
     ring_shape(c.n_theta, &L, &RW);
     const int n_chunks = (c.n_theta + L - 1) / L;
