@@ -286,6 +286,20 @@ def test_cluster_depth_sweep_matches_single_cta(monkeypatch, n_depth, topology):
     assert tl_err(got.tl_field, orc.tl_field) <= TL_TOL
 
 
+def test_cluster_kernels_deterministic():
+    """Race check for the DSMEM exchanges (st.async + mbarrier, double
+    buffered): a march that runs both cluster kernels (4096-row columns,
+    2048-azimuth rings) five times gives bitwise identical results."""
+    cfg = configs.build("cfg5", n_range=6, output_stride=3)
+    grid = cfg.grid
+    small = Config(Grid3D(6, 2048, 4096, grid.delta_r, 2 * math.pi / 2048, grid.delta_z, grid.r_start),
+                   cfg.environment, SourceSpec((500.0,), 600.0), RunOptions(output_stride=3))
+    runs = [march_frequencies(small, [500.0], flags=_native.FLAG_NO_GRAPH)[0] for _ in range(5)]
+    for r in runs[1:]:
+        assert r.final_slab.values.tobytes() == runs[0].final_slab.values.tobytes()
+        assert r.tl_field.tobytes() == runs[0].tl_field.tobytes()
+
+
 @pytest.mark.parametrize("nranks", [2, 4])
 def test_cluster_ring_slab_layout(nranks):
     """The cluster kernel on rank-chunked depth slabs (virtual ranks) equals
