@@ -282,17 +282,26 @@ cudaError_t enqueue_steps(Handle* h, const pe3d_grid* g, const MarchPlan& p, con
             if (e == cudaSuccess && !h->chain_join[k])
                 e = cudaEventCreateWithFlags(&h->chain_join[k], cudaEventDisableTiming);
         }
-        if (e == cudaSuccess) e = cudaEventRecord(h->chain_fork, c.stream);
-        for (int k = 0; k < chains && e == cudaSuccess; ++k) {
+        if (e != cudaSuccess) return e;
+        e = cudaEventRecord(h->chain_fork, c.stream);
+        if (e != cudaSuccess) return e;
+        // every forked chain is joined back, also after a failed launch, so a
+        // stream capture in progress can always be ended cleanly
+        cudaError_t first = cudaSuccess;
+        for (int k = 0; k < chains; ++k) {
             const int f0 = int(int64_t(c.n_freq) * k / chains), f1 = int(int64_t(c.n_freq) * (k + 1) / chains);
             e = cudaStreamWaitEvent(h->chain_stream[k], h->chain_fork, 0);
-            if (e == cudaSuccess)
+            if (e != cudaSuccess) { if (first == cudaSuccess) first = e; break; }
+            if (first == cudaSuccess) {
                 e = enqueue_group(h, g, p, f0, f1 - f0, h->chain_stream[k], d_tl, d_snap, d_final, d_clamped, d_wabs,
                                   prof);
-            if (e == cudaSuccess) e = cudaEventRecord(h->chain_join[k], h->chain_stream[k]);
-            if (e == cudaSuccess) e = cudaStreamWaitEvent(c.stream, h->chain_join[k], 0);
+                if (e != cudaSuccess) first = e;
+            }
+            cudaError_t e2 = cudaEventRecord(h->chain_join[k], h->chain_stream[k]);
+            if (e2 == cudaSuccess) e2 = cudaStreamWaitEvent(c.stream, h->chain_join[k], 0);
+            if (e2 != cudaSuccess && first == cudaSuccess) first = e2;
         }
-        return e;
+        return first;
     }
     for (int s = 0; s < g->n_steps; ++s) {
         const int j_new = g->first_index + s + 1;

@@ -1127,7 +1127,9 @@ static int cluster_chunk(int n_theta) {
 static RingPlan ring_plan(int n_theta) {
     RingPlan p;
     const bool block = getenv("PE3D_RING_BLOCK") != nullptr;
-    if (n_theta % 32 == 0 && n_theta / 32 >= 2 && n_theta / 32 <= 16 && !block) {
+    // ring-per-warp kernels are instantiated for L = 2, 4, 8, 16 (see launch_azimuth_scan)
+    const int Lw = n_theta / 32;
+    if (n_theta % 32 == 0 && (Lw == 2 || Lw == 4 || Lw == 8 || Lw == 16) && !block) {
         p.kind = 0;
         p.L = n_theta / 32;
         p.RW = 1;
