@@ -176,6 +176,21 @@ def test_ragged_grids_vs_oracle(topology, n_azimuth, n_depth):
         assert r.tl_field.shape == ref.tl_field.shape
 
 
+@pytest.mark.parametrize("n_azimuth,n_depth", [(768, 40), (1280, 24), (4000, 16), (64, 1500), (32, 2050), (96, 4096)])
+def test_ragged_wide_and_deep_grids_vs_oracle(n_azimuth, n_depth):
+    """The wide-ring (clusters of 3 and 5 segments, the direct kernel at
+    4000 azimuths) and long-column paths (1500 and 2050 rows: the 512-thread
+    TMA column kernel; 4096 rows: the cluster column kernel) on ragged sizes,
+    against the oracle."""
+    grid = make_grid(n_range=3, n_azimuth=n_azimuth, n_depth=n_depth, delta_r=5.0, delta_z=1.0, r_start=5.0)
+    env = make_env(grid)
+    cfg = Config(grid, env, SourceSpec((60.0,), 0.4 * grid.depth_extent), RunOptions(output_stride=1))
+    r = march_frequencies(cfg, [60.0])[0]
+    ref = O.run_frequency(cfg, 60.0)
+    assert rel_l2(r.final_slab.values, ref.final) <= FIELD_TOL
+    assert tl_err(r.tl_field, ref.tl_field) <= TL_TOL
+
+
 def test_singular_depth_becomes_step_error():
     grid = make_grid(n_azimuth=4, n_depth=8, delta_z=1.0)
     env = make_env(grid)
