@@ -364,7 +364,9 @@ def run_gpu_arm(a, rank, world, local):
 
 
 def run_slab_arm(a, rank, world, local):
-    """cfg5 on N GPUs: one grid, slab-decomposed (NCCL all-to-all transposes)."""
+    """cfg5 on N GPUs: one grid, slab-decomposed; the two transposes per step
+    are peer-direct stores over NVLink fused into the sweeps (NCCL
+    all-to-all when the shape does not allow it)."""
     import torch
     import torch.distributed as dist
     from paper_1711_00005_b200 import slab
@@ -375,8 +377,9 @@ def run_slab_arm(a, rank, world, local):
     f = cfg.source.frequencies[0]
     slab.distributed_slab_march(cfg, f, device=local, n_steps=a.warmup)
     dist.barrier()
+    transport = "peer" if slab.peer_transport_ok(grid, world) else "nccl"
     with ClockSampler(local) as clocks:
-        res = slab.distributed_slab_march(cfg, f, device=local, n_steps=a.steps)
+        res = slab.distributed_slab_march(cfg, f, device=local, n_steps=a.steps, transport=transport)
     t = torch.tensor([res.step_ms], device="cuda", dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
@@ -389,7 +392,8 @@ def run_slab_arm(a, rank, world, local):
             "dtype": "c128", "data": "synthetic",
             "config": {"workload": a.workload, "frequencies": 1, "n_theta": grid.n_azimuth, "n_depth": grid.n_depth,
                        "parallelism": f"slab x{world}: depth sweep on azimuth slabs, azimuth sweep on depth slabs, "
-                                      "2 NCCL all-to-all per step"},
+                                      + ("transposes fused into the sweeps as NVLink peer stores (CUDA IPC)"
+                                         if transport == "peer" else "2 NCCL all-to-all per step")},
             "roofline": {"bound": "hbm+nvlink", "achieved": STEP_BYTES_PER_POINT * value / world / 1e9, "peak": peak,
                          "unit": "GB/s", "frac": STEP_BYTES_PER_POINT * value / world / 1e9 / peak,
                          "peak_source": kind, "traffic": None},

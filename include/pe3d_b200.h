@@ -198,13 +198,16 @@ PE3D_API int pe3d_solve_batch_host(void* handle, int32_t n, int32_t members, int
  * Slab-decomposed march of ONE large grid over nranks GPUs (SURVEY.md §8(e),
  * BASELINE cfg5): the depth sweep runs on azimuth slabs (nranks column
  * ranges), the azimuth sweep on depth slabs (nranks tile ranges), joined
- * twice per step by an equal-split all-to-all (NCCL send/recv pairs), with
+ * twice per step by an equal-split all-to-all (NCCL send/recv pairs, or the
+ * peer-direct stores of pe3d_march_slab_p2p below), with
  * the ring sweep reading/writing the rank-chunked layout the all-to-all
  * delivers (no pack/unpack kernels).  No reference counterpart: the
  * reference never splits one frequency's grid.
  *
  * nccl_id == NULL: nranks VIRTUAL ranks driven by this process on its one
- *   device (device-to-device copies as the transport); u0 / u_final are full
+ *   device (peer-direct stores into the other virtual ranks' buffers, or
+ *   device-to-device copies when PE3D_SLAB_COPY is set or the shape does not
+ *   allow peer output); u0 / u_final are full
  *   [n_theta][n_depth] slabs and tl is [S][n_theta][n_depth].
  * nccl_id != NULL: this process is rank `rank` of nranks (one GPU each; id
  *   from pe3d_slab_unique_id on rank 0, broadcast by the caller); u0 /
@@ -218,6 +221,32 @@ PE3D_API int pe3d_slab_unique_id(void* out, int32_t bytes);
 PE3D_API int pe3d_march_slab(void* handle, const pe3d_grid* grid, const pe3d_coeffs* coeffs, int32_t nranks,
                              int32_t rank, const void* nccl_id, const pe3d_c128* local, const pe3d_c128* u0,
                              pe3d_c128* u_final, double* tl, int64_t* clamped, double* ms_steps, pe3d_error* err);
+
+/*
+ * Peer-direct (fused) transposes of the slab march: the depth sweep of rank
+ * p stores its output tiles straight into the azimuth-sweep input of every
+ * rank (NVLink peer memory mapped with CUDA IPC), and the azimuth sweep
+ * stores its next temp straight into the depth-sweep inputs; device-side
+ * counters order the sweeps across ranks.  No all-to-all and no send/receive
+ * buffers.  (The virtual-rank mode of pe3d_march_slab uses the same kernels
+ * with all ranks' buffers on one device, unless PE3D_SLAB_COPY is set.)
+ *
+ * pe3d_slab_p2p_export: allocate this rank's slab buffers for `grid` on the
+ *   handle's device, reset its counters, and write PE3D_SLAB_IPC_BYTES bytes
+ *   of CUDA IPC handles to `out`.
+ * pe3d_march_slab_p2p: `blobs` holds the nranks exported blobs in rank
+ *   order.  Every rank must have exported (its counters reset) before any
+ *   rank starts marching -- the caller barriers in between.  u0 / u_final /
+ *   tl are this rank's depth slab as in pe3d_march_slab.
+ * Requirements as pe3d_march_slab, plus n_depth / (8 nranks) % 32 == 0 and
+ * nranks <= 16.
+ */
+#define PE3D_SLAB_IPC_BYTES 192
+PE3D_API int pe3d_slab_p2p_export(void* handle, const pe3d_grid* grid, int32_t nranks, int32_t rank, void* out,
+                                  pe3d_error* err);
+PE3D_API int pe3d_march_slab_p2p(void* handle, const pe3d_grid* grid, const pe3d_coeffs* coeffs, int32_t nranks,
+                                 int32_t rank, const void* blobs, const pe3d_c128* local, const pe3d_c128* u0,
+                                 pe3d_c128* u_final, double* tl, int64_t* clamped, double* ms_steps, pe3d_error* err);
 
 /*
  * pe3d_profile_last -- kernel timings of the last march run with

@@ -60,6 +60,8 @@ struct Handle {
     DevBuf sb_in, sb_x, sb_cp, sb_inv, sb_y, sb_q;
     // extended medium (profile, lattice, two local-term grids)
     DevBuf med_prof, med_lat, med_local;
+    // slab march: ordering counters of the peer-direct transposes
+    DevBuf slab_flags;
     // one cached step-loop graph (reused when a march repeats with identical arguments)
     std::vector<unsigned char> graph_key;
     cudaGraphExec_t graph_exec = nullptr;
@@ -379,7 +381,7 @@ int pe3d_handle_destroy(void* handle) {
     for (DevBuf* b : {&h->field_a, &h->field_b, &h->field_c, &h->loc_tab, &h->mul_tab, &h->fdev, &h->w_abs, &h->err,
                       &h->az_cp, &h->az_inv, &h->az_q, &h->az_ring, &h->fail_row, &h->fail_mag, &h->ring_tab, &h->h_local,
                       &h->h_local2, &h->h_u0, &h->h_final, &h->h_tl, &h->h_snap, &h->h_clamped, &h->sb_in, &h->sb_x,
-                      &h->sb_cp, &h->sb_inv, &h->sb_y, &h->sb_q, &h->med_prof, &h->med_lat, &h->med_local})
+                      &h->sb_cp, &h->sb_inv, &h->sb_y, &h->sb_q, &h->med_prof, &h->med_lat, &h->med_local, &h->slab_flags})
         b->release();
     if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
     for (int k = 0; k < Handle::MAX_CHAINS; ++k) {
@@ -664,7 +666,7 @@ int pe3d_solve_batch_host(void* handle, int32_t n, int32_t members, int32_t cycl
     const int64_t total = e_sub + e_main + e_sup + e_rhs;
     CK(h->sb_in.ensure(total * sizeof(cplx)), "alloc");
     CK(h->sb_x.ensure(int64_t(members) * n * sizeof(cplx)), "alloc");
-    for (DevBuf* b : {&h->sb_cp, &h->sb_inv, &h->sb_y, &h->sb_q, &h->med_prof, &h->med_lat, &h->med_local}) CK(b->ensure(int64_t(members) * n * sizeof(cplx)), "alloc");
+    for (DevBuf* b : {&h->sb_cp, &h->sb_inv, &h->sb_y, &h->sb_q}) CK(b->ensure(int64_t(members) * n * sizeof(cplx)), "alloc");
     CK(h->fail_row.ensure(int64_t(members) * sizeof(int)), "alloc");
     CK(h->fail_mag.ensure(int64_t(members) * sizeof(double)), "alloc");
     CK(h->err.ensure(sizeof(pe3d::DevError)), "alloc");
@@ -914,22 +916,29 @@ int pe3d_slab_unique_id(void* out, int32_t bytes) {
     return PE3D_OK;
 }
 
-int pe3d_march_slab(void* handle, const pe3d_grid* g, const pe3d_coeffs* coeffs, int32_t N, int32_t rank,
-                    const void* nccl_id, const pe3d_c128* local, const pe3d_c128* u0, pe3d_c128* u_final, double* tl,
-                    int64_t* clamped, double* ms_steps, pe3d_error* err) {
-    Handle* h = static_cast<Handle*>(handle);
-    if (!h) return bad_arg(err, "null handle");
-    int st = check_grid(g, coeffs, err);
-    if (st != PE3D_OK) return st;
-    if (g->n_freq != 1) return bad_arg(err, "slab march: n_freq == 1");
-    if (g->topology != PE3D_PERIODIC) return bad_arg(err, "slab march: periodic azimuth");
-    if (N < 1 || g->n_theta % N || g->n_depth % (8 * N)) return bad_arg(err, "slab march: n_theta % N, n_depth % 8N");
-    if (!local || !u0) return bad_arg(err, "null local or u0");
-    const bool virt = nccl_id == nullptr;
-    if (!virt && (rank < 0 || rank >= N)) return bad_arg(err, "rank out of range");
-    CK(cudaSetDevice(h->device), "cudaSetDevice");
-    cudaStream_t s = h->stream;
+// Slab buffers of one rank in the peer-direct transport: A (depth-sweep
+// input, azimuth slab), R (azimuth-sweep input, depth slab, rank-chunked) and
+// the two ordering counters (K1 done, K2 done).
+struct SlabPeer {
+    cplx* A;
+    cplx* R;
+    unsigned long long* flags;
+};
 
+enum SlabMode { SLAB_VIRT_COPY, SLAB_VIRT_PEER, SLAB_NCCL, SLAB_IPC_PEER };
+
+static bool slab_peer_ok(const pe3d_grid* g, int N) {
+    const int NZT = g->n_depth / 8, NZT_s = NZT / N;
+    return NZT_s % 32 == 0 && (NZT <= 512 || (NZT % 128 == 0 && NZT / 128 <= 8));
+}
+
+static int slab_impl(Handle* h, const pe3d_grid* g, const pe3d_coeffs* coeffs, int32_t N, int32_t rank,
+                     SlabMode mode, const void* nccl_id, const SlabPeer* peers, const pe3d_c128* local,
+                     const pe3d_c128* u0, pe3d_c128* u_final, double* tl, int64_t* clamped, double* ms_steps,
+                     pe3d_error* err) {
+    cudaStream_t s = h->stream;
+    const bool virt = mode == SLAB_VIRT_COPY || mode == SLAB_VIRT_PEER;
+    const bool peer = mode == SLAB_VIRT_PEER || mode == SLAB_IPC_PEER;
     const int NT = g->n_theta, NZ = g->n_depth, NZT = NZ / 8;
     const int C = NT / N, NZT_s = NZT / N, NZ_s = NZ / N;
     const int64_t part = int64_t(NZT) * C * 8;             // elements per rank buffer
@@ -939,7 +948,7 @@ int pe3d_march_slab(void* handle, const pe3d_grid* g, const pe3d_coeffs* coeffs,
     const int r0 = virt ? 0 : rank;
 
     ncclComm_t comm = nullptr;
-    if (!virt && N > 1) {
+    if (mode == SLAB_NCCL && N > 1) {
         Nccl& n = nccl();
         if (!n.ok) return cuda_fail(err, cudaErrorNotSupported, "libnccl.so.2 not loadable");
         ncclUniqueId id;
@@ -956,13 +965,27 @@ int pe3d_march_slab(void* handle, const pe3d_grid* g, const pe3d_coeffs* coeffs,
     } guard{comm};
 
     std::vector<pe3d::FreqDev> fd = freq_table(g, coeffs);
-    // buffers: per driven rank A (K1 in / B->A recv), B (K1 out / A->B send), Rb (K2 in), W (K2 out)
-    CK(h->field_a.ensure(size_t(R) * part * 2 * sizeof(cplx)), "alloc");
-    CK(h->field_b.ensure(size_t(R) * part * 2 * sizeof(cplx)), "alloc");
+    // buffers.  Copy / NCCL transports: per driven rank A (K1 in), B (K1 out),
+    // Rb (K2 in), W (K2 out).  Peer transports: A and Rb only -- the sweeps
+    // store straight into the owners' inputs.
+    if (mode != SLAB_IPC_PEER) {
+        CK(h->field_a.ensure(size_t(R) * part * (peer ? 1 : 2) * sizeof(cplx)), "alloc");
+        CK(h->field_b.ensure(size_t(R) * part * (peer ? 1 : 2) * sizeof(cplx)), "alloc");
+    }
     cplx* Abuf = h->field_a.as<cplx>();
     cplx* Bbuf = Abuf + int64_t(R) * part;
     cplx* Rbuf = h->field_b.as<cplx>();
     cplx* Wbuf = Rbuf + int64_t(R) * part;
+    std::vector<SlabPeer> P(N);                             // every rank's A / R / counters
+    if (mode == SLAB_VIRT_PEER) {
+        CK(h->slab_flags.ensure(size_t(N) * 2 * sizeof(unsigned long long)), "alloc");
+        CK(cudaMemsetAsync(h->slab_flags.ptr, 0, size_t(N) * 2 * sizeof(unsigned long long), s), "memset");
+        for (int q = 0; q < N; ++q)
+            P[q] = {Abuf + q * part, Rbuf + q * part, h->slab_flags.as<unsigned long long>() + 2 * q};
+    } else if (mode == SLAB_IPC_PEER) {
+        for (int q = 0; q < N; ++q) P[q] = peers[q];
+    }
+    auto own = [&](int q) -> const SlabPeer& { return P[virt ? q : rank]; };
     CK(h->loc_tab.ensure(int64_t(NZ) * sizeof(cplx)), "alloc");
     CK(h->mul_tab.ensure(int64_t(NZ) * sizeof(cplx)), "alloc");
     CK(h->fdev.ensure(sizeof(pe3d::FreqDev)), "alloc");
@@ -1020,7 +1043,25 @@ int pe3d_march_slab(void* handle, const pe3d_grid* g, const pe3d_coeffs* coeffs,
         ea.n_samples = S;
         return ea;
     };
-    // transport W -> A (after K2) and B -> R (after K1)
+    // peer-direct transposes: K2 of depth slab q writes azimuth chunk p of its
+    // next temp into A_p at chunk q; K1 of azimuth slab p writes depth slab q
+    // of its output into R_q at chunk p
+    auto set_peers_k2 = [&](pe3d::EpilogueArgs& ea, int q) {
+        for (int p = 0; p < N; ++p) ea.peer[p] = P[p].A + int64_t(r0 + q) * chunk;
+    };
+    auto k1_ctx = [&](int p) {
+        pe3d::LaunchCtx c = c1;
+        if (peer) {
+            c.n_peers = N;
+            c.peer_tiles = NZT_s;
+            for (int q = 0; q < N; ++q) c.peer_dst[q] = P[q].R + int64_t(r0 + p) * chunk;
+        }
+        return c;
+    };
+    std::vector<unsigned long long*> f0(N), f1(N);          // every rank's K1-done / K2-done counters
+    if (peer)
+        for (int q = 0; q < N; ++q) { f0[q] = P[q].flags; f1[q] = P[q].flags + 1; }
+    // transport W -> A (after K2) and B -> R (after K1), copy / NCCL modes
     auto transpose = [&](cplx* send_base, cplx* recv_base) -> cudaError_t {
         if (virt) {
             for (int a = 0; a < N; ++a)          // sender
@@ -1043,7 +1084,7 @@ int pe3d_march_slab(void* handle, const pe3d_grid* g, const pe3d_coeffs* coeffs,
         return n.groupEnd() == ncclSuccess ? cudaSuccess : cudaErrorUnknown;
     };
 
-    // starter on depth slabs -> first temp (chunked, in W) -> A
+    // starter on depth slabs -> first temp (into W, or straight into every A)
     for (int q = 0; q < R; ++q) {
         pe3d::EpilogueArgs ea0 = ring_ea(q);
         ea0.tl = tl ? h->h_tl.as<double>() + int64_t(q) * S * slab_s : nullptr;
@@ -1051,18 +1092,31 @@ int pe3d_march_slab(void* handle, const pe3d_grid* g, const pe3d_coeffs* coeffs,
         ea0.w_abs = h->w_abs.as<double>();
         ea0.sample = 0;
         ea0.write_temp = g->n_steps > 0;
-        CK(pe3d::launch_finish(c2, h->h_u0.as<cplx>() + q * slab_s, 0, Wbuf + q * part, g->r_input, ea0), "prepare");
+        if (peer && g->n_steps > 0) set_peers_k2(ea0, q);
+        CK(pe3d::launch_finish(c2, h->h_u0.as<cplx>() + q * slab_s, 0, peer ? own(q).R : Wbuf + q * part,
+                               g->r_input, ea0), "prepare");
+        if (peer) CK(pe3d::launch_slab_signal(f1.data(), N, s), "signal");
     }
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0), "event");
     CK(cudaEventCreate(&e1), "event");
     CK(cudaEventRecord(e0, s), "event");
-    if (g->n_steps > 0) CK(transpose(Wbuf, Abuf), "transpose");
+    if (!peer && g->n_steps > 0) CK(transpose(Wbuf, Abuf), "transpose");
     for (int k = 0; k < g->n_steps; ++k) {
         const int j_new = g->first_index + k + 1;
         const double r_new = g->r_start + j_new * g->delta_r;
-        for (int q = 0; q < R; ++q) CK(pe3d::launch_depth_scan(c1, Abuf + q * part, Bbuf + q * part), "depth");
-        CK(transpose(Bbuf, Rbuf), "transpose");
+        const unsigned long long target = (unsigned long long)N * (k + 1);
+        for (int q = 0; q < R; ++q) {
+            if (peer) {
+                CK(pe3d::launch_slab_wait(own(q).flags + 1, target, s), "wait");
+                const pe3d::LaunchCtx c = k1_ctx(q);
+                CK(pe3d::launch_depth_scan(c, own(q).A, own(q).R), "depth");
+                CK(pe3d::launch_slab_signal(f0.data(), N, s), "signal");
+            } else {
+                CK(pe3d::launch_depth_scan(c1, Abuf + q * part, Bbuf + q * part), "depth");
+            }
+        }
+        if (!peer) CK(transpose(Bbuf, Rbuf), "transpose");
         const bool record = ((k + 1) % g->output_stride) == 0;
         for (int q = 0; q < R; ++q) {
             pe3d::EpilogueArgs ea = ring_ea(q);
@@ -1071,21 +1125,30 @@ int pe3d_march_slab(void* handle, const pe3d_grid* g, const pe3d_coeffs* coeffs,
             ea.final_out = (k == g->n_steps - 1) ? h->h_final.as<cplx>() + q * slab_s : nullptr;
             ea.w_abs = h->w_abs.as<double>() + ea.sample;
             ea.write_temp = (k < g->n_steps - 1);
-            CK(pe3d::launch_azimuth_scan(c2, Rbuf + q * part, Wbuf + q * part, h->ring_tab.as<cplx>() + int64_t(k) * E,
-                                         r_new, ea),
-               "azimuth");
+            if (peer) {
+                if (ea.write_temp) set_peers_k2(ea, q);
+                CK(pe3d::launch_slab_wait(own(q).flags, target, s), "wait");
+                CK(pe3d::launch_azimuth_scan(c2, own(q).R, own(q).R, h->ring_tab.as<cplx>() + int64_t(k) * E, r_new,
+                                             ea),
+                   "azimuth");
+                CK(pe3d::launch_slab_signal(f1.data(), N, s), "signal");
+            } else {
+                CK(pe3d::launch_azimuth_scan(c2, Rbuf + q * part, Wbuf + q * part,
+                                             h->ring_tab.as<cplx>() + int64_t(k) * E, r_new, ea),
+                   "azimuth");
+            }
         }
-        if (k < g->n_steps - 1) CK(transpose(Wbuf, Abuf), "transpose");
+        if (!peer && k < g->n_steps - 1) CK(transpose(Wbuf, Abuf), "transpose");
     }
     CK(cudaEventRecord(e1, s), "event");
-    st = decode_error(h, s, err);
+    int st = decode_error(h, s, err);
     float ms = 0.f;
     cudaEventElapsedTime(&ms, e0, e1);
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     if (ms_steps) *ms_steps = ms;
     if (st != PE3D_OK) return st;
-    // results: virtual -> reassemble full slabs; NCCL -> this rank's slab
+    // results: virtual -> reassemble full slabs; one rank -> this rank's slab
     for (int q = 0; q < R; ++q) {
         if (u_final) {
             if (virt)
@@ -1114,6 +1177,87 @@ int pe3d_march_slab(void* handle, const pe3d_grid* g, const pe3d_coeffs* coeffs,
     }
     CK(cudaStreamSynchronize(s), "sync");
     return PE3D_OK;
+}
+
+static int slab_check(Handle* h, const pe3d_grid* g, const pe3d_coeffs* coeffs, int32_t N, pe3d_error* err) {
+    if (!h) return bad_arg(err, "null handle");
+    int st = coeffs ? check_grid(g, coeffs, err) : PE3D_OK;
+    if (st != PE3D_OK) return st;
+    if (!g) return bad_arg(err, "null grid");
+    if (g->n_freq != 1) return bad_arg(err, "slab march: n_freq == 1");
+    if (g->topology != PE3D_PERIODIC) return bad_arg(err, "slab march: periodic azimuth");
+    if (N < 1 || N > pe3d::MAX_PEERS || g->n_theta % N || g->n_depth % (8 * N))
+        return bad_arg(err, "slab march: 1 <= N <= 16, n_theta % N, n_depth % 8N");
+    return PE3D_OK;
+}
+
+int pe3d_march_slab(void* handle, const pe3d_grid* g, const pe3d_coeffs* coeffs, int32_t N, int32_t rank,
+                    const void* nccl_id, const pe3d_c128* local, const pe3d_c128* u0, pe3d_c128* u_final, double* tl,
+                    int64_t* clamped, double* ms_steps, pe3d_error* err) {
+    Handle* h = static_cast<Handle*>(handle);
+    int st = slab_check(h, g, coeffs, N, err);
+    if (st != PE3D_OK) return st;
+    if (!local || !u0) return bad_arg(err, "null local or u0");
+    const bool virt = nccl_id == nullptr;
+    if (!virt && (rank < 0 || rank >= N)) return bad_arg(err, "rank out of range");
+    CK(cudaSetDevice(h->device), "cudaSetDevice");
+    SlabMode mode = SLAB_NCCL;
+    if (virt) mode = (slab_peer_ok(g, N) && !getenv("PE3D_SLAB_COPY")) ? SLAB_VIRT_PEER : SLAB_VIRT_COPY;
+    return slab_impl(h, g, coeffs, N, rank, mode, nccl_id, nullptr, local, u0, u_final, tl, clamped, ms_steps, err);
+}
+
+int pe3d_slab_p2p_export(void* handle, const pe3d_grid* g, int32_t N, int32_t rank, void* out, pe3d_error* err) {
+    Handle* h = static_cast<Handle*>(handle);
+    int st = slab_check(h, g, nullptr, N, err);
+    if (st != PE3D_OK) return st;
+    if (rank < 0 || rank >= N || !out) return bad_arg(err, "rank out of range or null output");
+    if (!slab_peer_ok(g, N)) return bad_arg(err, "peer transposes need n_depth / (8 N) % 32 == 0 and a TMA depth sweep");
+    CK(cudaSetDevice(h->device), "cudaSetDevice");
+    const int64_t part = int64_t(g->n_depth / 8) * (g->n_theta / N) * 8;
+    CK(h->field_a.ensure(size_t(part) * sizeof(cplx)), "alloc");
+    CK(h->field_b.ensure(size_t(part) * sizeof(cplx)), "alloc");
+    CK(h->slab_flags.ensure(2 * sizeof(unsigned long long)), "alloc");
+    CK(cudaMemset(h->slab_flags.ptr, 0, 2 * sizeof(unsigned long long)), "memset");
+    cudaIpcMemHandle_t hd[3];
+    CK(cudaIpcGetMemHandle(&hd[0], h->field_a.ptr), "ipc handle");
+    CK(cudaIpcGetMemHandle(&hd[1], h->field_b.ptr), "ipc handle");
+    CK(cudaIpcGetMemHandle(&hd[2], h->slab_flags.ptr), "ipc handle");
+    std::memcpy(out, hd, sizeof(hd));
+    return PE3D_OK;
+}
+
+int pe3d_march_slab_p2p(void* handle, const pe3d_grid* g, const pe3d_coeffs* coeffs, int32_t N, int32_t rank,
+                        const void* blobs, const pe3d_c128* local, const pe3d_c128* u0, pe3d_c128* u_final,
+                        double* tl, int64_t* clamped, double* ms_steps, pe3d_error* err) {
+    Handle* h = static_cast<Handle*>(handle);
+    int st = slab_check(h, g, coeffs, N, err);
+    if (st != PE3D_OK) return st;
+    if (rank < 0 || rank >= N || !blobs) return bad_arg(err, "rank out of range or null handles");
+    if (!local || !u0) return bad_arg(err, "null local or u0");
+    if (!slab_peer_ok(g, N)) return bad_arg(err, "peer transposes need n_depth / (8 N) % 32 == 0 and a TMA depth sweep");
+    CK(cudaSetDevice(h->device), "cudaSetDevice");
+    // map every other rank's A / R / counters into this process (NVLink peer memory)
+    std::vector<SlabPeer> P(N);
+    std::vector<void*> opened;
+    struct Closer {
+        std::vector<void*>& v;
+        ~Closer() { for (void* p : v) cudaIpcCloseMemHandle(p); }
+    } closer{opened};
+    const cudaIpcMemHandle_t* hd = static_cast<const cudaIpcMemHandle_t*>(blobs);
+    for (int q = 0; q < N; ++q) {
+        if (q == rank) {
+            P[q] = {h->field_a.as<cplx>(), h->field_b.as<cplx>(), h->slab_flags.as<unsigned long long>()};
+            continue;
+        }
+        void* ptr[3];
+        for (int k = 0; k < 3; ++k) {
+            CK(cudaIpcOpenMemHandle(&ptr[k], hd[3 * q + k], cudaIpcMemLazyEnablePeerAccess), "ipc open");
+            opened.push_back(ptr[k]);
+        }
+        P[q] = {static_cast<cplx*>(ptr[0]), static_cast<cplx*>(ptr[1]), static_cast<unsigned long long*>(ptr[2])};
+    }
+    return slab_impl(h, g, coeffs, N, rank, SLAB_IPC_PEER, nullptr, P.data(), local, u0, u_final, tl, clamped,
+                     ms_steps, err);
 }
 
 int pe3d_profile_last(void* handle, double* ms, int32_t* launches) {

@@ -365,6 +365,15 @@ k_depth_scan(const cplx* __restrict__ src, cplx* __restrict__ dst, const cplx* _
     cp_async_wait<0>();
 }
 
+// Output tensor maps of the TMA depth sweeps: tiles [q*nzt, (q+1)*nzt) of
+// every column go through map m[q].  The plain march uses one map over all
+// tiles; the slab march's fused transpose uses one map per destination rank
+// (the rank's depth-sweep output chunk in its azimuth-sweep input).
+struct DepthDst {
+    CUtensorMap m[MAX_PEERS];
+    int nzt;
+};
+
 // ------------------------------------------------------------- TMA variant
 // Same math as k_depth_scan<8, *>, but each warp's 32 column tiles move
 // through the Tensor Memory Accelerator: one 4-D tiled TMA load per warp and
@@ -375,7 +384,7 @@ k_depth_scan(const cplx* __restrict__ src, cplx* __restrict__ dst, const cplx* _
 // copies at all; a 3-deep per-warp stage ring keeps two columns in flight.
 template <int STAGES, int MINB, int MAXT>
 __global__ void __launch_bounds__(MAXT, MINB)
-k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ CUtensorMap tm_dst,
+k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ DepthDst tm_dst,
             const cplx* __restrict__ loc_tab, const cplx* __restrict__ mul_tab, const FreqDev* __restrict__ fdev,
             int n_theta, int n_tiles, int64_t total_cols, int cols_per_cta, int sector) {
     constexpr int RPT = 8;
@@ -537,7 +546,10 @@ k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ 
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-            tma_store_4d(&tm_dst, 0, col, tile0, f, cur);
+            {
+                const int qd = tile0 / tm_dst.nzt;
+                tma_store_4d(&tm_dst.m[qd], 0, col, tile0 - qd * tm_dst.nzt, f, cur);
+            }
             bulk_commit();
             bulk_wait_read<1>();            // the previous column's store has left its stage slot
             if (it + STAGES - 1 < n_cols) {
@@ -571,7 +583,7 @@ k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ 
 // (read-only) input.
 template <int STAGES, int MINB>
 __global__ void __launch_bounds__(128, MINB)
-k_depth_tma_cluster(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ CUtensorMap tm_dst,
+k_depth_tma_cluster(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ DepthDst tm_dst,
                     const cplx* __restrict__ src_raw, const cplx* __restrict__ loc_tab,
                     const cplx* __restrict__ mul_tab, const FreqDev* __restrict__ fdev, int n_theta, int n_tiles,
                     int64_t total_cols, int cols_per_cluster, int sector) {
@@ -804,7 +816,10 @@ k_depth_tma_cluster(const __grid_constant__ CUtensorMap tm_src, const __grid_con
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-            tma_store_4d(&tm_dst, 0, col, tile0, f, cur);
+            {
+                const int qd = tile0 / tm_dst.nzt;
+                tma_store_4d(&tm_dst.m[qd], 0, col, tile0 - qd * tm_dst.nzt, f, cur);
+            }
             bulk_commit();
             bulk_wait_read<1>();
             if (it + STAGES - 1 < n_cols) {
@@ -853,10 +868,26 @@ static bool field_tensor_map(CUtensorMap* tm, const void* base, const LaunchCtx&
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Output maps: the plain field, or one map per peer chunk (slab march).
+static bool depth_dst_maps(DepthDst* d, const void* dst, const LaunchCtx& c) {
+    if (c.n_peers == 0) {
+        d->nzt = c.n_tiles;
+        return field_tensor_map(&d->m[0], dst, c);
+    }
+    if (c.n_freq != 1 || c.peer_tiles % 32 != 0 || c.n_peers * c.peer_tiles != c.n_tiles) return false;
+    LaunchCtx cp = c;
+    cp.n_tiles = c.peer_tiles;
+    for (int q = 0; q < c.n_peers; ++q)
+        if (!field_tensor_map(&d->m[q], c.peer_dst[q], cp)) return false;
+    d->nzt = c.peer_tiles;
+    return true;
+}
+
 template <int STAGES, int MINB, int MAXT>
 static cudaError_t launch_depth_tma_cfg(const LaunchCtx& c, const cplx* src, cplx* dst) {
-    CUtensorMap tm_src, tm_dst;
-    if (!field_tensor_map(&tm_src, src, c) || !field_tensor_map(&tm_dst, dst, c)) return cudaErrorNotSupported;
+    CUtensorMap tm_src;
+    DepthDst tm_dst;
+    if (!field_tensor_map(&tm_src, src, c) || !depth_dst_maps(&tm_dst, dst, c)) return cudaErrorNotSupported;
     const int nthreads = (c.n_tiles + 31) / 32 * 32;
     const int nwarps = nthreads / 32;
     const size_t bytes = 1024 + sizeof(cplx) * (size_t(nwarps) * STAGES * 256 + 10 * size_t(nthreads) + 5 * nwarps) +
@@ -878,8 +909,9 @@ static cudaError_t launch_depth_tma_cfg(const LaunchCtx& c, const cplx* src, cpl
 }
 
 static cudaError_t launch_depth_tma_cluster(const LaunchCtx& c, const cplx* src, cplx* dst, int CL) {
-    CUtensorMap tm_src, tm_dst;
-    if (!field_tensor_map(&tm_src, src, c) || !field_tensor_map(&tm_dst, dst, c)) return cudaErrorNotSupported;
+    CUtensorMap tm_src;
+    DepthDst tm_dst;
+    if (!field_tensor_map(&tm_src, src, c) || !depth_dst_maps(&tm_dst, dst, c)) return cudaErrorNotSupported;
     constexpr int STAGES = 3, MINB = 3;
     const int nthreads = c.n_tiles / CL;
     const int nwarps = nthreads / 32;
@@ -943,9 +975,10 @@ cudaError_t launch_depth_scan(const LaunchCtx& c, const cplx* src, cplx* dst) {
                                                per, c.sector);
         return cudaGetLastError();
     };
-    if (c.n_tiles <= 512 && !getenv("PE3D_DEPTH_NO_TMA") && !(c.n_tiles > 128 && getenv("PE3D_DEPTH_WIDE_SCAN"))) {
+    if (c.n_peers > 0 || (c.n_tiles <= 512 && !getenv("PE3D_DEPTH_NO_TMA") &&
+                          !(c.n_tiles > 128 && getenv("PE3D_DEPTH_WIDE_SCAN")))) {
         cudaError_t e = launch_depth_tma(c, src, dst);
-        if (e != cudaErrorNotSupported) return e;
+        if (e != cudaErrorNotSupported || c.n_peers > 0) return e;    // peer output needs the TMA kernels
     }
     const int nt = round32(c.n_tiles);
     if (nt <= 128) return go(k_depth_scan<8, 128>, nt, depth_smem_elems<8, 128>(nt), DepthCfg<8, 128>::MINB);

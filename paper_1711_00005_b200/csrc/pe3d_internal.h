@@ -17,6 +17,9 @@ struct StridedC {
 
 // What the ring epilogue writes besides nothing: TL sample, snapshot,
 // final slab (reference layout), and the next step's temp (device tiles).
+// Peer-direct transposes of the slab march: at most this many ranks.
+constexpr int MAX_PEERS = 16;
+
 struct EpilogueArgs {
     double* tl;             // [F][n_samples][n_theta][n_depth] or null
     cplx* snap;             // [F][n_samples][n_theta][n_depth] or null
@@ -34,7 +37,19 @@ struct EpilogueArgs {
     int row_offset;
     int chunk_cols;
     int64_t chunk_gap;
+    // Peer-direct output (fused K2 -> K1 transpose): when peer[0] is set, the
+    // next temp of azimuth m, local tile t, row r goes to
+    // peer[m / chunk_cols] + (t * chunk_cols + m % chunk_cols) * 8 + r, i.e.
+    // straight into the depth-sweep input of the rank owning azimuth chunk
+    // m / chunk_cols (this rank's chunk of it).
+    cplx* peer[MAX_PEERS];
 };
+
+// Destination of the next temp of ring element (m, row r) of local tile t.
+__host__ __device__ __forceinline__ cplx* peer_elem(const EpilogueArgs& ea, int m, int tile, int r) {
+    const int p = m / ea.chunk_cols;
+    return ea.peer[p] + (int64_t(tile) * ea.chunk_cols + (m - p * ea.chunk_cols)) * 8 + r;
+}
 
 __host__ __device__ __forceinline__ int64_t ring_base(int f, int tile, int n_tiles, int n_theta, int chunk_cols) {
     return (int64_t(f) * n_tiles * n_theta + int64_t(tile) * chunk_cols) * 8;
@@ -70,8 +85,16 @@ struct LaunchCtx {
     cplx* mul_tab;          // [F][n_tiles*8]
     DevError* err;
     cudaStream_t stream;
+    // Peer-direct output of the depth sweep (fused K1 -> K2 transpose): when
+    // n_peers > 0, tiles [q*peer_tiles, (q+1)*peer_tiles) of every column go to
+    // peer_dst[q], laid out [tile][column][8] (n_theta columns).
+    int n_peers;
+    int peer_tiles;
+    cplx* peer_dst[MAX_PEERS];
 };
 
+cudaError_t launch_slab_signal(unsigned long long* const* flags, int n, cudaStream_t s);
+cudaError_t launch_slab_wait(const unsigned long long* flag, unsigned long long target, cudaStream_t s);
 void ring_shape(int n_theta, int* L, int* RW);
 int ring_table_elems(int n_theta);   // complex entries per (step, frequency) ring table
 cudaError_t launch_factor_depth(const LaunchCtx& c, const cplx* local, int64_t local_fstride, int step_for_error);

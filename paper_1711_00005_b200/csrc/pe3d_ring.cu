@@ -178,8 +178,9 @@ __device__ __forceinline__ void ring_epilogue(cplx (&u)[RT][L], int q, int n_chu
             if (k >= nvalid) break;
             const cplx um = k ? u[h][k - 1] : prev;
             const cplx up = (k + 1 < L && k < nvalid - 1) ? u[h][(k + 1) % L] : next;
-            stc_stream(dst_row + ring_off(m0 + k, ea.chunk_cols, ea.chunk_gap),
-                       cfma(b1, u[h][k], cmul(b2, cadd(up, um))));
+            const cplx tv = cfma(b1, u[h][k], cmul(b2, cadd(up, um)));
+            if (ea.peer[0]) stc_stream(peer_elem(ea, m0 + k, l0 >> 3, row0 + r), tv);   // fused transpose
+            else stc_stream(dst_row + ring_off(m0 + k, ea.chunk_cols, ea.chunk_gap), tv);
         }
     }
 }
@@ -443,7 +444,7 @@ __device__ __forceinline__ int ring_slot(int m, int r) { return m * 8 + (r ^ ((m
 
 // CHUNKED: rank-chunked ring layout of the slab march (ea.chunk_cols /
 // chunk_gap); the standard march compiles the plain contiguous addressing.
-template <int L, int RT, int STAGES, bool CHUNKED>
+template <int L, int RT, int STAGES, bool CHUNKED, bool PEER = false>
 __global__ void __launch_bounds__(32 * 8 / RT)
 k_azimuth_warp(const cplx* __restrict__ src, cplx* __restrict__ dst, const cplx* __restrict__ table, int E,
                const FreqDev* __restrict__ fdev, int n_tiles, int n_depth, int64_t total_items, int items_per_cta,
@@ -613,7 +614,8 @@ k_azimuth_warp(const cplx* __restrict__ src, cplx* __restrict__ dst, const cplx*
 #pragma unroll
             for (int j = 0; j < PER; ++j) {
                 const int e = j * NTHR + tid;
-                stc_stream(g + e + (CHUNKED ? int64_t((e >> 3) / C) * gap : 0), stg[ring_slot<L>(e >> 3, e & 7)]);
+                if (PEER) stc_stream(peer_elem(ea, e >> 3, tile, e & 7), stg[ring_slot<L>(e >> 3, e & 7)]);
+                else stc_stream(g + e + (CHUNKED ? int64_t((e >> 3) / C) * gap : 0), stg[ring_slot<L>(e >> 3, e & 7)]);
             }
         }
         if (++tile == n_tiles) { tile = 0; ++f; }
@@ -919,7 +921,13 @@ k_azimuth_cluster(const cplx* __restrict__ src, cplx* __restrict__ dst, const cp
         }
         if (ea.write_temp) {
             __syncthreads();                        // every warp's rows written
-            if (gap == 0) {
+            if (ea.peer[0]) {                       // fused transpose: straight into the owners' inputs
+#pragma unroll
+                for (int jj = 0; jj < PER; ++jj) {
+                    const int e = jj * NTHR + tid;
+                    stc_stream(peer_elem(ea, mseg + (e >> 3), tile, e & 7), stg[ring_slot<L>(e >> 3, e & 7)]);
+                }
+            } else if (gap == 0) {
                 cplx* g = dst + item_base(item) + s * ITEM + tid;
 #pragma unroll
                 for (int j = 0; j < PER; ++j) {
@@ -1172,7 +1180,8 @@ template <int L, int RT, int STAGES>
 static cudaError_t launch_warp_ring(const LaunchCtx& c, const cplx* src, cplx* dst, const cplx* table_step, int E,
                                    double r_new, const EpilogueArgs& ea) {
     const bool chunked = ea.chunk_gap != 0 || (ea.chunk_cols != 0 && ea.chunk_cols != c.n_theta);
-    auto kern = chunked ? k_azimuth_warp<L, RT, STAGES, true> : k_azimuth_warp<L, RT, STAGES, false>;
+    auto kern = ea.peer[0] ? k_azimuth_warp<L, RT, STAGES, true, true>
+                           : (chunked ? k_azimuth_warp<L, RT, STAGES, true> : k_azimuth_warp<L, RT, STAGES, false>);
     const int nthr = 32 * 8 / RT;
     const size_t bytes = sizeof(cplx) * (size_t(STAGES) * 32 * L * 8 + E);
     cudaError_t e = set_smem(kern, bytes);
@@ -1259,7 +1268,7 @@ cudaError_t launch_azimuth_scan(const LaunchCtx& c, const cplx* src, cplx* dst, 
     const RingLayout rl = plan.lay;
     const int nthreads = round32(RW * rl.n_chunks);
     const size_t stage_bytes = sizeof(cplx) * size_t(RW) * c.n_theta;
-    if (RW == 8 && 2 * stage_bytes <= 110 * 1024 && ea.chunk_gap == 0) {
+    if (RW == 8 && 2 * stage_bytes <= 110 * 1024 && ea.chunk_gap == 0 && !ea.peer[0]) {
         const int stages = (3 * stage_bytes <= 72 * 1024) ? 3 : 2;
         const int64_t items = int64_t(c.n_freq) * c.n_tiles;
         constexpr int RT = 2;
@@ -1310,7 +1319,7 @@ cudaError_t launch_azimuth_scan(const LaunchCtx& c, const cplx* src, cplx* dst, 
 
 cudaError_t launch_finish(const LaunchCtx& c, const cplx* src, int src_tiled, cplx* dst, double r,
                           const EpilogueArgs& ea) {
-    const bool standard = ea.chunk_gap == 0 && (ea.chunk_cols == 0 || ea.chunk_cols == c.n_theta);
+    const bool standard = ea.chunk_gap == 0 && (ea.chunk_cols == 0 || ea.chunk_cols == c.n_theta) && !ea.peer[0];
     if (!src_tiled && standard && c.n_theta % PREP_MB == 0 && !getenv("PE3D_PREPARE_RINGS")) {
         dim3 grid(c.n_theta / PREP_MB, (c.n_tiles * 8 + PREP_DB - 1) / PREP_DB, c.n_freq);
         k_prepare<<<grid, 256, 0, c.stream>>>(src, dst, c.fdev, c.n_theta, c.n_tiles, c.n_depth, r, c.delta_theta, ea);

@@ -61,7 +61,14 @@ def depth_slab(values: np.ndarray, nranks: int, rank: int) -> np.ndarray:
     return np.ascontiguousarray(values[..., rank * nz_s:(rank + 1) * nz_s])
 
 
-def _run(config, frequency, nranks, rank, nccl_id, n_steps, device):
+def peer_transport_ok(grid, nranks: int) -> bool:
+    """Shapes the peer-direct transposes support (pe3d_slab_p2p_export)."""
+    nzt = grid.n_depth // 8
+    nzt_s = nzt // nranks
+    return nranks <= 16 and nzt_s % 32 == 0 and (nzt <= 512 or (nzt % 128 == 0 and nzt // 128 <= 8))
+
+
+def _run(config, frequency, nranks, rank, nccl_id, n_steps, device, peer_blobs=None):
     grid, env, source, options = config
     check_slab_shape(grid, nranks)
     if not is_range_independent(env):
@@ -73,7 +80,7 @@ def _run(config, frequency, nranks, rank, nccl_id, n_steps, device):
     S = 1 + steps // stride
     local = _local_column(env, grid, grid.r_start, k0)
     u0 = gaussian_starter(grid, source, k0).values
-    virt = nccl_id is None
+    virt = nccl_id is None and peer_blobs is None
     if not virt:
         u0 = depth_slab(u0, nranks, rank)
     u0 = np.ascontiguousarray(u0)
@@ -82,10 +89,16 @@ def _run(config, frequency, nranks, rank, nccl_id, n_steps, device):
     clamped = np.zeros(1, dtype=np.int64)
     ms = C.c_double(0.0)
     g = _grid_params(grid, 1, steps, stride, 0, grid.r_start)
-    id_buf = None if virt else (C.c_char * NCCL_ID_BYTES).from_buffer_copy(nccl_id)
-    _native.call("pe3d_march_slab", _native.handle(device), g, coeffs, nranks, 0 if virt else rank,
-                 id_buf, _native.ptr(local), _native.ptr(u0), _native.ptr(final), _native.ptr(tl),
-                 _native.ptr(clamped), C.byref(ms))
+    if peer_blobs is not None:
+        blobs = (C.c_char * len(peer_blobs)).from_buffer_copy(peer_blobs)
+        _native.call("pe3d_march_slab_p2p", _native.handle(device), g, coeffs, nranks, rank, blobs,
+                     _native.ptr(local), _native.ptr(u0), _native.ptr(final), _native.ptr(tl),
+                     _native.ptr(clamped), C.byref(ms))
+    else:
+        id_buf = None if virt else (C.c_char * NCCL_ID_BYTES).from_buffer_copy(nccl_id)
+        _native.call("pe3d_march_slab", _native.handle(device), g, coeffs, nranks, 0 if virt else rank,
+                     id_buf, _native.ptr(local), _native.ptr(u0), _native.ptr(final), _native.ptr(tl),
+                     _native.ptr(clamped), C.byref(ms))
     ranges = np.asarray([grid.r_start] + [grid.range_at(s * stride) for s in range(1, S)])
     return SlabResult(frequency, ranges, tl, int(clamped[0]), final, ms.value, nranks, None if virt else rank)
 
@@ -104,11 +117,42 @@ def new_nccl_id() -> bytes:
     return bytes(buf)
 
 
+def export_peer_buffers(grid, nranks: int, rank: int, steps: int, stride: int, device: int) -> bytes:
+    """Allocate this rank's slab buffers, reset its ordering counters and
+    return their CUDA IPC handles (pe3d_slab_p2p_export)."""
+    out = (C.c_char * _native.SLAB_IPC_BYTES)()
+    g = _grid_params(grid, 1, steps, stride, 0, grid.r_start)
+    _native.call("pe3d_slab_p2p_export", _native.handle(device), g, nranks, rank, out)
+    return bytes(out)
+
+
 def distributed_slab_march(config, frequency: float, group=None, device: Optional[int] = None,
-                           n_steps: Optional[int] = None) -> SlabResult:
-    """One process per GPU: this rank's slab of the decomposed march."""
+                           n_steps: Optional[int] = None, transport: str = "auto") -> SlabResult:
+    """One process per GPU: this rank's slab of the decomposed march.
+
+    transport "peer" (the default when the shape allows it): the sweeps store
+    their output straight into the other ranks' inputs over NVLink (CUDA IPC
+    mappings exchanged here), ordered by device-side counters; "nccl": an
+    equal-split all-to-all of NCCL send/recv pairs after each sweep."""
     import torch.distributed as dist
     rank, world = dist.get_rank(group), dist.get_world_size(group)
+    dev = rank if device is None else device
+    grid = config.grid
+    if transport == "auto":
+        transport = "peer" if peer_transport_ok(grid, world) else "nccl"
+    if transport == "peer":
+        steps = steps_within(grid, config.options.max_range) if n_steps is None else n_steps
+        stride = config.options.output_stride or default_output_stride(grid.n_range)
+        blob = export_peer_buffers(grid, world, rank, steps, stride, dev)
+        blobs = [None] * world
+        dist.all_gather_object(blobs, blob, group=group)
+        dist.barrier(group=group)                   # every rank's counters reset before anyone marches
+        try:
+            return _run(config, frequency, world, rank, None, n_steps, dev, peer_blobs=b"".join(blobs))
+        finally:
+            dist.barrier(group=group)               # no late signal may land in a re-armed counter
+    if transport != "nccl":
+        raise InvariantError("transport in (auto, peer, nccl)", f"got {transport!r}")
     obj = [new_nccl_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0, group=group)
-    return _run(config, frequency, world, rank, obj[0], n_steps, rank if device is None else device)
+    return _run(config, frequency, world, rank, obj[0], n_steps, dev)

@@ -67,41 +67,57 @@ def test_gloo_two_ranks_static_blocks(fail_freq):
     assert failures == ([] if fail_freq is None else [(freqs.index(fail_freq), fail_freq)])
 
 
-def _slab_worker(rank, world, port, queue):
-    import numpy as np
+def _slab_worker(rank, world, port, queue, transport):
+    import ctypes as C
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_1711_00005_b200 import configs, slab
     seen = {}
 
-    def fake_call(name, handle, g, coeffs, nranks, rnk, id_buf, local, u0, final, tl, clamped, ms):
-        seen.update(name=name, nranks=nranks, rank=rnk, id=bytes(id_buf), n_depth=g.n_depth)
+    def fake_call(name, handle, g, *args):
+        if name == "pe3d_slab_p2p_export":          # (nranks, rank, out): a blob naming the rank
+            nranks, rnk, out = args
+            C.memmove(out, bytes([rnk + 1]) * slab._native.SLAB_IPC_BYTES, slab._native.SLAB_IPC_BYTES)
+            seen["exported"] = (nranks, rnk)
+            return
+        coeffs, nranks, rnk, blob = args[:4]
+        seen.update(name=name, nranks=nranks, rank=rnk, blob=bytes(blob), n_depth=g.n_depth)
 
     slab.new_nccl_id = lambda: bytes(range(128))
     slab._native.call = fake_call
     slab._native.handle = lambda device=0: None
     cfg = configs.build("cfg5", n_range=3)
-    res = slab.distributed_slab_march(cfg, 500.0, device=0, n_steps=2)
+    res = slab.distributed_slab_march(cfg, 500.0, device=0, n_steps=2, transport=transport)
     queue.put((rank, seen, res.final.shape, res.tl_field.shape))
     dist.destroy_process_group()
 
 
-def test_gloo_slab_march_id_broadcast_and_slabs():
+@pytest.mark.parametrize("transport", ["nccl", "peer"])
+def test_gloo_slab_march_handshake_and_slabs(transport):
+    """Host protocol of the distributed slab march on 2 gloo ranks: NCCL
+    transport -- rank 0's unique id reaches every rank; peer transport --
+    every rank exports its IPC blob and marches with all blobs in rank order."""
     ctx = mp.get_context("spawn")
     queue = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_slab_worker, args=(r, 2, port, queue)) for r in range(2)]
+    procs = [ctx.Process(target=_slab_worker, args=(r, 2, port, queue, transport)) for r in range(2)]
     for p in procs:
         p.start()
     out = dict((lambda t: (t[0], t[1:]))(queue.get(timeout=180)) for _ in range(2))
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
+    nb = 192
     for rank in (0, 1):
         seen, final_shape, tl_shape = out[rank]
-        assert seen["name"] == "pe3d_march_slab" and seen["nranks"] == 2 and seen["rank"] == rank
-        assert seen["id"] == bytes(range(128))            # rank 0's NCCL id reached every rank
+        assert seen["nranks"] == 2 and seen["rank"] == rank
+        if transport == "nccl":
+            assert seen["name"] == "pe3d_march_slab"
+            assert seen["blob"] == bytes(range(128))        # rank 0's NCCL id reached every rank
+        else:
+            assert seen["name"] == "pe3d_march_slab_p2p" and seen["exported"] == (2, rank)
+            assert seen["blob"][:2 * nb] == bytes([1]) * nb + bytes([2]) * nb   # all blobs, rank order
         assert final_shape == (4096, 2048)                 # this rank's depth slab
         assert tl_shape == (1, 4096, 2048)                 # stride 100: starter sample only
 

@@ -538,6 +538,50 @@ def test_slab_march_real_nccl_one_rank():
     assert got.tl_field.tobytes() == ref.tl_field.tobytes()
 
 
+@pytest.mark.parametrize("nranks", [2, 4])
+def test_slab_march_peer_vs_copy_transport(monkeypatch, nranks):
+    """Virtual ranks: the peer-direct (fused) transposes -- sweeps storing
+    straight into the other ranks' inputs, counters ordering the sweeps --
+    against the device-copy all-to-all, and both bitwise the plain march."""
+    from paper_1711_00005_b200 import slab_march
+    cfg = configs.build("cfg5", n_range=5, output_stride=2)
+    grid = cfg.grid
+    small = Config(Grid3D(5, 512, 2048, grid.delta_r, 2 * math.pi / 512, grid.delta_z, grid.r_start),
+                   cfg.environment, SourceSpec((500.0,), 300.0), RunOptions(output_stride=2))
+    ref = march_frequencies(small, [500.0])[0]
+    monkeypatch.delenv("PE3D_SLAB_COPY", raising=False)
+    peer = slab_march(small, 500.0, nranks)
+    monkeypatch.setenv("PE3D_SLAB_COPY", "1")
+    copy = slab_march(small, 500.0, nranks)
+    for got in (peer, copy):
+        assert got.final.tobytes() == ref.final_slab.values.tobytes()
+        assert got.tl_field.tobytes() == ref.tl_field.tobytes()
+
+
+def test_slab_march_ipc_peer_one_rank():
+    """The IPC entry points of the peer transport (export, all-gather of the
+    handles, barrier, pe3d_march_slab_p2p) with one rank: bitwise the plain
+    march."""
+    import socket
+    import torch.distributed as dist
+    from paper_1711_00005_b200 import slab
+    cfg = configs.build("cfg5", n_range=4, output_stride=2)
+    grid = cfg.grid
+    small = Config(Grid3D(4, 256, 2048, grid.delta_r, 2 * math.pi / 256, grid.delta_z, grid.r_start),
+                   cfg.environment, SourceSpec((500.0,), 300.0), RunOptions(output_stride=2))
+    ref = march_frequencies(small, [500.0])[0]
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        got = slab.distributed_slab_march(small, 500.0, device=0, transport="peer")
+    finally:
+        dist.destroy_process_group()
+    assert got.final.tobytes() == ref.final_slab.values.tobytes()
+    assert got.tl_field.tobytes() == ref.tl_field.tobytes()
+
+
 def test_slab_march_cfg5_full_size_vs_reference(golden):
     from paper_1711_00005_b200 import slab_march
     fx = golden("cfg5_f500_3steps.npz")
