@@ -210,15 +210,17 @@ struct MarchPlan {
 };
 
 // Number of concurrent step-loop chains.  Frequencies are independent, so a
-// march runs two disjoint frequency groups as parallel graph branches: each
-// chain's launch ramp, pipeline fill and tail are filled by the other chain's
+// march runs disjoint frequency groups as parallel graph branches: each
+// chain's launch ramp, pipeline fill and tail are filled by the other chains'
 // CTAs.  Measured on cfg4 (per-GPU step, 1 -> 2 chains): 64 frequencies
-// 216 -> 208 us, 32: 119 -> 105, 16: 66 -> 57, 8: 39 -> 34.5; four chains
-// are worse.  PE3D_CHAINS overrides.
+// 216 -> 208 us, 32: 119 -> 105, 16: 66 -> 57, 8: 39 -> 34.5.  Three chains
+// pay off only with few columns per resident CTA (8 frequencies: 33.2 ->
+// 31.9 us; 16: 56.9 -> 61.5).  PE3D_CHAINS overrides.
 int step_chains(const pe3d::LaunchCtx& c, bool profiling) {
     if (profiling || c.n_freq < 2) return 1;
     const char* env = getenv("PE3D_CHAINS");
-    int n = env ? atoi(env) : 2;
+    const int64_t cols = int64_t(c.n_freq) * c.n_theta;
+    int n = env ? atoi(env) : (cols <= int64_t(6) * 3 * c.num_sms ? 3 : 2);
     if (n > Handle::MAX_CHAINS) n = Handle::MAX_CHAINS;
     if (n > c.n_freq) n = c.n_freq;
     return n < 1 ? 1 : n;
