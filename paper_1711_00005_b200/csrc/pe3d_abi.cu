@@ -72,6 +72,10 @@ struct Handle {
     static constexpr int MAX_CHAINS = 4;
     cudaStream_t chain_stream[MAX_CHAINS] = {};
     cudaEvent_t chain_fork = nullptr, chain_join[MAX_CHAINS] = {};
+    // TL streaming to the host (pe3d_march_host): one copy stream per chain
+    // plus one for the starting sample, and their events
+    cudaStream_t tl_side[MAX_CHAINS + 1] = {};
+    std::vector<cudaEvent_t> tl_ev;
 };
 
 // Launch wrapper: in profile mode, bracket each launch with events.
@@ -226,11 +230,78 @@ int step_chains(const pe3d::LaunchCtx& c, bool profiling) {
     return n < 1 ? 1 : n;
 }
 
+// TL streaming (pe3d_march_host): the device keeps a ring of R samples per
+// frequency; after the kernel that writes sample k of a chain's frequencies,
+// the chain's copy stream moves it to the page-locked host stack, and the
+// kernel that writes sample k + R into the same slot waits for that copy.
+// The copies are graph nodes next to the sweeps, so they overlap the march.
+struct TlSink {
+    double* host;       // [F][S][n_theta][n_depth], page-locked
+    int S;              // samples of the host stack
+    int R;              // device ring slots per frequency
+};
+
+// events: per copy stream c (0..MAX_CHAINS): R "copied" slots + 1 "written"
+static cudaEvent_t& tl_event(Handle* h, int c, int slot, const TlSink& sk) {
+    return h->tl_ev[size_t(c) * (sk.R + 1) + slot];
+}
+
+static cudaError_t tl_prepare(Handle* h, const TlSink& sk) {
+    const size_t need = size_t(Handle::MAX_CHAINS + 1) * (sk.R + 1);
+    while (h->tl_ev.size() < need) {
+        cudaEvent_t e;
+        cudaError_t r = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+        if (r != cudaSuccess) return r;
+        h->tl_ev.push_back(e);
+    }
+    for (int c = 0; c <= Handle::MAX_CHAINS; ++c)
+        if (!h->tl_side[c]) {
+            cudaError_t r = cudaStreamCreateWithFlags(&h->tl_side[c], cudaStreamNonBlocking);
+            if (r != cudaSuccess) return r;
+        }
+    return cudaSuccess;
+}
+
+// before the kernel writing sample k (k >= 1) of copy stream c: the slot's
+// previous sample (k - R) must have left for the host
+static cudaError_t tl_before(Handle* h, const TlSink& sk, int c, int k, cudaStream_t st) {
+    const int prev = k - sk.R;
+    if (prev < 0) return cudaSuccess;
+    const int cs = prev == 0 ? Handle::MAX_CHAINS : c;      // sample 0 is copied by the starter stream
+    return cudaStreamWaitEvent(st, tl_event(h, cs, prev % sk.R, sk), 0);
+}
+
+// after the kernel writing sample k of frequencies [f0, f0 + nf) on st
+static cudaError_t tl_after(Handle* h, const TlSink& sk, int c, int k, int f0, int nf, int64_t oe,
+                            const double* ring, cudaStream_t st) {
+    cudaStream_t side = h->tl_side[c];
+    cudaError_t e = cudaEventRecord(tl_event(h, c, sk.R, sk), st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(side, tl_event(h, c, sk.R, sk), 0);
+    const size_t w = size_t(oe) * sizeof(double);
+    if (e == cudaSuccess)
+        e = cudaMemcpy2DAsync(sk.host + (int64_t(f0) * sk.S + k) * oe, sk.S * w, ring + (int64_t(f0) * sk.R + k % sk.R) * oe,
+                              sk.R * w, w, nf, cudaMemcpyDeviceToHost, side);
+    if (e == cudaSuccess) e = cudaEventRecord(tl_event(h, c, k % sk.R, sk), side);
+    return e;
+}
+
+// join every copy stream back into st (end of the step loop)
+static cudaError_t tl_join(Handle* h, const TlSink& sk, int n_copy_streams, cudaStream_t st) {
+    cudaError_t first = cudaSuccess;
+    for (int c = 0; c <= Handle::MAX_CHAINS; ++c) {
+        if (c >= n_copy_streams && c != Handle::MAX_CHAINS) continue;
+        cudaError_t e = cudaEventRecord(tl_event(h, c, sk.R, sk), h->tl_side[c]);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(st, tl_event(h, c, sk.R, sk), 0);
+        if (e != cudaSuccess && first == cudaSuccess) first = e;
+    }
+    return first;
+}
+
 // Step loop of the parallel (scan) path for frequencies [f0, f0 + nf) on
 // stream `st`; all pointers are offset to the group.
 cudaError_t enqueue_group(Handle* h, const pe3d_grid* g, const MarchPlan& p, int f0, int nf, cudaStream_t st,
                           double* d_tl, cplx* d_snap, cplx* d_final, int64_t* d_clamped, const double* d_wabs,
-                          Prof& prof) {
+                          Prof& prof, const TlSink* sink, int chain) {
     const pe3d::LaunchCtx& c = p.ctx;
     const int E = pe3d::ring_table_elems(c.n_theta);
     const int64_t fe = int64_t(c.n_tiles) * c.n_theta * 8;     // field elements per frequency
@@ -257,35 +328,78 @@ cudaError_t enqueue_group(Handle* h, const pe3d_grid* g, const MarchPlan& p, int
         if (e != cudaSuccess) return e;
         pe3d::EpilogueArgs ea{};
         const bool record = ((s + 1) % g->output_stride) == 0;
+        const int k = (s + 1) / g->output_stride;          // sample index
+        const bool stream_tl = record && d_tl && sink;
+        const int tl_slots = sink ? sink->R : p.n_samples;
+        if (stream_tl) {
+            e = tl_before(h, *sink, chain, k, st);
+            if (e != cudaSuccess) return e;
+        }
         ea.n_samples = p.n_samples;
-        ea.tl = record && d_tl ? d_tl + int64_t(f0) * p.n_samples * oe : nullptr;
+        ea.tl = record && d_tl ? d_tl + int64_t(f0) * tl_slots * oe : nullptr;
         ea.snap = record && d_snap ? d_snap + int64_t(f0) * p.n_samples * oe : nullptr;
         ea.final_out = (s == g->n_steps - 1) && d_final ? d_final + f0 * oe : nullptr;
         ea.clamped = d_clamped ? d_clamped + f0 : nullptr;
-        ea.sample = (s + 1) / g->output_stride;
-        ea.w_abs = d_wabs + int64_t(ea.sample) * g->n_freq + f0;
+        ea.sample = k;
+        ea.w_abs = d_wabs + int64_t(k) * g->n_freq + f0;
         ea.periodic = true;
         ea.write_temp = (s < g->n_steps - 1);
+        if (sink && !d_snap) {                              // TL in the device ring
+            ea.n_samples = sink->R;
+            ea.sample = k % sink->R;
+        }
         const cplx* tab = h->ring_tab.as<cplx>() + (int64_t(s) * c.n_freq + f0) * E;
         e = prof.run(1, [&] { return pe3d::launch_azimuth_scan(cg, B, A, tab, r_new, ea); });
         if (e != cudaSuccess) return e;
+        if (stream_tl) {
+            e = tl_after(h, *sink, chain, k, f0, nf, oe, d_tl, st);
+            if (e != cudaSuccess) return e;
+        }
     }
     return cudaSuccess;
 }
 
-// Enqueue the step loop (the body graphed by pe3d_march_device).
+cudaError_t enqueue_steps_body(Handle* h, const pe3d_grid* g, const MarchPlan& p, const cplx* d_local,
+                               double* d_tl, cplx* d_snap, cplx* d_final, int64_t* d_clamped,
+                               const double* d_wabs, Prof& prof, const TlSink* sink, int* n_copy_streams);
+
+// Enqueue the step loop (the body graphed by pe3d_march_device).  With a TL
+// sink the starting sample (written by the prologue) leaves first, and every
+// copy stream is joined back at the end.
 cudaError_t enqueue_steps(Handle* h, const pe3d_grid* g, const MarchPlan& p, const cplx* d_local,
                           double* d_tl, cplx* d_snap, cplx* d_final, int64_t* d_clamped,
-                          const double* d_wabs, Prof& prof) {
+                          const double* d_wabs, Prof& prof, const TlSink* sink) {
+    const pe3d::LaunchCtx& c = p.ctx;
+    if (sink && d_tl) {
+        const int64_t oe = int64_t(c.n_theta) * g->n_depth;
+        cudaError_t e = tl_after(h, *sink, Handle::MAX_CHAINS, 0, 0, c.n_freq, oe, d_tl, c.stream);
+        if (e != cudaSuccess) return e;
+    }
+    int n_copy = 0;
+    cudaError_t e = enqueue_steps_body(h, g, p, d_local, d_tl, d_snap, d_final, d_clamped, d_wabs, prof,
+                                       sink && d_tl ? sink : nullptr, &n_copy);
+    if (sink && d_tl) {
+        cudaError_t e2 = tl_join(h, *sink, n_copy, c.stream);
+        if (e == cudaSuccess) e = e2;
+    }
+    return e;
+}
+
+cudaError_t enqueue_steps_body(Handle* h, const pe3d_grid* g, const MarchPlan& p, const cplx* d_local,
+                               double* d_tl, cplx* d_snap, cplx* d_final, int64_t* d_clamped,
+                               const double* d_wabs, Prof& prof, const TlSink* sink, int* n_copy_streams) {
     const pe3d::LaunchCtx& c = p.ctx;
     cplx* A = h->field_a.as<cplx>();
     cplx* B = h->field_b.as<cplx>();
     cplx* C = h->field_c.as<cplx>();
     const bool periodic = g->topology == PE3D_PERIODIC;
+    *n_copy_streams = 1;
     if (periodic && !p.serial) {
         const int chains = step_chains(c, prof.on);
+        *n_copy_streams = chains;
         if (chains == 1)
-            return enqueue_group(h, g, p, 0, c.n_freq, c.stream, d_tl, d_snap, d_final, d_clamped, d_wabs, prof);
+            return enqueue_group(h, g, p, 0, c.n_freq, c.stream, d_tl, d_snap, d_final, d_clamped, d_wabs, prof, sink,
+                                 0);
         cudaError_t e = cudaSuccess;
         if (!h->chain_fork) e = cudaEventCreateWithFlags(&h->chain_fork, cudaEventDisableTiming);
         for (int k = 0; k < chains && e == cudaSuccess; ++k) {
@@ -305,7 +419,7 @@ cudaError_t enqueue_steps(Handle* h, const pe3d_grid* g, const MarchPlan& p, con
             if (e != cudaSuccess) { if (first == cudaSuccess) first = e; break; }
             if (first == cudaSuccess) {
                 e = enqueue_group(h, g, p, f0, f1 - f0, h->chain_stream[k], d_tl, d_snap, d_final, d_clamped, d_wabs,
-                                  prof);
+                                  prof, sink, k);
                 if (e != cudaSuccess) first = e;
             }
             cudaError_t e2 = cudaEventRecord(h->chain_join[k], h->chain_stream[k]);
@@ -331,20 +445,34 @@ cudaError_t enqueue_steps(Handle* h, const pe3d_grid* g, const MarchPlan& p, con
         if (e != cudaSuccess) return e;
         pe3d::EpilogueArgs ea{};
         const bool record = ((s + 1) % g->output_stride) == 0;
+        const int k = (s + 1) / g->output_stride;
+        const bool stream_tl = record && d_tl && sink;
+        if (stream_tl) {
+            e = tl_before(h, *sink, 0, k, c.stream);
+            if (e != cudaSuccess) return e;
+        }
         ea.tl = record ? d_tl : nullptr;
         ea.snap = record ? d_snap : nullptr;
         ea.final_out = (s == g->n_steps - 1) ? d_final : nullptr;
         ea.clamped = d_clamped;
         ea.n_samples = p.n_samples;
-        ea.sample = (s + 1) / g->output_stride;
-        ea.w_abs = d_wabs + int64_t(ea.sample) * g->n_freq;
+        ea.sample = k;
+        ea.w_abs = d_wabs + int64_t(k) * g->n_freq;
         ea.periodic = periodic;
         ea.write_temp = (s < g->n_steps - 1);
+        if (sink && !d_snap) {
+            ea.n_samples = sink->R;
+            ea.sample = k % sink->R;
+        }
         e = prof.run(1, [&] { return pe3d::launch_azimuth_serial(c, B, C, h->az_cp.as<cplx>(), h->az_inv.as<cplx>(),
                                                                  h->az_q.as<cplx>(), h->az_ring.as<cplx>(), r_new,
                                                                  j_new); });
         if (e == cudaSuccess) e = prof.run(2, [&] { return pe3d::launch_finish(c, C, 1, A, r_new, ea); });
         if (e != cudaSuccess) return e;
+        if (stream_tl) {
+            e = tl_after(h, *sink, 0, k, 0, c.n_freq, int64_t(c.n_theta) * g->n_depth, d_tl, c.stream);
+            if (e != cudaSuccess) return e;
+        }
     }
     return cudaSuccess;
 }
@@ -403,9 +531,22 @@ int pe3d_handle_destroy(void* handle) {
     return PE3D_OK;
 }
 
+static int march_device_impl(void* handle, const pe3d_grid* g, const pe3d_coeffs* coeffs, const pe3d_c128* d_local,
+                             const pe3d_c128* d_u0, pe3d_c128* d_u_final, double* d_tl, pe3d_c128* d_snapshots,
+                             int64_t* d_clamped, void* stream_v, pe3d_error* err, const TlSink* sink);
+
 int pe3d_march_device(void* handle, const pe3d_grid* g, const pe3d_coeffs* coeffs, const pe3d_c128* d_local,
                       const pe3d_c128* d_u0, pe3d_c128* d_u_final, double* d_tl, pe3d_c128* d_snapshots,
                       int64_t* d_clamped, void* stream_v, pe3d_error* err) {
+    return march_device_impl(handle, g, coeffs, d_local, d_u0, d_u_final, d_tl, d_snapshots, d_clamped, stream_v, err,
+                             nullptr);
+}
+
+// sink != null (pe3d_march_host with a page-locked TL stack): d_tl is the
+// device ring [F][R][n_theta][n_depth] and the samples stream to sink->host.
+static int march_device_impl(void* handle, const pe3d_grid* g, const pe3d_coeffs* coeffs, const pe3d_c128* d_local,
+                             const pe3d_c128* d_u0, pe3d_c128* d_u_final, double* d_tl, pe3d_c128* d_snapshots,
+                             int64_t* d_clamped, void* stream_v, pe3d_error* err, const TlSink* sink) {
     Handle* h = static_cast<Handle*>(handle);
     if (!h) return bad_arg(err, "null handle");
     int st = check_grid(g, coeffs, err);
@@ -483,10 +624,11 @@ int pe3d_march_device(void* handle, const pe3d_grid* g, const pe3d_coeffs* coeff
     ea0.final_out = g->n_steps == 0 ? reinterpret_cast<cplx*>(d_u_final) : nullptr;
     ea0.clamped = d_clamped;
     ea0.w_abs = h->w_abs.as<double>();
-    ea0.n_samples = S;
+    ea0.n_samples = sink ? sink->R : S;
     ea0.sample = 0;
     ea0.periodic = g->topology == PE3D_PERIODIC;
     ea0.write_temp = g->n_steps > 0;
+    if (sink) CK(tl_prepare(h, *sink), "tl streams");
     CK(prof.run(2, [&] { return pe3d::launch_finish(c, reinterpret_cast<const cplx*>(d_u0), 0, h->field_a.as<cplx>(),
                                                      g->r_input, ea0); }),
        "prepare");
@@ -510,6 +652,8 @@ int pe3d_march_device(void* handle, const pe3d_grid* g, const pe3d_coeffs* coeff
         add(tabs, sizeof(tabs));
         const int chains = step_chains(p.ctx, false);
         add(&chains, sizeof(chains));
+        const TlSink none{nullptr, 0, 0};
+        add(sink ? sink : &none, sizeof(TlSink));
         if (!(h->graph_exec && key == h->graph_key)) {
             if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
             h->graph_exec = nullptr;
@@ -517,7 +661,8 @@ int pe3d_march_device(void* handle, const pe3d_grid* g, const pe3d_coeffs* coeff
             cudaGraph_t graph = nullptr;
             CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal), "capture");
             cudaError_t e = enqueue_steps(h, g, p, local, d_tl, reinterpret_cast<cplx*>(d_snapshots),
-                                          reinterpret_cast<cplx*>(d_u_final), d_clamped, h->w_abs.as<double>(), prof);
+                                          reinterpret_cast<cplx*>(d_u_final), d_clamped, h->w_abs.as<double>(), prof,
+                                          sink);
             cudaError_t e2 = cudaStreamEndCapture(stream, &graph);
             if (e != cudaSuccess) { if (graph) cudaGraphDestroy(graph); return cuda_fail(err, e, "enqueue"); }
             if (e2 != cudaSuccess) return cuda_fail(err, e2, "end capture");
@@ -529,7 +674,7 @@ int pe3d_march_device(void* handle, const pe3d_grid* g, const pe3d_coeffs* coeff
         CK(cudaGraphLaunch(h->graph_exec, stream), "graph launch");
     } else {
         CK(enqueue_steps(h, g, p, local, d_tl, reinterpret_cast<cplx*>(d_snapshots),
-                         reinterpret_cast<cplx*>(d_u_final), d_clamped, h->w_abs.as<double>(), prof),
+                         reinterpret_cast<cplx*>(d_u_final), d_clamped, h->w_abs.as<double>(), prof, sink),
            "enqueue");
     }
     CK(cudaGetLastError(), "launch");
@@ -553,16 +698,27 @@ int pe3d_march_host(void* handle, const pe3d_grid* g, const pe3d_coeffs* coeffs,
     CK(h->h_u0.ensure(F * slab * sizeof(cplx)), "alloc");
     CK(h->h_clamped.ensure(F * sizeof(int64_t)), "alloc");
     if (u_final) CK(h->h_final.ensure(F * slab * sizeof(cplx)), "alloc");
-    if (tl) CK(h->h_tl.ensure(F * S * slab * sizeof(double)), "alloc");
+    // A page-locked TL stack (and no snapshots): stream the samples out while
+    // the march runs, through a device ring of a few samples per frequency.
+    TlSink sink{nullptr, 0, 0};
+    if (tl && !snapshots && !getenv("PE3D_NO_TL_STREAM")) {
+        cudaPointerAttributes pa{};
+        if (cudaPointerGetAttributes(&pa, tl) == cudaSuccess && pa.type == cudaMemoryTypeHost)
+            sink = TlSink{tl, int(S), int(S < 4 ? S : 4)};
+        cudaGetLastError();                                  // pageable memory: not an error
+    }
+    if (tl) CK(h->h_tl.ensure(F * (sink.host ? sink.R : S) * slab * sizeof(double)), "alloc");
     if (snapshots) CK(h->h_snap.ensure(F * S * slab * sizeof(cplx)), "alloc");
     CK(cudaMemcpyAsync(h->h_local.ptr, local, F * g->n_depth * sizeof(cplx), cudaMemcpyHostToDevice, s), "H2D");
     CK(cudaMemcpyAsync(h->h_u0.ptr, u0, F * slab * sizeof(cplx), cudaMemcpyHostToDevice, s), "H2D");
-    st = pe3d_march_device(handle, g, coeffs, h->h_local.as<pe3d_c128>(), h->h_u0.as<pe3d_c128>(),
+    st = march_device_impl(handle, g, coeffs, h->h_local.as<pe3d_c128>(), h->h_u0.as<pe3d_c128>(),
                            u_final ? h->h_final.as<pe3d_c128>() : nullptr, tl ? h->h_tl.as<double>() : nullptr,
-                           snapshots ? h->h_snap.as<pe3d_c128>() : nullptr, h->h_clamped.as<int64_t>(), s, err);
+                           snapshots ? h->h_snap.as<pe3d_c128>() : nullptr, h->h_clamped.as<int64_t>(), s, err,
+                           sink.host ? &sink : nullptr);
     if (st != PE3D_OK) return st;
     if (u_final) CK(cudaMemcpyAsync(u_final, h->h_final.ptr, F * slab * sizeof(cplx), cudaMemcpyDeviceToHost, s), "D2H");
-    if (tl) CK(cudaMemcpyAsync(tl, h->h_tl.ptr, F * S * slab * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
+    if (tl && !sink.host)
+        CK(cudaMemcpyAsync(tl, h->h_tl.ptr, F * S * slab * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
     if (snapshots)
         CK(cudaMemcpyAsync(snapshots, h->h_snap.ptr, F * S * slab * sizeof(cplx), cudaMemcpyDeviceToHost, s), "D2H");
     if (clamped) CK(cudaMemcpyAsync(clamped, h->h_clamped.ptr, F * sizeof(int64_t), cudaMemcpyDeviceToHost, s), "D2H");

@@ -381,6 +381,49 @@ def test_parallel_factorization_matches_reference_recurrence(monkeypatch):
         assert tl_err(y.tl_field, x.tl_field) <= 1e-9
 
 
+@pytest.mark.parametrize("n_steps,stride,chains,topology", [
+    (0, 1, "2", PERIODIC), (6, 6, "2", PERIODIC), (6, 2, "1", PERIODIC), (21, 3, "2", PERIODIC),
+    (21, 3, "3", PERIODIC), (13, 2, "1", SECTOR)])
+def test_tl_streaming_to_pinned_host(monkeypatch, n_steps, stride, chains, topology):
+    """pe3d_march_host with a page-locked TL stack streams the samples through
+    a device ring (R = min(S, 4) slots, copies overlapping the march, ring
+    wrap-around when S > 4): bitwise the stack copied after the march."""
+    import ctypes as C
+    import torch
+    from paper_1711_00005_b200.marching import _grid_params, _local_column
+    from paper_1711_00005_b200.environment import gaussian_starter
+    monkeypatch.setenv("PE3D_CHAINS", chains)
+    freqs = (50.0, 90.0, 150.0, 300.0)
+    grid = make_grid(n_range=max(n_steps, 3), n_azimuth=64, n_depth=96, delta_r=5.0, delta_z=2.0, r_start=5.0,
+                     topology=topology)
+    env = make_env(grid)
+    src = SourceSpec(freqs, 0.4 * grid.depth_extent)
+    k0s = [wavenumber(f, 1500.0) for f in freqs]
+    coeffs = _native.make_coeffs(k0s, [StepCoefficients.for_step(k0, grid.delta_r) for k0 in k0s])
+    local = np.ascontiguousarray(np.stack([_local_column(env, grid, grid.r_start, k0) for k0 in k0s]))
+    u0 = np.ascontiguousarray(np.stack([gaussian_starter(grid, src, k0).values for k0 in k0s]))
+    S = 1 + n_steps // stride
+    F, NT, NZ = len(freqs), grid.n_azimuth, grid.n_depth
+
+    def run(streamed):
+        if streamed:
+            monkeypatch.delenv("PE3D_NO_TL_STREAM", raising=False)
+        else:
+            monkeypatch.setenv("PE3D_NO_TL_STREAM", "1")
+        tl = torch.empty((F, S, NT, NZ), dtype=torch.float64).pin_memory()
+        fin = torch.empty((F, NT, NZ * 2), dtype=torch.float64).pin_memory()
+        cl = torch.zeros(F, dtype=torch.int64).pin_memory()
+        g = _grid_params(grid, F, n_steps, stride, 0, grid.r_start)
+        _native.call("pe3d_march_host", _native.handle(), g, coeffs, _native.ptr(local), _native.ptr(u0),
+                     C.c_void_p(fin.data_ptr()), C.c_void_p(tl.data_ptr()), None, C.c_void_p(cl.data_ptr()))
+        return tl.numpy().copy(), fin.numpy().copy(), cl.numpy().copy()
+
+    a, b = run(True), run(False)
+    for x, y in zip(a, b):
+        assert x.tobytes() == y.tobytes()
+    assert np.isfinite(a[0]).all()
+
+
 def test_run_frequency_contract():
     grid = make_grid(n_range=10, delta_r=5.0, r_start=5.0)
     env = make_env(grid)
