@@ -215,6 +215,52 @@ def run_reference_arm(a, rank, world):
 
 # ----------------------------------------------------------------- GPU arm
 
+def secondary_config(name, steps, local):
+    """Device-time throughput of another BASELINE config on this GPU: one
+    graph of `steps` steps, inputs resident, CUDA events (as the main line)."""
+    import torch
+    import ctypes as C
+    from paper_1711_00005_b200 import _native
+    from paper_1711_00005_b200.environment import gaussian_starter, wavenumber
+    from paper_1711_00005_b200.marching import _grid_params, _local_column
+    from paper_1711_00005_b200.operators import StepCoefficients
+    cfg = workload(name, steps)
+    grid, env, source, _ = cfg
+    freqs = list(source.frequencies)
+    k0s = [wavenumber(f, env.c0) for f in freqs]
+    coeffs = _native.make_coeffs(k0s, [StepCoefficients.for_step(k0, grid.delta_r) for k0 in k0s])
+    dev = torch.device("cuda", local)
+    d_local = torch.from_numpy(np.ascontiguousarray(np.stack(
+        [_local_column(env, grid, grid.r_start, k0) for k0 in k0s])).view(np.float64)).to(dev)
+    d_u0 = torch.from_numpy(np.ascontiguousarray(np.stack(
+        [gaussian_starter(grid, source, k0).values for k0 in k0s])).view(np.float64)).to(dev)
+    d_final = torch.empty_like(d_u0)
+    d_cl = torch.zeros(len(freqs), dtype=torch.int64, device=dev)
+    tl = torch.empty((len(freqs), 2, grid.n_azimuth, grid.n_depth), dtype=torch.float64, device=dev)
+    stream = torch.cuda.Stream(device=dev)
+    h = _native.handle(local)
+
+    def march():
+        g = _grid_params(grid, len(freqs), steps, steps, 0, grid.r_start)
+        _native.call("pe3d_march_device", h, g, coeffs, C.c_void_p(d_local.data_ptr()), C.c_void_p(d_u0.data_ptr()),
+                     C.c_void_p(d_final.data_ptr()), C.c_void_p(tl.data_ptr()), None, C.c_void_p(d_cl.data_ptr()),
+                     C.c_void_p(stream.cuda_stream))
+    with torch.cuda.stream(stream):
+        march()
+        march()
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        t0.record(stream)
+        march()
+        t1.record(stream)
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1)
+    pts = len(freqs) * grid.n_azimuth * grid.n_depth * steps
+    return {"value": pts / (ms / 1e3), "unit": UNIT, "ms_per_step": ms / steps, "steps": steps,
+            "l2": "field L2-resident (8 MiB)", "note": "BASELINE configs[1]; HBM roofline not meaningful"}
+
+
 def run_gpu_arm(a, rank, world, local):
     import torch
     import ctypes as C
@@ -333,6 +379,11 @@ def run_gpu_arm(a, rank, world, local):
                "d2h_bytes_per_step": d2h / a.steps, "wall_s": wall,
                "path": "pe3d_march_host (C ABI, pinned host buffers; starter+medium in, final slab+TL out)"}
 
+    # BASELINE configs[1] (cfg2, L2-resident) alongside, measured the same way
+    secondary = None
+    if rank == 0 and world == 1 and a.workload == "cfg4" and not a.no_cpu:
+        secondary = {"cfg2": secondary_config("cfg2", 400, local)}
+
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:
         nf, ns = CPU_SAMPLES[a.workload]
@@ -357,6 +408,7 @@ def run_gpu_arm(a, rank, world, local):
             "e2e": e2e,
             "gpu_launches": sum(kn),
             "clocks": clocks.summary(),
+            "secondary": secondary,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
