@@ -985,42 +985,124 @@ int pe3d_march_medium_host(void* handle, const pe3d_grid* g, const pe3d_coeffs* 
     ea0.write_temp = g->n_steps > 0;
     CK(pe3d::launch_finish(c, h->h_u0.as<cplx>(), 0, A, g->r_input, ea0), "prepare");
     const int64_t E = periodic ? pe3d::ring_table_elems(NT) : 0;
-    for (int k = 0; k < g->n_steps; ++k) {
-        const int j_new = g->first_index + k + 1;
-        const double r_new = g->r_start + j_new * g->delta_r;
-        cplx* now = L[k & 1];
-        cplx* nxt = L[(k + 1) & 1];
-        if (scan_path) {
-            CK(pe3d::launch_depth_medium_scan(c, M, A, B, now, nxt, g->delta_z, r_new, h->fail_row.as<int>(),
-                                              h->fail_mag.as<double>()),
-               "depth");
-        } else {
-            CK(pe3d::launch_medium_local(c, M, nxt, g->delta_z, r_new), "medium");
-            CK(pe3d::launch_depth_serial(c, A, B, Cc, now, nxt, int64_t(NZ) * NT, 1, NT, h->fail_row.as<int>(),
-                                         h->fail_mag.as<double>()),
-               "depth");
+    // The step loop.  Scan path: the medium at r_(j+1) is evaluated on the
+    // whole grid by a wide kernel on a side stream, one step ahead, so it
+    // overlaps the previous step's azimuth sweep; the per-column scan reads
+    // it (that kernel has one small CTA per column and is latency bound).
+    const bool pre = scan_path && !getenv("PE3D_MEDIUM_FUSED");
+    if (pre) {
+        if (!h->chain_stream[0]) CK(cudaStreamCreateWithFlags(&h->chain_stream[0], cudaStreamNonBlocking), "stream");
+        for (int k = 0; k < 2; ++k)
+            if (!h->chain_join[k]) CK(cudaEventCreateWithFlags(&h->chain_join[k], cudaEventDisableTiming), "event");
+        if (!h->chain_fork) CK(cudaEventCreateWithFlags(&h->chain_fork, cudaEventDisableTiming), "event");
+    }
+    cudaStream_t sd = h->chain_stream[0];
+    cudaEvent_t ev_med = h->chain_join[0], ev_scan = h->chain_join[1];
+    auto step_loop = [&]() -> cudaError_t {
+        cudaError_t e = cudaSuccess;
+        if (pre && g->n_steps > 0) {                    // medium of step 0, on the side stream
+            e = cudaEventRecord(h->chain_fork, s);
+            if (e == cudaSuccess) e = cudaStreamWaitEvent(sd, h->chain_fork, 0);
+            if (e == cudaSuccess) {
+                pe3d::LaunchCtx cs = c;
+                cs.stream = sd;
+                e = pe3d::launch_medium_local_tiles(cs, M, L[1], g->delta_z,
+                                                    g->r_start + (g->first_index + 1) * g->delta_r);
+            }
+            if (e == cudaSuccess) e = cudaEventRecord(ev_med, sd);
         }
-        CK(pe3d::launch_reduce_failures(h->fail_row.as<int>(), h->fail_mag.as<double>(), F, NT, j_new, 0, -1, c.err, s),
-           "reduce");
-        pe3d::EpilogueArgs ea{};
-        const bool record = ((k + 1) % g->output_stride) == 0;
-        ea.tl = record ? d_tl : nullptr;
-        ea.snap = record ? d_snap : nullptr;
-        ea.final_out = (k == g->n_steps - 1) ? d_final : nullptr;
-        ea.clamped = d_cl;
-        ea.n_samples = S;
-        ea.sample = (k + 1) / g->output_stride;
-        ea.w_abs = h->w_abs.as<double>() + int64_t(ea.sample) * F;
-        ea.periodic = periodic;
-        ea.write_temp = (k < g->n_steps - 1);
-        if (periodic) {
-            CK(pe3d::launch_azimuth_scan(c, B, A, h->ring_tab.as<cplx>() + int64_t(k) * F * E, r_new, ea), "azimuth");
-        } else {
-            CK(pe3d::launch_azimuth_serial(c, B, Cc, h->az_cp.as<cplx>(), h->az_inv.as<cplx>(), h->az_q.as<cplx>(),
-                                           h->az_ring.as<cplx>(), r_new, j_new),
-               "azimuth");
-            CK(pe3d::launch_finish(c, Cc, 1, A, r_new, ea), "finish");
+        for (int k = 0; k < g->n_steps && e == cudaSuccess; ++k) {
+            const int j_new = g->first_index + k + 1;
+            const double r_new = g->r_start + j_new * g->delta_r;
+            cplx* now = L[k & 1];
+            cplx* nxt = L[(k + 1) & 1];
+            if (scan_path) {
+                if (pre) e = cudaStreamWaitEvent(s, ev_med, 0);
+                if (e == cudaSuccess)
+                    e = pe3d::launch_depth_medium_scan(c, M, A, B, now, nxt, g->delta_z, r_new, h->fail_row.as<int>(),
+                                                       h->fail_mag.as<double>(), pre ? 1 : 0);
+                if (pre && e == cudaSuccess) {          // medium of step k+1 into `now`, once the scan read it
+                    e = cudaEventRecord(ev_scan, s);
+                    if (e == cudaSuccess) e = cudaStreamWaitEvent(sd, ev_scan, 0);
+                    if (e == cudaSuccess && k + 1 < g->n_steps) {
+                        pe3d::LaunchCtx cs = c;
+                        cs.stream = sd;
+                        e = pe3d::launch_medium_local_tiles(cs, M, now, g->delta_z, r_new + g->delta_r);
+                    }
+                    if (e == cudaSuccess) e = cudaEventRecord(ev_med, sd);
+                }
+            } else {
+                e = pe3d::launch_medium_local(c, M, nxt, g->delta_z, r_new);
+                if (e == cudaSuccess)
+                    e = pe3d::launch_depth_serial(c, A, B, Cc, now, nxt, int64_t(NZ) * NT, 1, NT, h->fail_row.as<int>(),
+                                                  h->fail_mag.as<double>());
+            }
+            if (e == cudaSuccess)
+                e = pe3d::launch_reduce_failures(h->fail_row.as<int>(), h->fail_mag.as<double>(), F, NT, j_new, 0, -1,
+                                                 c.err, s);
+            if (e != cudaSuccess) break;
+            pe3d::EpilogueArgs ea{};
+            const bool record = ((k + 1) % g->output_stride) == 0;
+            ea.tl = record ? d_tl : nullptr;
+            ea.snap = record ? d_snap : nullptr;
+            ea.final_out = (k == g->n_steps - 1) ? d_final : nullptr;
+            ea.clamped = d_cl;
+            ea.n_samples = S;
+            ea.sample = (k + 1) / g->output_stride;
+            ea.w_abs = h->w_abs.as<double>() + int64_t(ea.sample) * F;
+            ea.periodic = periodic;
+            ea.write_temp = (k < g->n_steps - 1);
+            if (periodic) {
+                e = pe3d::launch_azimuth_scan(c, B, A, h->ring_tab.as<cplx>() + int64_t(k) * F * E, r_new, ea);
+            } else {
+                e = pe3d::launch_azimuth_serial(c, B, Cc, h->az_cp.as<cplx>(), h->az_inv.as<cplx>(),
+                                                h->az_q.as<cplx>(), h->az_ring.as<cplx>(), r_new, j_new);
+                if (e == cudaSuccess) e = pe3d::launch_finish(c, Cc, 1, A, r_new, ea);
+            }
         }
+        if (pre && g->n_steps > 0) {                    // join the side stream (always, for a clean capture)
+            cudaError_t e2 = cudaStreamWaitEvent(s, ev_med, 0);
+            if (e == cudaSuccess) e = e2;
+        }
+        return e;
+    };
+    if (!(g->flags & PE3D_FLAG_NO_GRAPH) && g->n_steps >= 2) {
+        // one CUDA graph for the step loop (the side stream included), reused
+        // while every baked-in argument repeats (the handle's graph cache)
+        std::vector<unsigned char> key;
+        auto add = [&](const void* q, size_t n) {
+            const unsigned char* b = static_cast<const unsigned char*>(q);
+            key.insert(key.end(), b, b + n);
+        };
+        const char tag[] = "medium";
+        add(tag, sizeof(tag));
+        add(g, sizeof(*g));
+        add(coeffs, sizeof(pe3d_coeffs) * F);
+        add(&M, sizeof(M));
+        const void* ptrs[12] = {A, B, Cc, L[0], L[1], d_tl, d_snap, d_final, d_cl, h->ring_tab.ptr, h->w_abs.ptr,
+                                h->fail_row.ptr};
+        add(ptrs, sizeof(ptrs));
+        add(&s, sizeof(s));
+        const int flags2[2] = {pre ? 1 : 0, scan_path ? 1 : 0};
+        add(flags2, sizeof(flags2));
+        if (!(h->graph_exec && key == h->graph_key)) {
+            if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
+            h->graph_exec = nullptr;
+            h->graph_key.clear();
+            cudaGraph_t graph = nullptr;
+            CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "capture");
+            cudaError_t e = step_loop();
+            cudaError_t e2 = cudaStreamEndCapture(s, &graph);
+            if (e != cudaSuccess) { if (graph) cudaGraphDestroy(graph); return cuda_fail(err, e, "enqueue"); }
+            if (e2 != cudaSuccess) return cuda_fail(err, e2, "end capture");
+            e = cudaGraphInstantiate(&h->graph_exec, graph, 0);
+            cudaGraphDestroy(graph);
+            if (e != cudaSuccess) { h->graph_exec = nullptr; return cuda_fail(err, e, "instantiate"); }
+            h->graph_key = key;
+        }
+        CK(cudaGraphLaunch(h->graph_exec, s), "graph launch");
+    } else {
+        CK(step_loop(), "enqueue");
     }
     st = decode_error(h, s, err);
     if (st != PE3D_OK) return st;

@@ -113,7 +113,7 @@ cudaError_t launch_medium_local(const LaunchCtx& c, const MediumDev& M, cplx* lo
 cudaError_t launch_medium_local_tiles(const LaunchCtx& c, const MediumDev& M, cplx* local, double dz, double r);
 cudaError_t launch_depth_medium_scan(const LaunchCtx& c, const MediumDev& M, const cplx* src, cplx* dst,
                                      const cplx* local_now, cplx* local_next, double dz, double r_new, int* fail_row,
-                                     double* fail_mag);
+                                     double* fail_mag, int precomputed);
 cudaError_t launch_azimuth_serial(const LaunchCtx& c, const cplx* src, cplx* dst, cplx* cp, cplx* inv, cplx* qv,
                                   cplx* ring, double r_new, int step_for_error);
 cudaError_t launch_solve_batch(int n, int members, int cyclic, StridedC sub, StridedC mainv, StridedC sup,

@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(512)
 k_depth_medium_scan(MediumDev M, const cplx* __restrict__ src, cplx* __restrict__ dst,
                     const cplx* __restrict__ local_now, cplx* __restrict__ local_next, const FreqDev* __restrict__ fdev,
                     int n_theta, int n_tiles, int n_depth, double delta_theta, double dz, double r_new, int sector,
-                    int* __restrict__ fail_row, double* __restrict__ fail_mag) {
+                    int* __restrict__ fail_row, double* __restrict__ fail_mag, int precomputed) {
     __shared__ M2 sM[16];
     __shared__ cplx sPY[16][2];
     __shared__ cplx sUp[16], sDn[16];
@@ -163,8 +163,12 @@ k_depth_medium_scan(MediumDev M, const cplx* __restrict__ src, cplx* __restrict_
         const bool real_row = active && l < n_depth;
         x[i] = active ? ldc(src + line + i) : czero();
         ln[i] = real_row ? ldc(local_now + line + i) : czero();
-        lw[i] = real_row ? medium_local(M, r_new, theta, l, n_depth, dz, fd.k0) : czero();
-        if (active) stc(local_next + line + i, lw[i]);
+        if (precomputed) {                          // local_next filled by k_medium_local_tiles
+            lw[i] = real_row ? ldc(local_next + line + i) : czero();
+        } else {
+            lw[i] = real_row ? medium_local(M, r_new, theta, l, n_depth, dz, fd.k0) : czero();
+            if (active) stc(local_next + line + i, lw[i]);
+        }
     }
     // ---- halos
     cplx up = shfl_up(x[7], 1), dn = shfl_down(x[0], 1);
@@ -283,13 +287,13 @@ k_depth_medium_scan(MediumDev M, const cplx* __restrict__ src, cplx* __restrict_
 
 cudaError_t launch_depth_medium_scan(const LaunchCtx& c, const MediumDev& M, const cplx* src, cplx* dst,
                                      const cplx* local_now, cplx* local_next, double dz, double r_new, int* fail_row,
-                                     double* fail_mag) {
+                                     double* fail_mag, int precomputed) {
     const int nthreads = (c.n_tiles + 31) / 32 * 32;
     if (nthreads > 512) return cudaErrorNotSupported;
     dim3 grid(c.n_theta, c.n_freq);
     k_depth_medium_scan<<<grid, nthreads, 0, c.stream>>>(M, src, dst, local_now, local_next, c.fdev, c.n_theta,
                                                          c.n_tiles, c.n_depth, c.delta_theta, dz, r_new, c.sector,
-                                                         fail_row, fail_mag);
+                                                         fail_row, fail_mag, precomputed);
     return cudaGetLastError();
 }
 
