@@ -138,11 +138,12 @@ __device__ __forceinline__ M2 shfl_up_m2(const M2& x, int d) {
     return M2{shfl_up(x.a, d), shfl_up(x.b, d), shfl_up(x.c, d), shfl_up(x.d, d)};
 }
 
-__global__ void __launch_bounds__(512)
+template <bool PRE, int MAXT>
+__global__ void __launch_bounds__(MAXT)
 k_depth_medium_scan(MediumDev M, const cplx* __restrict__ src, cplx* __restrict__ dst,
                     const cplx* __restrict__ local_now, cplx* __restrict__ local_next, const FreqDev* __restrict__ fdev,
                     int n_theta, int n_tiles, int n_depth, double delta_theta, double dz, double r_new, int sector,
-                    int* __restrict__ fail_row, double* __restrict__ fail_mag, int precomputed) {
+                    int* __restrict__ fail_row, double* __restrict__ fail_mag) {
     __shared__ M2 sM[16];
     __shared__ cplx sPY[16][2];
     __shared__ cplx sUp[16], sDn[16];
@@ -163,7 +164,7 @@ k_depth_medium_scan(MediumDev M, const cplx* __restrict__ src, cplx* __restrict_
         const bool real_row = active && l < n_depth;
         x[i] = active ? ldc(src + line + i) : czero();
         ln[i] = real_row ? ldc(local_now + line + i) : czero();
-        if (precomputed) {                          // local_next filled by k_medium_local_tiles
+        if (PRE) {                                  // local_next filled by k_medium_local_tiles
             lw[i] = real_row ? ldc(local_next + line + i) : czero();
         } else {
             lw[i] = real_row ? medium_local(M, r_new, theta, l, n_depth, dz, fd.k0) : czero();
@@ -291,9 +292,13 @@ cudaError_t launch_depth_medium_scan(const LaunchCtx& c, const MediumDev& M, con
     const int nthreads = (c.n_tiles + 31) / 32 * 32;
     if (nthreads > 512) return cudaErrorNotSupported;
     dim3 grid(c.n_theta, c.n_freq);
-    k_depth_medium_scan<<<grid, nthreads, 0, c.stream>>>(M, src, dst, local_now, local_next, c.fdev, c.n_theta,
-                                                         c.n_tiles, c.n_depth, c.delta_theta, dz, r_new, c.sector,
-                                                         fail_row, fail_mag, precomputed);
+    // the precomputed-medium instantiation carries no medium code: this kernel
+    // runs at low occupancy and its size showed up as instruction-cache stalls
+    // (columns of up to 128 tiles also get the register budget of a 128-thread CTA: no spills)
+    auto kern = nthreads <= 128 ? (precomputed ? k_depth_medium_scan<true, 128> : k_depth_medium_scan<false, 128>)
+                                : (precomputed ? k_depth_medium_scan<true, 512> : k_depth_medium_scan<false, 512>);
+    kern<<<grid, nthreads, 0, c.stream>>>(M, src, dst, local_now, local_next, c.fdev, c.n_theta, c.n_tiles, c.n_depth,
+                                          c.delta_theta, dz, r_new, c.sector, fail_row, fail_mag);
     return cudaGetLastError();
 }
 
