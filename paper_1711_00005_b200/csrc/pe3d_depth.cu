@@ -382,14 +382,14 @@ struct DepthDst {
 // last tile), completion on a per-warp mbarrier, and one TMA bulk store of
 // the solved column from the same stage.  The warps issue no per-line
 // copies at all; a 3-deep per-warp stage ring keeps two columns in flight.
-template <int STAGES, int MINB, int MAXT>
+template <int STAGES, int MINB, int MAXT, int NTH = 0>
 __global__ void __launch_bounds__(MAXT, MINB)
 k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ DepthDst tm_dst,
             const cplx* __restrict__ loc_tab, const cplx* __restrict__ mul_tab, const FreqDev* __restrict__ fdev,
             int n_theta, int n_tiles, int64_t total_cols, int cols_per_cta, int sector) {
     constexpr int RPT = 8;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    const int nthreads = blockDim.x;
+    const int nthreads = NTH ? NTH : int(blockDim.x);   // compile-time when NTH: constant table offsets
     const int nwarps = nthreads >> 5;
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     // 1024-B aligned stage ring (128-B swizzle atoms), then barriers and tables
@@ -414,6 +414,7 @@ k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ 
     const int nz8 = n_tiles * 8;
     const bool active = t * RPT < nz8;
     const int tile0 = warp * 32;
+    const int qdst = tile0 / tm_dst.nzt;            // output map of this warp's tiles
 
     if (lane == 0) {
 #pragma unroll
@@ -546,10 +547,7 @@ k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ 
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-            {
-                const int qd = tile0 / tm_dst.nzt;
-                tma_store_4d(&tm_dst.m[qd], 0, col, tile0 - qd * tm_dst.nzt, f, cur);
-            }
+            tma_store_4d(&tm_dst.m[qdst], 0, col, tile0 - qdst * tm_dst.nzt, f, cur);
             bulk_commit();
             bulk_wait_read<1>();            // the previous column's store has left its stage slot
             if (it + STAGES - 1 < n_cols) {
@@ -581,8 +579,8 @@ k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ 
 // (mbarrier transaction counts, no cluster barrier in the loop).  The depth
 // stencil's halo rows across sub-column edges are plain global loads of the
 // (read-only) input.
-template <int STAGES, int MINB>
-__global__ void __launch_bounds__(128, MINB)
+template <int STAGES, int MINB, int NTH>
+__global__ void __launch_bounds__(NTH, MINB)
 k_depth_tma_cluster(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ DepthDst tm_dst,
                     const cplx* __restrict__ src_raw, const cplx* __restrict__ loc_tab,
                     const cplx* __restrict__ mul_tab, const FreqDev* __restrict__ fdev, int n_theta, int n_tiles,
@@ -593,8 +591,8 @@ k_depth_tma_cluster(const __grid_constant__ CUtensorMap tm_src, const __grid_con
     const int CL = int(cluster.num_blocks());
     const int s = int(cluster.block_rank());
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    const int nthreads = blockDim.x;                // = 32 * tiles per CTA / 32 ... one tile per thread
-    const int nwarps = nthreads >> 5;
+    constexpr int nthreads = NTH;                   // one tile per thread (= tiles per CTA)
+    constexpr int nwarps = NTH / 32;
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     cplx* base = reinterpret_cast<cplx*>(smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u));
     cplx* stage = base + warp * (STAGES * 256);
@@ -622,6 +620,7 @@ k_depth_tma_cluster(const __grid_constant__ CUtensorMap tm_src, const __grid_con
     const int n_cols = int(g1 - g0);
     const int nz8 = n_tiles * 8;
     const int tile0 = s * tpc + warp * 32;
+    const int qdst = tile0 / tm_dst.nzt;            // output map of this warp's tiles
 
     if (lane == 0) {
 #pragma unroll
@@ -816,10 +815,7 @@ k_depth_tma_cluster(const __grid_constant__ CUtensorMap tm_src, const __grid_con
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-            {
-                const int qd = tile0 / tm_dst.nzt;
-                tma_store_4d(&tm_dst.m[qd], 0, col, tile0 - qd * tm_dst.nzt, f, cur);
-            }
+            tma_store_4d(&tm_dst.m[qdst], 0, col, tile0 - qdst * tm_dst.nzt, f, cur);
             bulk_commit();
             bulk_wait_read<1>();
             if (it + STAGES - 1 < n_cols) {
@@ -893,7 +889,7 @@ static cudaError_t launch_depth_tma_cfg(const LaunchCtx& c, const cplx* src, cpl
     const size_t bytes = 1024 + sizeof(cplx) * (size_t(nwarps) * STAGES * 256 + 10 * size_t(nthreads) + 5 * nwarps) +
                          sizeof(uint64_t) * nwarps * STAGES;
     if (bytes > 227 * 1024) return cudaErrorNotSupported;
-    auto kern = k_depth_tma<STAGES, MINB, MAXT>;
+    auto kern = (MAXT == 128 && nthreads == 128) ? k_depth_tma<STAGES, MINB, MAXT, 128> : k_depth_tma<STAGES, MINB, MAXT>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
     if (e != cudaSuccess) return e;
     const int64_t total = int64_t(c.n_freq) * c.n_theta;
@@ -918,7 +914,8 @@ static cudaError_t launch_depth_tma_cluster(const LaunchCtx& c, const cplx* src,
     const size_t bytes = 1024 + sizeof(cplx) * (size_t(nwarps) * STAGES * 256 + 12 * size_t(nthreads) + 5 * nwarps +
                                                 2 * 16 * 2 + 2 * 16 + 4) +
                          sizeof(uint64_t) * (4 + nwarps * STAGES);
-    auto kern = k_depth_tma_cluster<STAGES, MINB>;
+    if (nthreads != 128) return cudaErrorNotSupported;
+    auto kern = k_depth_tma_cluster<STAGES, MINB, 128>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
