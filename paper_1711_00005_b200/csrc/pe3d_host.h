@@ -1,0 +1,202 @@
+// pe3d_host.h -- host-side internals shared by the C ABI translation units
+// (pe3d_abi.cu: handles and marches; pe3d_slab.cu: the slab-decomposed
+// march): device workspace buffers, the handle, error records and the small
+// helpers every entry point uses.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "../../include/pe3d_b200.h"
+#include "pe3d_internal.h"
+
+namespace pe3d_host {
+
+using pe3d::cplx;
+
+struct DevBuf {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+    cudaError_t ensure(size_t want) {
+        if (want <= bytes) return cudaSuccess;
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        bytes = 0;
+        cudaError_t e = cudaMalloc(&ptr, want);
+        if (e == cudaSuccess) bytes = want;
+        return e;
+    }
+    void release() {
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        bytes = 0;
+    }
+    template <class T> T* as() const { return static_cast<T*>(ptr); }
+};
+
+struct Handle {
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t stream = nullptr;
+    // march workspace
+    DevBuf field_a, field_b, field_c;     // device tiles [F][n_tiles][n_theta][8]
+    DevBuf loc_tab, mul_tab, fdev, w_abs, err;
+    DevBuf az_cp, az_inv, az_q, az_ring, fail_row, fail_mag, ring_tab;
+    // staging for the host entry points
+    DevBuf h_local, h_local2, h_u0, h_final, h_tl, h_snap, h_clamped;
+    // solve_batch
+    DevBuf sb_in, sb_x, sb_cp, sb_inv, sb_y, sb_q;
+    // extended medium (profile, lattice, two local-term grids)
+    DevBuf med_prof, med_lat, med_local;
+    // slab march: ordering counters of the peer-direct transposes
+    DevBuf slab_flags;
+    // one cached step-loop graph (reused when a march repeats with identical arguments)
+    std::vector<unsigned char> graph_key;
+    cudaGraphExec_t graph_exec = nullptr;
+    // PE3D_FLAG_PROFILE accounting
+    double prof_ms[3] = {0, 0, 0};
+    int32_t prof_n[3] = {0, 0, 0};
+    // concurrent step-loop chains over disjoint frequency groups
+    static constexpr int MAX_CHAINS = 4;
+    cudaStream_t chain_stream[MAX_CHAINS] = {};
+    cudaEvent_t chain_fork = nullptr, chain_join[MAX_CHAINS] = {};
+    // TL streaming to the host (pe3d_march_host): one copy stream per chain
+    // plus one for the starting sample, and their events
+    cudaStream_t tl_side[MAX_CHAINS + 1] = {};
+    std::vector<cudaEvent_t> tl_ev;
+};
+
+// Launch wrapper: in profile mode, bracket each launch with events.
+struct Prof {
+    Handle* h;
+    bool on;
+    cudaStream_t s;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
+    template <class F> cudaError_t run(int cls, F&& f) {
+        if (!on) return f();
+        cudaEvent_t a, b;
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+        cudaEventRecord(a, s);
+        cudaError_t e = f();
+        cudaEventRecord(b, s);
+        ev.push_back({cls, {a, b}});
+        return e;
+    }
+    void collect() {
+        if (!on) return;
+        for (int k = 0; k < 3; ++k) { h->prof_ms[k] = 0; h->prof_n[k] = 0; }
+        for (auto& p : ev) {
+            float ms = 0;
+            cudaEventSynchronize(p.second.second);
+            cudaEventElapsedTime(&ms, p.second.first, p.second.second);
+            h->prof_ms[p.first] += ms;
+            h->prof_n[p.first] += 1;
+            cudaEventDestroy(p.second.first);
+            cudaEventDestroy(p.second.second);
+        }
+        ev.clear();
+    }
+};
+
+constexpr unsigned long long NO_ERROR = ~0ull;
+
+inline void set_error(pe3d_error* err, int32_t range_index, int32_t sweep, const char* fmt, const char* what) {
+    if (!err) return;
+    std::memset(err, 0, sizeof(*err));
+    err->range_index = range_index;
+    err->sweep = sweep;
+    std::snprintf(err->message, sizeof(err->message), fmt, what);
+}
+
+inline int cuda_fail(pe3d_error* err, cudaError_t e, const char* where) {
+    if (err) {
+        std::memset(err, 0, sizeof(*err));
+        err->range_index = -1;
+        std::snprintf(err->message, sizeof(err->message), "%s: %s", where, cudaGetErrorString(e));
+    }
+    return PE3D_CUDA_ERROR;
+}
+
+inline int bad_arg(pe3d_error* err, const char* what) {
+    set_error(err, -1, 0, "%s", what);
+    return PE3D_BAD_ARGUMENT;
+}
+
+#define CK(call, where)                                   \
+    do {                                                  \
+        cudaError_t e_ = (call);                          \
+        if (e_ != cudaSuccess) return cuda_fail(err, e_, where); \
+    } while (0)
+
+inline int check_grid(const pe3d_grid* g, const pe3d_coeffs* c, pe3d_error* err) {
+    if (!g || !c) return bad_arg(err, "null grid or coefficients");
+    if (g->n_freq < 1) return bad_arg(err, "n_freq >= 1");
+    if (g->n_theta < 3 || g->n_depth < 3) return bad_arg(err, "n_theta >= 3 and n_depth >= 3");
+    if (g->n_theta > 4096) return bad_arg(err, "n_theta <= 4096 (ring kernels)");
+    if (g->n_depth > 4096) return bad_arg(err, "n_depth <= 4096 (depth kernels)");
+    if (g->n_steps < 0) return bad_arg(err, "n_steps >= 0");
+    if (g->output_stride < 1) return bad_arg(err, "output_stride >= 1");
+    if (g->topology != PE3D_PERIODIC && g->topology != PE3D_SECTOR) return bad_arg(err, "topology");
+    if (!(g->delta_r > 0) || !(g->delta_theta > 0) || !(g->delta_z > 0)) return bad_arg(err, "spacings > 0");
+    if (!(g->r_input > 0)) return bad_arg(err, "r_input > 0");
+    for (int f = 0; f < g->n_freq; ++f)
+        if (!(c[f].k0 > 0)) return bad_arg(err, "k0 > 0");
+    return PE3D_OK;
+}
+
+inline std::vector<pe3d::FreqDev> freq_table(const pe3d_grid* g, const pe3d_coeffs* c) {
+    std::vector<pe3d::FreqDev> t(g->n_freq);
+    for (int f = 0; f < g->n_freq; ++f) {
+        pe3d::FreqDev& d = t[f];
+        d.k0 = c[f].k0;
+        const double kz = c[f].k0 * g->delta_z;
+        d.s_z = 1.0 / (kz * kz);                                    // ref operators.py:94
+        d.cx_lhs = pe3d::mk(c[f].cx_lhs.re, c[f].cx_lhs.im);
+        d.cx_rhs = pe3d::mk(c[f].cx_rhs.re, c[f].cx_rhs.im);
+        d.cy_lhs = pe3d::mk(c[f].cy_lhs.re, c[f].cy_lhs.im);
+        d.cy_rhs = pe3d::mk(c[f].cy_rhs.re, c[f].cy_rhs.im);
+        d.off_z = pe3d::mk(d.cx_lhs.re * d.s_z, d.cx_lhs.im * d.s_z);  // complex(coeff * s)
+    }
+    return t;
+}
+
+// |w(r)| exactly as the reference computes it (environment.py:287-294):
+// abs(complex(cos(k0 r), sin(k0 r)) / sqrt(r))
+inline double hankel_abs_host(double k0, double r) {
+    const double s = std::sqrt(r);
+    return std::hypot(std::cos(k0 * r) / s, std::sin(k0 * r) / s);
+}
+
+inline bool needs_serial(const pe3d_grid* g, const std::vector<pe3d::FreqDev>& fd) {
+    if (g->flags & PE3D_FLAG_SERIAL) return true;
+    for (const auto& d : fd)
+        if (d.off_z.re == 0.0 && d.off_z.im == 0.0) return true;
+    return false;
+}
+
+inline int decode_error(Handle* h, cudaStream_t stream, pe3d_error* err) {
+    pe3d::DevError de;
+    CK(cudaMemcpyAsync(&de, h->err.ptr, sizeof(de), cudaMemcpyDeviceToHost, stream), "error readback");
+    CK(cudaStreamSynchronize(stream), "march");
+    if (de.key == NO_ERROR) return PE3D_OK;
+    if (err) {
+        std::memset(err, 0, sizeof(*err));
+        err->range_index = int32_t(de.key >> 40);
+        err->sweep = int32_t((de.key >> 39) & 1);
+        err->frequency = int32_t((de.key >> 24) & 0x7fff);
+        err->member = int32_t(de.key & 0xffffff);
+        err->pivot = de.pivot;
+        err->rank1 = de.rank1;
+        std::snprintf(err->message, sizeof(err->message), "singular system: pivot %d, batch member %d", de.pivot,
+                      err->member);
+    }
+    return PE3D_SINGULAR;
+}
+
+}  // namespace pe3d_host
