@@ -481,10 +481,11 @@ k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ 
         PHASE(1);
         mbar_wait(&bars[slot], parity);
         PHASE(2);
-        const int sw = lane & 7;
+        // this lane's 128-B line of the swizzled stage: chunk i at line ^ (i << 4)
+        const unsigned line = smem_addr(cur + lane * 8) + ((lane & 7) << 4);
         cplx x[RPT];
 #pragma unroll
-        for (int i = 0; i < RPT; ++i) x[i] = cur[lane * 8 + (i ^ sw)];
+        for (int i = 0; i < RPT; ++i) x[i] = lds_at(line ^ unsigned(i << 4));
 
         cplx up = shfl_up(x[RPT - 1], 1), dn = shfl_down(x[0], 1);
         if (lane == 31) sUp[warp] = x[RPT - 1];
@@ -518,7 +519,13 @@ k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ 
         __syncthreads();
         PHASE(6);
         cplx C = czero();
-        for (int w = 0; w < warp; ++w) C = cfma(spw[w], C, sY[w]);
+        if (NTH) {                                  // compile-time warp count: predicated, unrolled
+#pragma unroll
+            for (int w = 0; w < (NTH ? NTH : 32) / 32; ++w)
+                if (w < warp) C = cfma(spw[w], C, sY[w]);
+        } else {
+            for (int w = 0; w < warp; ++w) C = cfma(spw[w], C, sY[w]);
+        }
         cplx y = shfl_up(cfma(pincf[t], C, Y), 1);
         if (lane == 0) y = C;
 #pragma unroll
@@ -534,7 +541,13 @@ k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ 
         __syncthreads();
         PHASE(8);
         cplx D = czero();
-        for (int w = nwarps - 1; w > warp; --w) D = cfma(spw[w], D, sX[w]);
+        if (NTH) {
+#pragma unroll
+            for (int w = (NTH ? NTH : 32) / 32 - 1; w >= 0; --w)
+                if (w > warp) D = cfma(spw[w], D, sX[w]);
+        } else {
+            for (int w = nwarps - 1; w > warp; --w) D = cfma(spw[w], D, sX[w]);
+        }
         cplx xv = shfl_down(cfma(pincb[t], D, X), 1);
         if (lane == 31) xv = D;
 #pragma unroll
@@ -543,7 +556,7 @@ k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ 
         PHASE(9);
         // ---- solved column back through the stage, one TMA store per warp
 #pragma unroll
-        for (int i = 0; i < RPT; ++i) cur[lane * 8 + (i ^ sw)] = b[i];
+        for (int i = 0; i < RPT; ++i) sts_at(line ^ unsigned(i << 4), b[i]);
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {

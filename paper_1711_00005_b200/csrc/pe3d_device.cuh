@@ -175,6 +175,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
         "r"(parity)
         : "memory");
 }
+// Shared-memory complex load/store at a 32-bit shared address (the swizzled
+// stage addresses are formed as line_base ^ (i << 4): one LOP3 per element).
+__device__ __forceinline__ cplx lds_at(unsigned a) {
+    cplx v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.re), "=d"(v.im) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts_at(unsigned a, cplx v) {
+    asm volatile("st.shared.v2.f64 [%0], {%1, %2};\n" ::"r"(a), "d"(v.re), "d"(v.im) : "memory");
+}
+
 // Wait for a phase completed by st.async writes of other CTAs of the cluster
 // (distributed shared memory).  The writes land in this CTA's shared memory
 // and are counted on this CTA's mbarrier as transaction bytes, exactly like a
