@@ -256,6 +256,13 @@ PE3D_API int pe3d_march_slab_p2p(void* handle, const pe3d_grid* grid, const pe3d
  */
 PE3D_API int pe3d_profile_last(void* handle, double* ms, int32_t* launches);
 
+/*
+ * pe3d_last_launches -- number of kernels the last pe3d_march_device /
+ * pe3d_march_host call on this handle launched, graph replays included
+ * (measurement only).
+ */
+PE3D_API int pe3d_last_launches(void* handle, int64_t* launches);
+
 #ifdef __cplusplus
 }
 #endif

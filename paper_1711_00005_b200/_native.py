@@ -29,7 +29,7 @@ EXPORTED_SYMBOLS = (
     "pe3d_abi_version", "pe3d_device_count", "pe3d_handle_create", "pe3d_handle_destroy",
     "pe3d_sample_count", "pe3d_march_host", "pe3d_march_device", "pe3d_step_general_host",
     "pe3d_solve_batch_host", "pe3d_profile_last", "pe3d_march_medium_host", "pe3d_slab_unique_id",
-    "pe3d_march_slab", "pe3d_slab_p2p_export", "pe3d_march_slab_p2p",
+    "pe3d_march_slab", "pe3d_slab_p2p_export", "pe3d_march_slab_p2p", "pe3d_last_launches",
 )
 SLAB_IPC_BYTES = 192
 
@@ -88,6 +88,7 @@ _SIGNATURES = {
     "pe3d_solve_batch_host": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, Strided, Strided, Strided,
                                         Strided, _P, C.POINTER(ErrorRecord)]),
     "pe3d_profile_last": (C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_int32)]),
+    "pe3d_last_launches": (C.c_int, [_P, C.POINTER(C.c_int64)]),
     "pe3d_march_medium_host": (C.c_int, [_P, C.POINTER(GridParams), C.POINTER(Coeffs), C.POINTER(Medium),
                                          _P, _P, _P, _P, _P, C.POINTER(ErrorRecord)]),
     "pe3d_slab_unique_id": (C.c_int, [_P, C.c_int32]),

@@ -480,10 +480,13 @@ static int march_device_impl(void* handle, const pe3d_grid* g, const pe3d_coeffs
             h->graph_exec = nullptr;
             h->graph_key.clear();
             cudaGraph_t graph = nullptr;
+            const int64_t before = prof.launches;
             CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal), "capture");
             cudaError_t e = enqueue_steps(h, g, p, local, d_tl, reinterpret_cast<cplx*>(d_snapshots),
                                           reinterpret_cast<cplx*>(d_u_final), d_clamped, h->w_abs.as<double>(), prof,
                                           sink);
+            h->graph_launches = prof.launches - before;
+            prof.launches = before;
             cudaError_t e2 = cudaStreamEndCapture(stream, &graph);
             if (e != cudaSuccess) { if (graph) cudaGraphDestroy(graph); return cuda_fail(err, e, "enqueue"); }
             if (e2 != cudaSuccess) return cuda_fail(err, e2, "end capture");
@@ -493,6 +496,7 @@ static int march_device_impl(void* handle, const pe3d_grid* g, const pe3d_coeffs
             h->graph_key = key;
         }
         CK(cudaGraphLaunch(h->graph_exec, stream), "graph launch");
+        prof.launches += h->graph_launches;
     } else {
         CK(enqueue_steps(h, g, p, local, d_tl, reinterpret_cast<cplx*>(d_snapshots),
                          reinterpret_cast<cplx*>(d_u_final), d_clamped, h->w_abs.as<double>(), prof, sink),
@@ -500,6 +504,7 @@ static int march_device_impl(void* handle, const pe3d_grid* g, const pe3d_coeffs
     }
     CK(cudaGetLastError(), "launch");
     prof.collect();
+    h->last_launches = prof.launches;
     return decode_error(h, stream, err);
 }
 
@@ -939,6 +944,13 @@ int pe3d_march_medium_host(void* handle, const pe3d_grid* g, const pe3d_coeffs* 
 
 // NCCL is loaded lazily (only the slab march needs it), so the library has
 // no link-time dependency on a particular libnccl.
+int pe3d_last_launches(void* handle, int64_t* launches) {
+    Handle* h = static_cast<Handle*>(handle);
+    if (!h || !launches) return PE3D_BAD_ARGUMENT;
+    *launches = h->last_launches;
+    return PE3D_OK;
+}
+
 int pe3d_profile_last(void* handle, double* ms, int32_t* launches) {
     Handle* h = static_cast<Handle*>(handle);
     if (!h) return PE3D_BAD_ARGUMENT;

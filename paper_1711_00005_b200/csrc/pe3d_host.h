@@ -61,6 +61,8 @@ struct Handle {
     // PE3D_FLAG_PROFILE accounting
     double prof_ms[3] = {0, 0, 0};
     int32_t prof_n[3] = {0, 0, 0};
+    // kernels launched by the last march (graph replays included)
+    int64_t graph_launches = 0, last_launches = 0;
     // concurrent step-loop chains over disjoint frequency groups
     static constexpr int MAX_CHAINS = 4;
     cudaStream_t chain_stream[MAX_CHAINS] = {};
@@ -77,7 +79,9 @@ struct Prof {
     bool on;
     cudaStream_t s;
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
+    int64_t launches = 0;                               // kernels enqueued through run()
     template <class F> cudaError_t run(int cls, F&& f) {
+        ++launches;
         if (!on) return f();
         cudaEvent_t a, b;
         cudaEventCreate(&a);
