@@ -1,5 +1,6 @@
 // pe3d_internal.h -- launch interface between the C ABI (pe3d_abi.cu) and
-// the kernels (pe3d_kernels.cu).  Not part of the public ABI.
+// the kernels (pe3d_depth.cu, pe3d_ring.cu, pe3d_serial.cu, pe3d_medium.cu,
+// pe3d_slab.cu).  Not part of the public ABI.
 #pragma once
 
 #include <cuda_runtime.h>

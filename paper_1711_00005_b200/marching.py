@@ -2,17 +2,20 @@
 
 ``run_frequency`` (ref :144-193) and ``range_step`` (ref :93-136) keep the
 reference's signatures, state objects, results and exceptions; the
-arithmetic of every step runs in the sm_100a kernels of
-``csrc/pe3d_kernels.cu`` through the C ABI.  ``march_frequencies`` is the
-batched entry point: many frequencies of one config in one device march
-(the body of ``frequency_farm``).
+arithmetic of every step runs in the sm_100a kernels of ``csrc/`` through
+the C ABI (``libpe3d_b200.so``).  ``march_frequencies`` is the batched
+entry point: many frequencies of one config in one device march (the body
+of ``frequency_farm``).
 
-Range-independent media (every reference ``Environment``, and extended
-media without bathymetry slope or perturbation) use the device-resident
-march: the depth matrix is factored once per frequency on the device and
-the whole step loop is one CUDA graph.  Media that vary with range or
-azimuth are stepped one range step per ABI call, with the per-point local
-term of both ranges handed to the thread-per-column depth kernel.
+* Range-independent media (every reference ``Environment``, and extended
+  media without bathymetry slope or perturbation): ``pe3d_march_host``,
+  the depth matrix factored once per frequency on the device and the step
+  loop one CUDA graph (concurrent frequency chains).
+* Range/azimuth-dependent ``LayeredMedium`` (cfg3): ``pe3d_march_medium_host``,
+  the medium regenerated on the device every step.
+* Any other range-dependent environment: one range step per ABI call
+  (``pe3d_step_general_host``) with the per-point local term of both ranges
+  computed on the host, as the reference does.
 """
 
 from __future__ import annotations

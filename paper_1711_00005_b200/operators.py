@@ -5,7 +5,7 @@
 
 with cx = 1/4 -/+ d/4 and cy = -/+ d/4.  The matrix-free operators and
 the per-system assembly of the reference (``operators.py:90-272``) live
-inside the CUDA kernels (``csrc/pe3d_kernels.cu``) and, as the checker,
+inside the CUDA kernels (``csrc/pe3d_depth.cu``, ``csrc/pe3d_ring.cu``) and, as the checker,
 in ``oracle/pe3d_oracle.py``.
 """
 
