@@ -30,14 +30,22 @@
 namespace pe3d {
 
 #ifdef PE3D_PHASE_TIMING
-// Phase timing of k_depth_scan (profiling builds only): per CTA, thread 0
-// accumulates clock64 deltas of each phase into g_phase[blockIdx][phase].
+// Phase timing of the depth sweeps (profiling builds only): per CTA, thread 0
+// accumulates clock64 deltas of each phase in shared memory (no global
+// round trip inside the timed phases) and adds them to g_phase[blockIdx][phase]
+// at the end.
 __device__ unsigned long long g_phase[4096][16];
-#define PHASE_BEGIN long long _ph_t = clock64();
-#define PHASE(k) do { if (threadIdx.x == 0) { long long _n = clock64(); g_phase[blockIdx.x][k] += _n - _ph_t; _ph_t = _n; } } while (0)
+#define PHASE_BEGIN                                                         \
+    __shared__ unsigned long long _ph_acc[16];                              \
+    if (threadIdx.x == 0)                                                   \
+        for (int _k = 0; _k < 16; ++_k) _ph_acc[_k] = 0;                    \
+    long long _ph_t = clock64();
+#define PHASE(k) do { if (threadIdx.x == 0) { long long _n = clock64(); _ph_acc[k] += _n - _ph_t; _ph_t = _n; } } while (0)
+#define PHASE_END do { if (threadIdx.x == 0) for (int _k = 0; _k < 16; ++_k) g_phase[blockIdx.x][_k] += _ph_acc[_k]; } while (0)
 #else
 #define PHASE_BEGIN
 #define PHASE(k) do {} while (0)
+#define PHASE_END do {} while (0)
 #endif
 
 // One thread per frequency: Thomas pivots of the depth matrix with the
@@ -363,6 +371,7 @@ k_depth_scan(const cplx* __restrict__ src, cplx* __restrict__ dst, const cplx* _
         slot = (slot + 1 == STAGES) ? 0 : slot + 1;
     }
     cp_async_wait<0>();
+    PHASE_END;
 }
 
 // Output tensor maps of the TMA depth sweeps: tiles [q*nzt, (q+1)*nzt) of
@@ -423,6 +432,25 @@ k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ 
     }
     __syncthreads();
 
+    int f = int(g0 / n_theta), col = int(g0 - int64_t(f) * n_theta);
+    int cur_f = -1;
+    cplx A[RPT], M[RPT], beta = czero(), P0f = czero(), P0b = czero();
+    // A frequency's tables and constants are loaded in ONE round of
+    // independent loads ahead of any arithmetic on them (under full HBM load
+    // each dependent round costs microseconds); the first frequency's round
+    // is issued before the column prefetches so it does not queue behind them.
+    cplx lc[RPT];
+    FreqDev fd;
+    auto load_freq = [&](int ff) {
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+            lc[i] = active ? ldc(loc_tab + int64_t(ff) * nz8 + RPT * t + i) : czero();
+            M[i] = active ? ldc(mul_tab + int64_t(ff) * nz8 + RPT * t + i) : czero();
+        }
+        fd = fdev[ff];
+    };
+    load_freq(f);
+
     int pf = int(g0 / n_theta), pc = int(g0 - int64_t(pf) * n_theta);
     if (lane == 0) {
 #pragma unroll
@@ -435,46 +463,46 @@ k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ 
         }
     }
 
-    int f = int(g0 / n_theta), col = int(g0 - int64_t(f) * n_theta);
-    int cur_f = -1;
-    cplx A[RPT], M[RPT], beta = czero(), P0f = czero(), P0b = czero();
+    auto setup_freq = [&]() {
+        const cplx kappa = crecip(cneg(fd.off_z));
+        beta = cmul(kappa, crmul(fd.s_z, fd.cx_rhs));
+        cplx P = cone();
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+            A[i] = csub(cmul(kappa, cadd(cone(), cmul(fd.cx_rhs, lc[i]))), cadd(beta, beta));
+            P = cmul(M[i], P);
+        }
+        if (!active) P = cone();
+        __syncthreads();
+        P0f = lane >= 1 ? P : czero();
+        P0b = lane + 1 < 32 ? P : czero();
+        cplx Pf = P, Pb = P;
+#pragma unroll
+        for (int d = 0; d < 5; ++d) {
+            const int o = 1 << d;
+            if (d > 0) {
+                mf[(d - 1) * nthreads + t] = lane >= o ? Pf : czero();
+                mb[(d - 1) * nthreads + t] = lane + o < 32 ? Pb : czero();
+            }
+            const cplx pu = shfl_up(Pf, o), pd = shfl_down(Pb, o);
+            if (lane >= o) Pf = cmul(Pf, pu);
+            if (lane + o < 32) Pb = cmul(Pb, pd);
+        }
+        pincf[t] = Pf;
+        pincb[t] = Pb;
+        if (lane == 31) spw[warp] = Pf;
+        __syncthreads();
+        cur_f = f;
+    };
+    setup_freq();           // first frequency outside the loop: lc and fd are not loop-carried
+
     int slot = 0;
     unsigned parity = 0;
     PHASE_BEGIN
     for (int it = 0; it < n_cols; ++it) {
         if (f != cur_f) {
-            const FreqDev fd = fdev[f];
-            const cplx kappa = crecip(cneg(fd.off_z));
-            beta = cmul(kappa, crmul(fd.s_z, fd.cx_rhs));
-            cplx P = cone();
-#pragma unroll
-            for (int i = 0; i < RPT; ++i) {
-                const cplx lc = active ? ldc(loc_tab + int64_t(f) * nz8 + RPT * t + i) : czero();
-                M[i] = active ? ldc(mul_tab + int64_t(f) * nz8 + RPT * t + i) : czero();
-                A[i] = csub(cmul(kappa, cadd(cone(), cmul(fd.cx_rhs, lc))), cadd(beta, beta));
-                P = cmul(M[i], P);
-            }
-            if (!active) P = cone();
-            __syncthreads();
-            P0f = lane >= 1 ? P : czero();
-            P0b = lane + 1 < 32 ? P : czero();
-            cplx Pf = P, Pb = P;
-#pragma unroll
-            for (int d = 0; d < 5; ++d) {
-                const int o = 1 << d;
-                if (d > 0) {
-                    mf[(d - 1) * nthreads + t] = lane >= o ? Pf : czero();
-                    mb[(d - 1) * nthreads + t] = lane + o < 32 ? Pb : czero();
-                }
-                const cplx pu = shfl_up(Pf, o), pd = shfl_down(Pb, o);
-                if (lane >= o) Pf = cmul(Pf, pu);
-                if (lane + o < 32) Pb = cmul(Pb, pd);
-            }
-            pincf[t] = Pf;
-            pincb[t] = Pb;
-            if (lane == 31) spw[warp] = Pf;
-            __syncthreads();
-            cur_f = f;
+            load_freq(f);
+            setup_freq();
             PHASE(0);
         }
         cplx* cur = stage + slot * 256;
@@ -577,6 +605,7 @@ k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ 
     }
     if (lane == 0) bulk_wait_read<0>();
     __syncwarp();
+    PHASE_END;
 }
 
 // Long columns (cfg5: 4096 rows): a thread-block cluster of CL CTAs per

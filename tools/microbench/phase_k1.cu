@@ -1,5 +1,5 @@
-// Phase-timing driver for k_depth_scan (built with -DPE3D_PHASE_TIMING):
-// marches cfg4-shaped data for a few steps through the C ABI and prints the
+// Phase-timing driver for the cfg4 depth sweep (k_depth_tma) (built with -DPE3D_PHASE_TIMING):
+// marches cfg4-shaped data (F frequencies, argv[1], default 64) for a few steps through the C ABI and prints the
 // mean cycles per column of each phase for CTA-thread 0.
 #include <cstdio>
 #include <cstdlib>
@@ -8,7 +8,7 @@
 #include "../../include/pe3d_b200.h"
 namespace pe3d { extern __device__ unsigned long long g_phase[4096][16]; }
 int main(int argc, char** argv) {
-    const int F = 64, NT = 256, NZ = 1024, steps = 4;
+    const int F = argc > 1 ? atoi(argv[1]) : 64, NT = 256, NZ = 1024, steps = 4;
     pe3d_grid g{F, NT, NZ, PE3D_PERIODIC, steps, steps, 0, PE3D_FLAG_NO_GRAPH, 1.0, 6.283185307179586 / NT, 0.25, 1.0, 1.0};
     std::vector<pe3d_coeffs> co(F);
     for (int f = 0; f < F; ++f) {
@@ -27,9 +27,10 @@ int main(int argc, char** argv) {
     int rc = pe3d_march_device(h, &g, co.data(), dl, du, df, dtl, nullptr, (int64_t*)dc, nullptr, &err);
     std::vector<unsigned long long> ph(4096 * 16);
     cudaMemcpyFromSymbol(ph.data(), pe3d::g_phase, ph.size() * 8);
-    const char* names[11] = {"freq prologue", "issue prefetch", "wait stage", "load+halo publish", "BAR halo",
-                             "rhs+fwd local+scan", "BAR fwd", "carry+rerun+bwd local+scan", "BAR bwd",
-                             "carry+rerun", "stage out+STG"};
+    // phase k = time from PHASE(k-1) (or the previous column's PHASE(10)) to PHASE(k)
+    const char* names[11] = {"freq prologue", "loop/freq check", "wait stage (mbarrier)", "load+halo publish",
+                             "BAR halo", "rhs+fwd local+scan", "BAR fwd", "carry+rerun+bwd local+scan", "BAR bwd",
+                             "carry+rerun", "stage out+TMA store+next load"};
     double cols = double(F) * NT * steps;
     int ctas = 0;
     for (int b = 0; b < 4096; ++b) if (ph[b * 16 + 2]) ++ctas;
