@@ -449,6 +449,7 @@ k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ 
         }
         fd = fdev[ff];
     };
+    PHASE_BEGIN
     load_freq(f);
 
     int pf = int(g0 / n_theta), pc = int(g0 - int64_t(pf) * n_theta);
@@ -495,10 +496,10 @@ k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ 
         cur_f = f;
     };
     setup_freq();           // first frequency outside the loop: lc and fd are not loop-carried
+    PHASE(11);
 
     int slot = 0;
     unsigned parity = 0;
-    PHASE_BEGIN
     for (int it = 0; it < n_cols; ++it) {
         if (f != cur_f) {
             load_freq(f);
@@ -605,6 +606,7 @@ k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ 
     }
     if (lane == 0) bulk_wait_read<0>();
     __syncwarp();
+    PHASE(12);
     PHASE_END;
 }
 

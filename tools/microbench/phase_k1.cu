@@ -44,5 +44,10 @@ int main(int argc, char** argv) {
         printf("  %-30s %8.0f cycles/column\n", names[k], per_col);
     }
     printf("  %-30s %8.0f cycles/column\n", "TOTAL (excl. prologue)", total);
+    const char* once[2] = {"first setup (per CTA)", "store drain (per CTA)"};
+    for (int k = 11; k < 13; ++k) {
+        double s = 0; for (int b = 0; b < 4096; ++b) s += ph[b * 16 + k];
+        printf("  %-30s %8.0f cycles per CTA per launch\n", once[k - 11], s / ctas / steps);
+    }
     return 0;
 }
