@@ -132,6 +132,7 @@ cudaError_t enqueue_group(Handle* h, const pe3d_grid* g, const MarchPlan& p, int
     cg.fdev = c.fdev + f0;
     cg.loc_tab = c.loc_tab + int64_t(f0) * c.n_tiles * 8;
     cg.mul_tab = c.mul_tab + int64_t(f0) * c.n_tiles * 8;
+    if (c.k1_tab) cg.k1_tab = c.k1_tab + int64_t(f0) * pe3d::k1_stride((c.n_tiles + 31) / 32 * 32);
     cg.stream = st;
     cplx* A = h->field_a.as<cplx>() + f0 * fe;
     cplx* B = h->field_b.as<cplx>() + f0 * fe;
@@ -336,7 +337,7 @@ int pe3d_handle_destroy(void* handle) {
     Handle* h = static_cast<Handle*>(handle);
     if (!h) return PE3D_OK;
     cudaSetDevice(h->device);
-    for (DevBuf* b : {&h->field_a, &h->field_b, &h->field_c, &h->loc_tab, &h->mul_tab, &h->fdev, &h->w_abs, &h->err,
+    for (DevBuf* b : {&h->field_a, &h->field_b, &h->field_c, &h->loc_tab, &h->mul_tab, &h->k1_tab, &h->fdev, &h->w_abs, &h->err,
                       &h->az_cp, &h->az_inv, &h->az_q, &h->az_ring, &h->fail_row, &h->fail_mag, &h->ring_tab, &h->h_local,
                       &h->h_local2, &h->h_u0, &h->h_final, &h->h_tl, &h->h_snap, &h->h_clamped, &h->sb_in, &h->sb_x,
                       &h->sb_cp, &h->sb_inv, &h->sb_y, &h->sb_q, &h->med_prof, &h->med_lat, &h->med_local, &h->slab_flags})
@@ -390,6 +391,9 @@ static int march_device_impl(void* handle, const pe3d_grid* g, const pe3d_coeffs
     CK(h->field_b.ensure(field * sizeof(cplx)), "alloc field");
     CK(h->loc_tab.ensure(int64_t(F) * n_tiles * 8 * sizeof(cplx)), "alloc tables");
     CK(h->mul_tab.ensure(int64_t(F) * n_tiles * 8 * sizeof(cplx)), "alloc tables");
+    const bool k1_table = n_tiles <= pe3d::K1_TAB_MAX_TILES;
+    if (k1_table)
+        CK(h->k1_tab.ensure(int64_t(F) * pe3d::k1_stride((n_tiles + 31) / 32 * 32) * sizeof(cplx)), "alloc tables");
     CK(h->fdev.ensure(F * sizeof(pe3d::FreqDev)), "alloc coeffs");
     CK(h->w_abs.ensure(int64_t(S) * F * sizeof(double)), "alloc w");
     CK(h->err.ensure(sizeof(pe3d::DevError)), "alloc err");
@@ -424,6 +428,7 @@ static int march_device_impl(void* handle, const pe3d_grid* g, const pe3d_coeffs
     c.fdev = h->fdev.as<pe3d::FreqDev>();
     c.loc_tab = h->loc_tab.as<cplx>();
     c.mul_tab = h->mul_tab.as<cplx>();
+    c.k1_tab = k1_table ? h->k1_tab.as<cplx>() : nullptr;
     c.err = h->err.as<pe3d::DevError>();
     c.stream = stream;
 
@@ -469,7 +474,7 @@ static int march_device_impl(void* handle, const pe3d_grid* g, const pe3d_coeffs
         add(coeffs, sizeof(pe3d_coeffs) * F);
         add(ptrs, sizeof(ptrs));
         add(&stream, sizeof(stream));
-        const void* tabs[5] = {h->w_abs.ptr, h->fdev.ptr, h->loc_tab.ptr, h->err.ptr, h->ring_tab.ptr};
+        const void* tabs[6] = {h->w_abs.ptr, h->fdev.ptr, h->loc_tab.ptr, h->err.ptr, h->ring_tab.ptr, h->k1_tab.ptr};
         add(tabs, sizeof(tabs));
         const int chains = step_chains(p.ctx, false);
         add(&chains, sizeof(chains));

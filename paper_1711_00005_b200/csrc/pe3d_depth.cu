@@ -391,11 +391,12 @@ struct DepthDst {
 // last tile), completion on a per-warp mbarrier, and one TMA bulk store of
 // the solved column from the same stage.  The warps issue no per-line
 // copies at all; a 3-deep per-warp stage ring keeps two columns in flight.
-template <int STAGES, int MINB, int MAXT, int NTH = 0>
+template <int STAGES, int MINB, int MAXT, int NTH = 0, bool TAB = false>
 __global__ void __launch_bounds__(MAXT, MINB)
 k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ DepthDst tm_dst,
             const cplx* __restrict__ loc_tab, const cplx* __restrict__ mul_tab, const FreqDev* __restrict__ fdev,
-            int n_theta, int n_tiles, int64_t total_cols, int cols_per_cta, int sector) {
+            const cplx* __restrict__ k1_tab, int n_theta, int n_tiles, int64_t total_cols, int cols_per_cta,
+            int sector) {
     constexpr int RPT = 8;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     const int nthreads = NTH ? NTH : int(blockDim.x);   // compile-time when NTH: constant table offsets
@@ -415,6 +416,7 @@ k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ 
     cplx* sUp = sX + nwarps;
     cplx* sDn = sUp + nwarps;
     uint64_t* bars = reinterpret_cast<uint64_t*>(sDn + nwarps) + warp * STAGES;
+    uint64_t* tbar = reinterpret_cast<uint64_t*>(sDn + nwarps) + nwarps * STAGES;   // frequency-table copy
 
     const int64_t g0 = int64_t(blockIdx.x) * cols_per_cta;
     const int64_t g1 = g0 + cols_per_cta < total_cols ? g0 + cols_per_cta : total_cols;
@@ -428,6 +430,7 @@ k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ 
     if (lane == 0) {
 #pragma unroll
         for (int k = 0; k < STAGES; ++k) mbar_init(&bars[k], 1);
+        if (t == 0) mbar_init(tbar, 1);
         mbar_fence_init();
     }
     __syncthreads();
@@ -441,13 +444,34 @@ k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ 
     // is issued before the column prefetches so it does not queue behind them.
     cplx lc[RPT];
     FreqDev fd;
+    // With the per-march table (k_depth_setup) a frequency is one bulk copy of
+    // its shared-memory image plus register loads, no arithmetic.
+    const int img = k1_img(nthreads), kstride = k1_stride(nthreads);
+    unsigned tpar = 0;
     auto load_freq = [&](int ff) {
+        if constexpr (TAB) {
+            const cplx* kt = k1_tab + int64_t(ff) * kstride;
+            if (t == 0) {
+                const unsigned bytes = unsigned(10 * nthreads + nwarps) * unsigned(sizeof(cplx));
+                mbar_expect_tx(tbar, bytes);
+                bulk_load(mf, kt, bytes, tbar);
+            }
 #pragma unroll
-        for (int i = 0; i < RPT; ++i) {
-            lc[i] = active ? ldc(loc_tab + int64_t(ff) * nz8 + RPT * t + i) : czero();
-            M[i] = active ? ldc(mul_tab + int64_t(ff) * nz8 + RPT * t + i) : czero();
+            for (int i = 0; i < RPT; ++i) {
+                A[i] = ldc(kt + img + RPT * t + i);
+                M[i] = active ? ldc(mul_tab + int64_t(ff) * nz8 + RPT * t + i) : czero();
+            }
+            P0f = ldc(kt + img + 8 * nthreads + t);
+            P0b = ldc(kt + img + 9 * nthreads + t);
+            beta = ldc(kt + img + 10 * nthreads);
+        } else {
+#pragma unroll
+            for (int i = 0; i < RPT; ++i) {
+                lc[i] = active ? ldc(loc_tab + int64_t(ff) * nz8 + RPT * t + i) : czero();
+                M[i] = active ? ldc(mul_tab + int64_t(ff) * nz8 + RPT * t + i) : czero();
+            }
+            fd = fdev[ff];
         }
-        fd = fdev[ff];
     };
     PHASE_BEGIN
     load_freq(f);
@@ -465,6 +489,12 @@ k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ 
     }
 
     auto setup_freq = [&]() {
+        if constexpr (TAB) {
+            mbar_wait(tbar, tpar);
+            tpar ^= 1u;
+            cur_f = f;
+            return;
+        }
         const cplx kappa = crecip(cneg(fd.off_z));
         beta = cmul(kappa, crmul(fd.s_z, fd.cx_rhs));
         cplx P = cone();
@@ -502,6 +532,7 @@ k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ 
     unsigned parity = 0;
     for (int it = 0; it < n_cols; ++it) {
         if (f != cur_f) {
+            if constexpr (TAB) __syncthreads();     // every warp is done with the old shared tables
             load_freq(f);
             setup_freq();
             PHASE(0);
@@ -608,6 +639,57 @@ k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ 
     __syncwarp();
     PHASE(12);
     PHASE_END;
+}
+
+// Per-frequency setup of k_depth_tma, once per march (one CTA of nt threads
+// per frequency): exactly the arithmetic k_depth_tma otherwise performs at
+// every frequency it meets -- folded RHS coefficients, the column-independent
+// Kogge-Stone multipliers and warp products -- written as the k1_tab record
+// (pe3d_internal.h), so the sweep's frequency setup is loads only.
+__global__ void k_depth_setup(const cplx* __restrict__ loc_tab, const cplx* __restrict__ mul_tab,
+                              const FreqDev* __restrict__ fdev, int n_tiles, cplx* __restrict__ k1_tab) {
+    constexpr int RPT = 8;
+    const int f = blockIdx.x;
+    const int nthreads = blockDim.x, t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int nz8 = n_tiles * 8;
+    const bool active = t * RPT < nz8;
+    cplx* kt = k1_tab + int64_t(f) * k1_stride(nthreads);
+    const int img = k1_img(nthreads);
+    cplx* mf = kt;
+    cplx* mb = mf + 4 * nthreads;
+    cplx* pincf = mb + 4 * nthreads;
+    cplx* pincb = pincf + nthreads;
+    cplx* spw = pincb + nthreads;
+    const FreqDev fd = fdev[f];
+    const cplx kappa = crecip(cneg(fd.off_z));
+    const cplx beta = cmul(kappa, crmul(fd.s_z, fd.cx_rhs));
+    cplx P = cone();
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+        const cplx lc = active ? ldc(loc_tab + int64_t(f) * nz8 + RPT * t + i) : czero();
+        const cplx m = active ? ldc(mul_tab + int64_t(f) * nz8 + RPT * t + i) : czero();
+        kt[img + RPT * t + i] = csub(cmul(kappa, cadd(cone(), cmul(fd.cx_rhs, lc))), cadd(beta, beta));
+        P = cmul(m, P);
+    }
+    if (!active) P = cone();
+    kt[img + 8 * nthreads + t] = lane >= 1 ? P : czero();
+    kt[img + 9 * nthreads + t] = lane + 1 < 32 ? P : czero();
+    cplx Pf = P, Pb = P;
+#pragma unroll
+    for (int d = 0; d < 5; ++d) {
+        const int o = 1 << d;
+        if (d > 0) {
+            mf[(d - 1) * nthreads + t] = lane >= o ? Pf : czero();
+            mb[(d - 1) * nthreads + t] = lane + o < 32 ? Pb : czero();
+        }
+        const cplx pu = shfl_up(Pf, o), pd = shfl_down(Pb, o);
+        if (lane >= o) Pf = cmul(Pf, pu);
+        if (lane + o < 32) Pb = cmul(Pb, pd);
+    }
+    pincf[t] = Pf;
+    pincb[t] = Pb;
+    if (lane == 31) spw[warp] = Pf;
+    if (t == 0) kt[img + 10 * nthreads] = beta;
 }
 
 // Long columns (cfg5: 4096 rows): a thread-block cluster of CL CTAs per
@@ -931,9 +1013,12 @@ static cudaError_t launch_depth_tma_cfg(const LaunchCtx& c, const cplx* src, cpl
     const int nthreads = (c.n_tiles + 31) / 32 * 32;
     const int nwarps = nthreads / 32;
     const size_t bytes = 1024 + sizeof(cplx) * (size_t(nwarps) * STAGES * 256 + 10 * size_t(nthreads) + 5 * nwarps) +
-                         sizeof(uint64_t) * nwarps * STAGES;
+                         sizeof(uint64_t) * (nwarps * STAGES + 1);
     if (bytes > 227 * 1024) return cudaErrorNotSupported;
-    auto kern = (MAXT == 128 && nthreads == 128) ? k_depth_tma<STAGES, MINB, MAXT, 128> : k_depth_tma<STAGES, MINB, MAXT>;
+    const cplx* k1 = (c.k1_tab && c.n_tiles <= K1_TAB_MAX_TILES && nthreads == round32(c.n_tiles)) ? c.k1_tab : nullptr;
+    auto kern = (MAXT == 128 && nthreads == 128)
+                    ? (k1 ? k_depth_tma<STAGES, MINB, MAXT, 128, true> : k_depth_tma<STAGES, MINB, MAXT, 128>)
+                    : (k1 ? k_depth_tma<STAGES, MINB, MAXT, 0, true> : k_depth_tma<STAGES, MINB, MAXT>);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
     if (e != cudaSuccess) return e;
     const int64_t total = int64_t(c.n_freq) * c.n_theta;
@@ -943,8 +1028,8 @@ static cudaError_t launch_depth_tma_cfg(const LaunchCtx& c, const cplx* src, cpl
     const int64_t ctas = int64_t(c.num_sms) * per_sm;
     const int per = int((total + ctas - 1) / ctas);
     const int grid = int((total + per - 1) / per);
-    kern<<<grid, nthreads, bytes, c.stream>>>(tm_src, tm_dst, c.loc_tab, c.mul_tab, c.fdev, c.n_theta, c.n_tiles,
-                                              total, per, c.sector);
+    kern<<<grid, nthreads, bytes, c.stream>>>(tm_src, tm_dst, c.loc_tab, c.mul_tab, c.fdev, k1, c.n_theta,
+                                              c.n_tiles, total, per, c.sector);
     return cudaGetLastError();
 }
 
@@ -1030,14 +1115,21 @@ cudaError_t launch_depth_scan(const LaunchCtx& c, const cplx* src, cplx* dst) {
 // Factor tables once per march: the parallel continuant scan (pe3d_medium.cu)
 // for columns of up to 4096 rows; the reference-order single-thread
 // recurrence when PE3D_FACTOR_SERIAL is set (it was 0.46 ms per cfg4 march).
+static cudaError_t launch_depth_setup(const LaunchCtx& c) {
+    if (!c.k1_tab || c.n_tiles > K1_TAB_MAX_TILES) return cudaSuccess;
+    k_depth_setup<<<c.n_freq, round32(c.n_tiles), 0, c.stream>>>(c.loc_tab, c.mul_tab, c.fdev, c.n_tiles, c.k1_tab);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_factor_depth(const LaunchCtx& c, const cplx* local, int64_t local_fstride, int step_for_error) {
     if (!getenv("PE3D_FACTOR_SERIAL")) {
         const cudaError_t e = launch_factor_depth_scan(c, local, local_fstride, step_for_error);
-        if (e != cudaErrorNotSupported) return e;
+        if (e != cudaErrorNotSupported) return e != cudaSuccess ? e : launch_depth_setup(c);
     }
     k_factor_depth<<<c.n_freq, 1, 0, c.stream>>>(local, local_fstride, c.loc_tab, c.mul_tab, c.fdev, c.n_depth,
                                                  c.n_tiles * 8, step_for_error, c.err);
-    return cudaGetLastError();
+    const cudaError_t e = cudaGetLastError();
+    return e != cudaSuccess ? e : launch_depth_setup(c);
 }
 
 }  // namespace pe3d

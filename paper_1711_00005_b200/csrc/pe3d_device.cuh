@@ -233,6 +233,13 @@ __device__ __forceinline__ void tma_store_4d(const void* tmap, int c0, int c1, i
         "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_addr(smem_src))
         : "memory");
 }
+// Plain bulk copy global -> shared (16-B aligned, size % 16 == 0), completion counted on `bar`.
+__device__ __forceinline__ void bulk_load(void* smem_dst, const void* gsrc, unsigned bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     smem_addr(smem_dst)),
+                 "l"(gsrc), "r"(bytes), "r"(smem_addr(bar))
+                 : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() {

@@ -45,7 +45,7 @@ struct Handle {
     cudaStream_t stream = nullptr;
     // march workspace
     DevBuf field_a, field_b, field_c;     // device tiles [F][n_tiles][n_theta][8]
-    DevBuf loc_tab, mul_tab, fdev, w_abs, err;
+    DevBuf loc_tab, mul_tab, fdev, w_abs, err, k1_tab;
     DevBuf az_cp, az_inv, az_q, az_ring, fail_row, fail_mag, ring_tab;
     // staging for the host entry points
     DevBuf h_local, h_local2, h_u0, h_final, h_tl, h_snap, h_clamped;

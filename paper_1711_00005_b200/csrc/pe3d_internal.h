@@ -84,6 +84,10 @@ struct LaunchCtx {
     const FreqDev* fdev;
     cplx* loc_tab;          // [F][n_tiles*8]
     cplx* mul_tab;          // [F][n_tiles*8]
+    // Per-frequency setup of the column depth sweep (k_depth_tma), built once
+    // per march by launch_factor_depth when set (null: computed in-kernel):
+    // [F][k1_stride(nt)], nt = threads per column, layout in k1_img / k1_stride.
+    cplx* k1_tab;
     DevError* err;
     cudaStream_t stream;
     // Peer-direct output of the depth sweep (fused K1 -> K2 transpose): when
@@ -93,6 +97,16 @@ struct LaunchCtx {
     int peer_tiles;
     cplx* peer_dst[MAX_PEERS];
 };
+
+// k1_tab record of one frequency for nt threads per column (nt % 32 == 0):
+//   [0, 10 nt + nt/32)     shared-memory image: scan multipliers mf[4][nt],
+//                          mb[4][nt], pincf[nt], pincb[nt], warp products spw
+//   [img, img + 8 nt)      folded RHS coefficients A'_l, thread-contiguous
+//   [img + 8 nt, +2 nt)    first-level scan multipliers P0f[nt], P0b[nt]
+//   img + 10 nt            beta
+__host__ __device__ __forceinline__ int k1_img(int nt) { return (10 * nt + nt / 32 + 7) / 8 * 8; }
+__host__ __device__ __forceinline__ int k1_stride(int nt) { return (k1_img(nt) + 10 * nt + 1 + 7) / 8 * 8; }
+constexpr int K1_TAB_MAX_TILES = 128;   // columns the table path covers (one 128-thread CTA)
 
 cudaError_t launch_slab_signal(unsigned long long* const* flags, int n, cudaStream_t s);
 cudaError_t launch_slab_wait(const unsigned long long* flag, unsigned long long target, cudaStream_t s);
