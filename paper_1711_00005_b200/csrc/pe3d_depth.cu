@@ -1025,7 +1025,10 @@ static cudaError_t launch_depth_tma_cfg(const LaunchCtx& c, const cplx* src, cpl
     int per_sm = int((227 * 1024) / (bytes + 1024));
     if (per_sm > MINB) per_sm = MINB;
     if (per_sm < 1) per_sm = 1;
-    const int64_t ctas = int64_t(c.num_sms) * per_sm;
+    int64_t ctas = int64_t(c.num_sms) * per_sm;
+#ifdef PE3D_PHASE_CTAS
+    ctas = PE3D_PHASE_CTAS;         // phase-timing builds: uncontended critical path with few CTAs
+#endif
     const int per = int((total + ctas - 1) / ctas);
     const int grid = int((total + per - 1) / per);
     kern<<<grid, nthreads, bytes, c.stream>>>(tm_src, tm_dst, c.loc_tab, c.mul_tab, c.fdev, k1, c.n_theta,
