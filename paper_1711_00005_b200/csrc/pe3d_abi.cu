@@ -45,7 +45,10 @@ int step_chains(const pe3d::LaunchCtx& c, bool profiling) {
     if (profiling || c.n_freq < 2) return 1;
     const char* env = getenv("PE3D_CHAINS");
     const int64_t cols = int64_t(c.n_freq) * c.n_theta;
-    int n = env ? atoi(env) : (cols <= int64_t(6) * 3 * c.num_sms ? 3 : 2);
+    // few columns per SM (8 frequencies per GPU): one chain per frequency, up to
+    // MAX_CHAINS (8 frequencies: 3 chains 31.2 us, 4 chains 29.6-30.0, 8 chains
+    // 28.3 us per step); otherwise two (16 frequencies: 2 chains 54.2 us, 4 chains 55.4)
+    int n = env ? atoi(env) : (cols <= int64_t(6) * 3 * c.num_sms ? Handle::MAX_CHAINS : 2);
     if (n > Handle::MAX_CHAINS) n = Handle::MAX_CHAINS;
     if (n > c.n_freq) n = c.n_freq;
     return n < 1 ? 1 : n;

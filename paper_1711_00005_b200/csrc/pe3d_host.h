@@ -64,7 +64,7 @@ struct Handle {
     // kernels launched by the last march (graph replays included)
     int64_t graph_launches = 0, last_launches = 0;
     // concurrent step-loop chains over disjoint frequency groups
-    static constexpr int MAX_CHAINS = 4;
+    static constexpr int MAX_CHAINS = 8;
     cudaStream_t chain_stream[MAX_CHAINS] = {};
     cudaEvent_t chain_fork = nullptr, chain_join[MAX_CHAINS] = {};
     // TL streaming to the host (pe3d_march_host): one copy stream per chain

@@ -350,12 +350,12 @@ def test_cluster_ring_slab_layout(nranks):
     assert got.tl_field.tobytes() == ref.tl_field.tobytes()
 
 
-@pytest.mark.parametrize("chains", ["2", "3"])
+@pytest.mark.parametrize("chains", ["2", "3", "8"])
 def test_concurrent_chains_bitwise_equal_to_one_chain(monkeypatch, chains):
     """Disjoint frequency groups marched as concurrent graph branches
     (PE3D_CHAINS) give bitwise the single-chain results: TL at every output
     range, clamped counts and final slabs, with uneven groups (5 = 2+3 or
-    1+2+2 frequencies)."""
+    1+2+2 frequencies) and one chain per frequency (8, clamped to 5)."""
     freqs = (50.0, 90.0, 150.0, 300.0, 500.0)
     cfg = configs.build("cfg4", n_range=8, frequencies=freqs, output_stride=2)
     monkeypatch.setenv("PE3D_CHAINS", "1")
@@ -383,7 +383,7 @@ def test_parallel_factorization_matches_reference_recurrence(monkeypatch):
 
 @pytest.mark.parametrize("n_steps,stride,chains,topology", [
     (0, 1, "2", PERIODIC), (6, 6, "2", PERIODIC), (6, 2, "1", PERIODIC), (21, 3, "2", PERIODIC),
-    (21, 3, "3", PERIODIC), (13, 2, "1", SECTOR)])
+    (21, 3, "3", PERIODIC), (21, 3, "8", PERIODIC), (13, 2, "1", SECTOR)])
 def test_tl_streaming_to_pinned_host(monkeypatch, n_steps, stride, chains, topology):
     """pe3d_march_host with a page-locked TL stack streams the samples through
     a device ring (R = min(S, 4) slots, copies overlapping the march, ring
