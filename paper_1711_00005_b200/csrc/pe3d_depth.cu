@@ -787,6 +787,7 @@ k_depth_tma_cluster(const __grid_constant__ CUtensorMap tm_src, const __grid_con
     cplx A[RPT], M[RPT], beta = czero(), P0f = czero(), P0b = czero(), Pcta = czero();
     int slot = 0;
     unsigned parity = 0;
+    PHASE_BEGIN
     for (int it = 0; it < n_cols; ++it) {
         const int buf = it & 1;
         const unsigned xpar = unsigned(it >> 1) & 1u;
@@ -853,9 +854,12 @@ k_depth_tma_cluster(const __grid_constant__ CUtensorMap tm_src, const __grid_con
                 psuf[t] = lane < 31 ? cmul(after, pincb[t + 1]) : after;
             }
             cur_f = f;
+            PHASE(0);
         }
         cplx* cur = stage + slot * 256;
+        PHASE(1);
         mbar_wait(&bars[slot], parity);
+        PHASE(2);
         const int sw = lane & 7;
         cplx x[RPT];
 #pragma unroll
@@ -864,7 +868,9 @@ k_depth_tma_cluster(const __grid_constant__ CUtensorMap tm_src, const __grid_con
         cplx up = shfl_up(x[RPT - 1], 1), dn = shfl_down(x[0], 1);
         if (lane == 31) sUp[warp] = x[RPT - 1];
         if (lane == 0) sDn[warp] = x[0];
+        PHASE(3);
         __syncthreads();
+        PHASE(4);
         if (lane == 0) up = warp > 0 ? sUp[warp - 1] : up_g;
         if (lane == 31) dn = warp < nwarps - 1 ? sDn[warp + 1] : dn_g;
 
@@ -886,7 +892,9 @@ k_depth_tma_cluster(const __grid_constant__ CUtensorMap tm_src, const __grid_con
 #pragma unroll
         for (int d = 0; d < 5; ++d) Y = cfma(d == 0 ? P0f : mf[(d - 1) * nthreads + t], shfl_up(Y, 1 << d), Y);
         if (lane == 31) sY[warp] = Y;
+        PHASE(5);
         __syncthreads();
+        PHASE(6);
         cplx C = czero();
         for (int w = 0; w < warp; ++w) C = cfma(spw[w], C, sY[w]);
         const cplx yinc = cfma(pincf[t], C, Y);         // y at this thread's last row, zero CTA carry
@@ -901,7 +909,9 @@ k_depth_tma_cluster(const __grid_constant__ CUtensorMap tm_src, const __grid_con
         }
         cplx y = shfl_up(yinc, 1);
         if (lane == 0) y = C;
+        PHASE(15);
         mbar_wait(&xbar[buf], xpar);
+        PHASE(13);
         {
             cplx cin = czero();
             for (int u = 0; u < s; ++u) cin = cfma(tF[2 * u + 1], cin, tF[2 * u]);
@@ -916,7 +926,9 @@ k_depth_tma_cluster(const __grid_constant__ CUtensorMap tm_src, const __grid_con
 #pragma unroll
         for (int d = 0; d < 5; ++d) X = cfma(d == 0 ? P0b : mb[(d - 1) * nthreads + t], shfl_down(X, 1 << d), X);
         if (lane == 0) sX[warp] = X;
+        PHASE(7);
         __syncthreads();
+        PHASE(8);
         cplx D = czero();
         for (int w = nwarps - 1; w > warp; --w) D = cfma(spw[w], D, sX[w]);
         const cplx xinc = cfma(pincb[t], D, X);         // x at this thread's first row, zero carry from below
@@ -927,7 +939,9 @@ k_depth_tma_cluster(const __grid_constant__ CUtensorMap tm_src, const __grid_con
         }
         cplx xv = shfl_down(xinc, 1);
         if (lane == 31) xv = D;
+        PHASE(9);
         mbar_wait(&xbar[2 + buf], xpar);
+        PHASE(14);
         {
             cplx din = czero();
             for (int u = CL - 1; u > s; --u) din = cfma(tF[2 * u + 1], din, tB[u]);
@@ -936,6 +950,7 @@ k_depth_tma_cluster(const __grid_constant__ CUtensorMap tm_src, const __grid_con
 #pragma unroll
         for (int i = RPT - 1; i >= 0; --i) { xv = cfma(M[i], xv, b[i]); b[i] = xv; }
 
+        PHASE(11);
 #pragma unroll
         for (int i = 0; i < RPT; ++i) cur[lane * 8 + (i ^ sw)] = b[i];
         fence_proxy_async_smem();
@@ -952,11 +967,14 @@ k_depth_tma_cluster(const __grid_constant__ CUtensorMap tm_src, const __grid_con
             }
         }
         __syncwarp();
+        PHASE(10);
         if (++col == n_theta) { col = 0; ++f; }
         if (++slot == STAGES) { slot = 0; parity ^= 1u; }
     }
     if (lane == 0) bulk_wait_read<0>();
     __syncwarp();
+    PHASE(12);
+    PHASE_END;
     cluster_barrier();                              // no CTA leaves while peers may still address it
 }
 
