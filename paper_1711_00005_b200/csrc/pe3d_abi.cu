@@ -135,7 +135,7 @@ cudaError_t enqueue_group(Handle* h, const pe3d_grid* g, const MarchPlan& p, int
     cg.fdev = c.fdev + f0;
     cg.loc_tab = c.loc_tab + int64_t(f0) * c.n_tiles * 8;
     cg.mul_tab = c.mul_tab + int64_t(f0) * c.n_tiles * 8;
-    if (c.k1_tab) cg.k1_tab = c.k1_tab + int64_t(f0) * pe3d::k1_stride((c.n_tiles + 31) / 32 * 32);
+    if (c.k1_tab) cg.k1_tab = c.k1_tab + pe3d::k1_tab_elems(f0, c.n_tiles);
     cg.stream = st;
     cplx* A = h->field_a.as<cplx>() + f0 * fe;
     cplx* B = h->field_b.as<cplx>() + f0 * fe;
@@ -394,9 +394,9 @@ static int march_device_impl(void* handle, const pe3d_grid* g, const pe3d_coeffs
     CK(h->field_b.ensure(field * sizeof(cplx)), "alloc field");
     CK(h->loc_tab.ensure(int64_t(F) * n_tiles * 8 * sizeof(cplx)), "alloc tables");
     CK(h->mul_tab.ensure(int64_t(F) * n_tiles * 8 * sizeof(cplx)), "alloc tables");
-    const bool k1_table = n_tiles <= pe3d::K1_TAB_MAX_TILES;
-    if (k1_table)
-        CK(h->k1_tab.ensure(int64_t(F) * pe3d::k1_stride((n_tiles + 31) / 32 * 32) * sizeof(cplx)), "alloc tables");
+    const int64_t k1_elems = pe3d::k1_tab_elems(F, n_tiles);
+    const bool k1_table = k1_elems > 0;
+    if (k1_table) CK(h->k1_tab.ensure(k1_elems * sizeof(cplx)), "alloc tables");
     CK(h->fdev.ensure(F * sizeof(pe3d::FreqDev)), "alloc coeffs");
     CK(h->w_abs.ensure(int64_t(S) * F * sizeof(double)), "alloc w");
     CK(h->err.ensure(sizeof(pe3d::DevError)), "alloc err");

@@ -692,6 +692,72 @@ __global__ void k_depth_setup(const cplx* __restrict__ loc_tab, const cplx* __re
     if (t == 0) kt[img + 10 * nthreads] = beta;
 }
 
+// The same for the long-column cluster sweep: one 128-thread CTA per
+// (frequency, sub-column s), rows [1024 s, 1024 (s + 1)), exactly the
+// arithmetic of k_depth_tma_cluster's in-kernel setup, written as the
+// K1C record (pe3d_internal.h).
+__global__ void __launch_bounds__(128) k_depth_setup_cluster(const cplx* __restrict__ loc_tab,
+                                                             const cplx* __restrict__ mul_tab,
+                                                             const FreqDev* __restrict__ fdev, int n_tiles,
+                                                             cplx* __restrict__ k1_tab) {
+    constexpr int RPT = 8, nthreads = 128, nwarps = 4;
+    const int n_sub = n_tiles / 128;
+    const int f = blockIdx.x / n_sub, s = blockIdx.x - f * n_sub;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int nz8 = n_tiles * 8, row0 = s * 1024;
+    cplx* kt = k1_tab + int64_t(blockIdx.x) * K1C_STRIDE;
+    cplx* mf = kt;
+    cplx* mb = mf + 4 * nthreads;
+    cplx* pincf_g = mb + 4 * nthreads;
+    cplx* pincb_g = pincf_g + nthreads;
+    cplx* pexc = pincb_g + nthreads;
+    cplx* psuf = pexc + nthreads;
+    cplx* spw_g = psuf + nthreads;
+    __shared__ cplx pincf[nthreads], pincb[nthreads], spw[nwarps];
+    const FreqDev fd = fdev[f];
+    const cplx kappa = crecip(cneg(fd.off_z));
+    const cplx beta = cmul(kappa, crmul(fd.s_z, fd.cx_rhs));
+    cplx P = cone();
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+        const int64_t o = int64_t(f) * nz8 + row0 + RPT * t + i;
+        const cplx lc = ldc(loc_tab + o);
+        const cplx m = ldc(mul_tab + o);
+        kt[K1C_IMG + RPT * t + i] = csub(cmul(kappa, cadd(cone(), cmul(fd.cx_rhs, lc))), cadd(beta, beta));
+        P = cmul(m, P);
+    }
+    kt[K1C_IMG + 8 * nthreads + t] = lane >= 1 ? P : czero();
+    kt[K1C_IMG + 9 * nthreads + t] = lane + 1 < 32 ? P : czero();
+    cplx Pf = P, Pb = P;
+#pragma unroll
+    for (int d = 0; d < 5; ++d) {
+        const int o = 1 << d;
+        if (d > 0) {
+            mf[(d - 1) * nthreads + t] = lane >= o ? Pf : czero();
+            mb[(d - 1) * nthreads + t] = lane + o < 32 ? Pb : czero();
+        }
+        const cplx pu = shfl_up(Pf, o), pd = shfl_down(Pb, o);
+        if (lane >= o) Pf = cmul(Pf, pu);
+        if (lane + o < 32) Pb = cmul(Pb, pd);
+    }
+    pincf[t] = pincf_g[t] = Pf;
+    pincb[t] = pincb_g[t] = Pb;
+    if (lane == 31) spw[warp] = spw_g[warp] = Pf;
+    __syncthreads();
+    cplx before = cone(), after = cone(), Pcta = cone();
+    for (int w = 0; w < nwarps; ++w) {
+        if (w < warp) before = cmul(before, spw[w]);
+        if (w > warp) after = cmul(after, spw[w]);
+        Pcta = cmul(Pcta, spw[w]);
+    }
+    pexc[t] = lane > 0 ? cmul(before, pincf[t - 1]) : before;
+    psuf[t] = lane < 31 ? cmul(after, pincb[t + 1]) : after;
+    if (t == 0) {
+        kt[K1C_IMG + 10 * nthreads] = beta;
+        kt[K1C_IMG + 10 * nthreads + 1] = Pcta;
+    }
+}
+
 // Long columns (cfg5: 4096 rows): a thread-block cluster of CL CTAs per
 // column, CTA s solving rows [s*R, (s+1)*R) (R = 8*tiles_per_cta <= 1024)
 // with exactly the 128-thread k_depth_tma scheme above, so the SM runs three
@@ -705,12 +771,13 @@ __global__ void k_depth_setup(const cplx* __restrict__ loc_tab, const cplx* __re
 // (mbarrier transaction counts, no cluster barrier in the loop).  The depth
 // stencil's halo rows across sub-column edges are plain global loads of the
 // (read-only) input.
-template <int STAGES, int MINB, int NTH>
+template <int STAGES, int MINB, int NTH, bool TAB = false>
 __global__ void __launch_bounds__(NTH, MINB)
 k_depth_tma_cluster(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ DepthDst tm_dst,
                     const cplx* __restrict__ src_raw, const cplx* __restrict__ loc_tab,
-                    const cplx* __restrict__ mul_tab, const FreqDev* __restrict__ fdev, int n_theta, int n_tiles,
-                    int64_t total_cols, int cols_per_cluster, int sector) {
+                    const cplx* __restrict__ mul_tab, const FreqDev* __restrict__ fdev,
+                    const cplx* __restrict__ k1_tab, int n_theta, int n_tiles, int64_t total_cols,
+                    int cols_per_cluster, int sector) {
     constexpr int RPT = 8;
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
@@ -733,10 +800,12 @@ k_depth_tma_cluster(const __grid_constant__ CUtensorMap tm_src, const __grid_con
     cplx* sX = sY + nwarps;
     cplx* sUp = sX + nwarps;
     cplx* sDn = sUp + nwarps;
-    cplx* xF = sDn + nwarps;                        // [2][16][2]: (Ytot, P) of every CTA
-    cplx* xB = xF + 2 * 16 * 2;                     // [2][16]: Xtot, then [2][2] halo rows
-    uint64_t* xbar = reinterpret_cast<uint64_t*>(xB + 2 * 16 + 4);   // [0..1] forward, [2..3] backward
-    uint64_t* bars = xbar + 4 + warp * STAGES;
+    constexpr int MAXCL = 8;                        // cluster sizes the launcher uses (n_tiles / 128 <= 8)
+    cplx* xF = sDn + nwarps;                        // [2][MAXCL][2]: (Ytot, P) of every CTA
+    cplx* xB = xF + 2 * MAXCL * 2;                  // [2][MAXCL]: Xtot, then [2][2] halo rows
+    uint64_t* xbar = reinterpret_cast<uint64_t*>(xB + 2 * MAXCL + 4);   // [0..1] forward, [2..3] backward
+    uint64_t* tbar = xbar + 4;                      // frequency-table copy
+    uint64_t* bars = xbar + 5 + warp * STAGES;
 
     const int tpc = n_tiles / CL;                   // tiles per CTA (= nthreads)
     const int row0 = s * tpc * 8;
@@ -754,10 +823,39 @@ k_depth_tma_cluster(const __grid_constant__ CUtensorMap tm_src, const __grid_con
     }
     if (t == 0) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) mbar_init(&xbar[k], 1);
+        for (int k = 0; k < 5; ++k) mbar_init(&xbar[k], 1);
     }
     if (lane == 0) mbar_fence_init();
     cluster_barrier();                              // every peer's barriers initialised
+
+    int f = int(g0 / n_theta), col = int(g0 - int64_t(f) * n_theta);
+    int cur_f = -1;
+    cplx A[RPT], M[RPT], beta = czero(), P0f = czero(), P0b = czero(), Pcta = czero();
+    // With the per-march table (k_depth_setup_cluster) a frequency is one bulk
+    // copy of this CTA's shared-memory image plus register loads, issued for
+    // the first frequency before the column prefetches.
+    const int n_sub = n_tiles / 128;
+    unsigned tpar = 0;
+    auto load_freq = [&](int ff) {
+        if constexpr (TAB) {
+            const cplx* kt = k1_tab + (int64_t(ff) * n_sub + s) * K1C_STRIDE;
+            if (t == 0) {
+                constexpr unsigned bytes = unsigned(12 * nthreads + nwarps) * unsigned(sizeof(cplx));
+                mbar_expect_tx(tbar, bytes);
+                bulk_load(mf, kt, bytes, tbar);
+            }
+#pragma unroll
+            for (int i = 0; i < RPT; ++i) {
+                A[i] = ldc(kt + K1C_IMG + RPT * t + i);
+                M[i] = ldc(mul_tab + int64_t(ff) * nz8 + row0 + RPT * t + i);
+            }
+            P0f = ldc(kt + K1C_IMG + 8 * nthreads + t);
+            P0b = ldc(kt + K1C_IMG + 9 * nthreads + t);
+            beta = ldc(kt + K1C_IMG + 10 * nthreads);
+            Pcta = ldc(kt + K1C_IMG + 10 * nthreads + 1);
+        }
+    };
+    if constexpr (TAB) load_freq(f);
 
     int pf = int(g0 / n_theta), pc = int(g0 - int64_t(pf) * n_theta);
     if (lane == 0) {
@@ -771,11 +869,9 @@ k_depth_tma_cluster(const __grid_constant__ CUtensorMap tm_src, const __grid_con
         }
     }
 
-    int f = int(g0 / n_theta), col = int(g0 - int64_t(f) * n_theta);
-    int cur_f = -1;
     // thread 0 keeps the row above the sub-column, the last thread the row below
     const bool halo_thread = (t == 0 && s > 0) || (t == nthreads - 1 && s < CL - 1);
-    cplx* halo = xB + 2 * 16 + (t == 0 ? 0 : 2);    // [2] per edge thread
+    cplx* halo = xB + 2 * MAXCL + (t == 0 ? 0 : 2); // [2] per edge thread
     auto halo_src = [&](int hf, int hc) -> const cplx* {
         return t == 0 ? src_raw + ((int64_t(hf) * n_tiles + (row0 >> 3) - 1) * n_theta + hc) * 8 + 7
                       : src_raw + ((int64_t(hf) * n_tiles + (row0 >> 3) + tpc) * n_theta + hc) * 8;
@@ -784,15 +880,14 @@ k_depth_tma_cluster(const __grid_constant__ CUtensorMap tm_src, const __grid_con
         cp_async16(&halo[0], halo_src(f, col));
         cp_async_commit();
     }
-    cplx A[RPT], M[RPT], beta = czero(), P0f = czero(), P0b = czero(), Pcta = czero();
     int slot = 0;
     unsigned parity = 0;
     PHASE_BEGIN
     for (int it = 0; it < n_cols; ++it) {
         const int buf = it & 1;
         const unsigned xpar = unsigned(it >> 1) & 1u;
-        cplx* tF = xF + buf * 32;
-        cplx* tB = xB + buf * 16;
+        cplx* tF = xF + buf * (2 * MAXCL);
+        cplx* tB = xB + buf * MAXCL;
         if (t == 0) {
             mbar_expect_tx(&xbar[buf], unsigned(CL) * 2 * sizeof(cplx));
             mbar_expect_tx(&xbar[2 + buf], unsigned(CL) * sizeof(cplx));
@@ -810,7 +905,17 @@ k_depth_tma_cluster(const __grid_constant__ CUtensorMap tm_src, const __grid_con
                 cp_async_commit();
             }
         }
-        if (f != cur_f) {
+        if (TAB && f != cur_f) {
+            if (cur_f >= 0) {
+                __syncthreads();                    // every warp is done with the old shared tables
+                load_freq(f);
+            }
+            mbar_wait(tbar, tpar);
+            tpar ^= 1u;
+            cur_f = f;
+            PHASE(0);
+        }
+        if (!TAB && f != cur_f) {
             const FreqDev fd = fdev[f];
             const cplx kappa = crecip(cneg(fd.off_z));
             beta = cmul(kappa, crmul(fd.s_z, fd.cx_rhs));
@@ -1062,10 +1167,11 @@ static cudaError_t launch_depth_tma_cluster(const LaunchCtx& c, const cplx* src,
     const int nthreads = c.n_tiles / CL;
     const int nwarps = nthreads / 32;
     const size_t bytes = 1024 + sizeof(cplx) * (size_t(nwarps) * STAGES * 256 + 12 * size_t(nthreads) + 5 * nwarps +
-                                                2 * 16 * 2 + 2 * 16 + 4) +
-                         sizeof(uint64_t) * (4 + nwarps * STAGES);
-    if (nthreads != 128) return cudaErrorNotSupported;
-    auto kern = k_depth_tma_cluster<STAGES, MINB, 128>;
+                                                2 * 8 * 2 + 2 * 8 + 4) +
+                         sizeof(uint64_t) * (5 + nwarps * STAGES);
+    if (nthreads != 128 || CL > K1C_MAX_SUB) return cudaErrorNotSupported;
+    const cplx* k1 = c.k1_tab;                      // the march builds the K1C records for this column length
+    auto kern = k1 ? k_depth_tma_cluster<STAGES, MINB, 128, true> : k_depth_tma_cluster<STAGES, MINB, 128>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
@@ -1092,8 +1198,8 @@ static cudaError_t launch_depth_tma_cluster(const LaunchCtx& c, const cplx* src,
     const int per = int((total + resident[CL] - 1) / resident[CL]);
     const int clusters = int((total + per - 1) / per);
     cfg.gridDim = dim3(clusters * CL);
-    return cudaLaunchKernelEx(&cfg, kern, tm_src, tm_dst, src, c.loc_tab, c.mul_tab, c.fdev, c.n_theta, c.n_tiles,
-                              total, per, c.sector);
+    return cudaLaunchKernelEx(&cfg, kern, tm_src, tm_dst, src, c.loc_tab, c.mul_tab, c.fdev, k1, c.n_theta,
+                              c.n_tiles, total, per, c.sector);
 }
 
 // Columns of up to 128 tiles: 128-thread CTAs, 3 stages, 3 CTAs per SM.
@@ -1137,8 +1243,12 @@ cudaError_t launch_depth_scan(const LaunchCtx& c, const cplx* src, cplx* dst) {
 // for columns of up to 4096 rows; the reference-order single-thread
 // recurrence when PE3D_FACTOR_SERIAL is set (it was 0.46 ms per cfg4 march).
 static cudaError_t launch_depth_setup(const LaunchCtx& c) {
-    if (!c.k1_tab || c.n_tiles > K1_TAB_MAX_TILES) return cudaSuccess;
-    k_depth_setup<<<c.n_freq, round32(c.n_tiles), 0, c.stream>>>(c.loc_tab, c.mul_tab, c.fdev, c.n_tiles, c.k1_tab);
+    if (!c.k1_tab) return cudaSuccess;
+    if (c.n_tiles <= K1_TAB_MAX_TILES)
+        k_depth_setup<<<c.n_freq, round32(c.n_tiles), 0, c.stream>>>(c.loc_tab, c.mul_tab, c.fdev, c.n_tiles, c.k1_tab);
+    else if (k1_tab_elems(c.n_freq, c.n_tiles) > 0)
+        k_depth_setup_cluster<<<c.n_freq * (c.n_tiles / 128), 128, 0, c.stream>>>(c.loc_tab, c.mul_tab, c.fdev,
+                                                                                 c.n_tiles, c.k1_tab);
     return cudaGetLastError();
 }
 

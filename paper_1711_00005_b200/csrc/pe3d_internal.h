@@ -107,6 +107,21 @@ struct LaunchCtx {
 __host__ __device__ __forceinline__ int k1_img(int nt) { return (10 * nt + nt / 32 + 7) / 8 * 8; }
 __host__ __device__ __forceinline__ int k1_stride(int nt) { return (k1_img(nt) + 10 * nt + 1 + 7) / 8 * 8; }
 constexpr int K1_TAB_MAX_TILES = 128;   // columns the table path covers (one 128-thread CTA)
+// Long columns (k_depth_tma_cluster, n_tiles = 128 * n_sub, n_sub <= 8): one
+// record per (frequency, sub-column CTA) of 128 threads:
+//   [0, 12*128 + 4)        shared-memory image: mf[4][128], mb[4][128], pincf,
+//                          pincb, pexc, psuf [128] each, warp products spw[4]
+//   [K1C_IMG, +8*128)      folded RHS coefficients A'_l, thread-contiguous
+//   [K1C_IMG + 1024, +256) P0f[128], P0b[128];  K1C_IMG + 1280: beta, + 1281: Pcta
+constexpr int K1C_IMG = (12 * 128 + 4 + 7) / 8 * 8;
+constexpr int K1C_STRIDE = (K1C_IMG + 10 * 128 + 2 + 7) / 8 * 8;
+constexpr int K1C_MAX_SUB = 8;
+// k1_tab elements a march of F frequencies needs (0: no table path for this column length)
+__host__ __device__ __forceinline__ int64_t k1_tab_elems(int n_freq, int n_tiles) {
+    if (n_tiles <= K1_TAB_MAX_TILES) return int64_t(n_freq) * k1_stride((n_tiles + 31) / 32 * 32);
+    if (n_tiles % 128 == 0 && n_tiles / 128 <= K1C_MAX_SUB) return int64_t(n_freq) * (n_tiles / 128) * K1C_STRIDE;
+    return 0;
+}
 
 cudaError_t launch_slab_signal(unsigned long long* const* flags, int n, cudaStream_t s);
 cudaError_t launch_slab_wait(const unsigned long long* flag, unsigned long long target, cudaStream_t s);
