@@ -395,7 +395,7 @@ static int march_device_impl(void* handle, const pe3d_grid* g, const pe3d_coeffs
     CK(h->loc_tab.ensure(int64_t(F) * n_tiles * 8 * sizeof(cplx)), "alloc tables");
     CK(h->mul_tab.ensure(int64_t(F) * n_tiles * 8 * sizeof(cplx)), "alloc tables");
     const int64_t k1_elems = pe3d::k1_tab_elems(F, n_tiles);
-    const bool k1_table = k1_elems > 0;
+    const bool k1_table = k1_elems > 0 && !getenv("PE3D_NO_K1_TABLE");    // A/B: in-kernel frequency setup
     if (k1_table) CK(h->k1_tab.ensure(k1_elems * sizeof(cplx)), "alloc tables");
     CK(h->fdev.ensure(F * sizeof(pe3d::FreqDev)), "alloc coeffs");
     CK(h->w_abs.ensure(int64_t(S) * F * sizeof(double)), "alloc w");
@@ -477,7 +477,7 @@ static int march_device_impl(void* handle, const pe3d_grid* g, const pe3d_coeffs
         add(coeffs, sizeof(pe3d_coeffs) * F);
         add(ptrs, sizeof(ptrs));
         add(&stream, sizeof(stream));
-        const void* tabs[6] = {h->w_abs.ptr, h->fdev.ptr, h->loc_tab.ptr, h->err.ptr, h->ring_tab.ptr, h->k1_tab.ptr};
+        const void* tabs[6] = {h->w_abs.ptr, h->fdev.ptr, h->loc_tab.ptr, h->err.ptr, h->ring_tab.ptr, p.ctx.k1_tab};
         add(tabs, sizeof(tabs));
         const int chains = step_chains(p.ctx, false);
         add(&chains, sizeof(chains));

@@ -368,6 +368,29 @@ def test_concurrent_chains_bitwise_equal_to_one_chain(monkeypatch, chains):
         assert x.clamped_samples == y.clamped_samples
 
 
+@pytest.mark.parametrize("shape", ["cfg4", "long"])
+def test_depth_setup_table_bitwise_equal_to_in_kernel_setup(monkeypatch, shape):
+    """The per-march depth-sweep setup records (k_depth_setup /
+    k_depth_setup_cluster, bulk-copied at a frequency switch) against the
+    in-kernel frequency setup (PE3D_NO_K1_TABLE): bitwise equal TL, final
+    slabs and clamped counts, several frequencies per CTA (switches), for
+    1024-row columns (k_depth_tma) and 2048-row columns (the cluster sweep)."""
+    freqs = (50.0, 90.0, 150.0)
+    if shape == "cfg4":
+        cfg = configs.build("cfg4", n_range=6, frequencies=freqs, output_stride=3)
+    else:
+        grid = make_grid(n_range=6, n_azimuth=512, n_depth=2048, delta_r=2.0, delta_z=0.5, r_start=2.0)
+        cfg = Config(grid, make_env(grid), SourceSpec(freqs, 0.3 * grid.depth_extent), RunOptions(output_stride=3))
+    monkeypatch.setenv("PE3D_NO_K1_TABLE", "1")
+    ref = march_frequencies(cfg, list(freqs))
+    monkeypatch.delenv("PE3D_NO_K1_TABLE")
+    got = march_frequencies(cfg, list(freqs))
+    for x, y in zip(ref, got):
+        assert x.tl_field.tobytes() == y.tl_field.tobytes()
+        assert x.final_slab.values.tobytes() == y.final_slab.values.tobytes()
+        assert x.clamped_samples == y.clamped_samples
+
+
 def test_parallel_factorization_matches_reference_recurrence(monkeypatch):
     """The depth tables from the continuant scan (one CTA per frequency)
     against the reference-order single-thread Thomas recurrence."""
