@@ -493,37 +493,37 @@ k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ 
             mbar_wait(tbar, tpar);
             tpar ^= 1u;
             cur_f = f;
-            return;
-        }
-        const cplx kappa = crecip(cneg(fd.off_z));
-        beta = cmul(kappa, crmul(fd.s_z, fd.cx_rhs));
-        cplx P = cone();
+        } else {
+            const cplx kappa = crecip(cneg(fd.off_z));
+            beta = cmul(kappa, crmul(fd.s_z, fd.cx_rhs));
+            cplx P = cone();
 #pragma unroll
-        for (int i = 0; i < RPT; ++i) {
-            A[i] = csub(cmul(kappa, cadd(cone(), cmul(fd.cx_rhs, lc[i]))), cadd(beta, beta));
-            P = cmul(M[i], P);
-        }
-        if (!active) P = cone();
-        __syncthreads();
-        P0f = lane >= 1 ? P : czero();
-        P0b = lane + 1 < 32 ? P : czero();
-        cplx Pf = P, Pb = P;
-#pragma unroll
-        for (int d = 0; d < 5; ++d) {
-            const int o = 1 << d;
-            if (d > 0) {
-                mf[(d - 1) * nthreads + t] = lane >= o ? Pf : czero();
-                mb[(d - 1) * nthreads + t] = lane + o < 32 ? Pb : czero();
+            for (int i = 0; i < RPT; ++i) {
+                A[i] = csub(cmul(kappa, cadd(cone(), cmul(fd.cx_rhs, lc[i]))), cadd(beta, beta));
+                P = cmul(M[i], P);
             }
-            const cplx pu = shfl_up(Pf, o), pd = shfl_down(Pb, o);
-            if (lane >= o) Pf = cmul(Pf, pu);
-            if (lane + o < 32) Pb = cmul(Pb, pd);
+            if (!active) P = cone();
+            __syncthreads();
+            P0f = lane >= 1 ? P : czero();
+            P0b = lane + 1 < 32 ? P : czero();
+            cplx Pf = P, Pb = P;
+#pragma unroll
+            for (int d = 0; d < 5; ++d) {
+                const int o = 1 << d;
+                if (d > 0) {
+                    mf[(d - 1) * nthreads + t] = lane >= o ? Pf : czero();
+                    mb[(d - 1) * nthreads + t] = lane + o < 32 ? Pb : czero();
+                }
+                const cplx pu = shfl_up(Pf, o), pd = shfl_down(Pb, o);
+                if (lane >= o) Pf = cmul(Pf, pu);
+                if (lane + o < 32) Pb = cmul(Pb, pd);
+            }
+            pincf[t] = Pf;
+            pincb[t] = Pb;
+            if (lane == 31) spw[warp] = Pf;
+            __syncthreads();
+            cur_f = f;
         }
-        pincf[t] = Pf;
-        pincb[t] = Pb;
-        if (lane == 31) spw[warp] = Pf;
-        __syncthreads();
-        cur_f = f;
     };
     setup_freq();           // first frequency outside the loop: lc and fd are not loop-carried
     PHASE(11);

@@ -480,38 +480,49 @@ k_azimuth_warp(const cplx* __restrict__ src, cplx* __restrict__ dst, const cplx*
             cp_async16(d + ring_slot<L>(e >> 3, e & 7), g + e + (CHUNKED ? int64_t((e >> 3) / C) * gap : 0));
         }
     };
+    int f = int(it0 / n_tiles), tile = int(it0 - int64_t(f) * n_tiles);
+    // The first item's ring table and frequency constants are requested
+    // before the item prefetches (as the oldest cp.async group and register
+    // loads), so they do not queue behind the field traffic of every CTA;
+    // later frequencies load them at the switch.
+    for (int e = tid; e < E; e += NTHR) cp_async16(T + e, table + int64_t(f) * E + e);
+    cp_async_commit();
+    double fk0 = fdev[f].k0;
+    cplx fcy = fdev[f].cy_rhs;
 #pragma unroll
     for (int p = 0; p < STAGES - 1; ++p) {
         if (it0 + p < it1) fetch(it0 + p, p);
         cp_async_commit();
     }
-    int f = int(it0 / n_tiles), tile = int(it0 - int64_t(f) * n_tiles);
     int cur_f = -1;
     int slot = 0;
     cplx rho = czero(), inv_wrap = czero(), scale = czero(), b1 = czero(), b2 = czero();
     bool diagonal = false;
     for (int64_t item = it0; item < it1; ++item) {
         __syncthreads();                            // previous item's stage fully stored
-        if (f != cur_f) {
+        const bool new_f = f != cur_f;
+        if (new_f && cur_f >= 0) {
             for (int e = tid; e < E; e += NTHR) T[e] = table[int64_t(f) * E + e];
-            __syncthreads();
-            cur_f = f;
-            rho = T[0];
-            scale = T[1];
-            inv_wrap = T[2];
-            diagonal = T[3].re != 0.0;
-            const FreqDev fd = fdev[f];
-            const cplx alpha = crmul(azimuth_scale(fd.k0, r_new, delta_theta), fd.cy_rhs);
-            b2 = cmul(scale, alpha);
-            b1 = csub(scale, cadd(b2, b2));
+            fk0 = fdev[f].k0;
+            fcy = fdev[f].cy_rhs;
         }
         {
             const int64_t ip = item + STAGES - 1;
             if (ip < it1) fetch(ip, (slot + STAGES - 1) % STAGES);
             cp_async_commit();
-            cp_async_wait<STAGES - 1>();
+            cp_async_wait<STAGES - 1>();            // also the first frequency's table (the oldest group)
         }
-        __syncthreads();                            // item's lines visible to every warp
+        __syncthreads();                            // item's lines (and a new table) visible to every warp
+        if (new_f) {
+            cur_f = f;
+            rho = T[0];
+            scale = T[1];
+            inv_wrap = T[2];
+            diagonal = T[3].re != 0.0;
+            const cplx alpha = crmul(azimuth_scale(fk0, r_new, delta_theta), fcy);
+            b2 = cmul(scale, alpha);
+            b1 = csub(scale, cadd(b2, b2));
+        }
         cplx* stg = smem + slot * ITEM;
         cplx v[RT][L];
 #pragma unroll
