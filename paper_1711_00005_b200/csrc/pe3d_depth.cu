@@ -475,6 +475,7 @@ k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ 
     };
     PHASE_BEGIN
     load_freq(f);
+    griddep_wait();                                 // the field (input and output) belongs to the previous sweep until here
 
     int pf = int(g0 / n_theta), pc = int(g0 - int64_t(pf) * n_theta);
     if (lane == 0) {
@@ -538,6 +539,7 @@ k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ 
             PHASE(0);
         }
         cplx* cur = stage + slot * 256;
+        if (it == n_cols - 1) griddep_launch();     // last column: the next sweep may start launching
         PHASE(1);
         mbar_wait(&bars[slot], parity);
         PHASE(2);
@@ -1154,9 +1156,8 @@ static cudaError_t launch_depth_tma_cfg(const LaunchCtx& c, const cplx* src, cpl
 #endif
     const int per = int((total + ctas - 1) / ctas);
     const int grid = int((total + per - 1) / per);
-    kern<<<grid, nthreads, bytes, c.stream>>>(tm_src, tm_dst, c.loc_tab, c.mul_tab, c.fdev, k1, c.n_theta,
-                                              c.n_tiles, total, per, c.sector);
-    return cudaGetLastError();
+    return launch_pdl(c.pdl != 0, kern, dim3(grid), dim3(nthreads), bytes, c.stream, tm_src, tm_dst, c.loc_tab,
+                      c.mul_tab, c.fdev, k1, c.n_theta, c.n_tiles, total, per, c.sector);
 }
 
 static cudaError_t launch_depth_tma_cluster(const LaunchCtx& c, const cplx* src, cplx* dst, int CL) {

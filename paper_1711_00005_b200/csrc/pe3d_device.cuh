@@ -240,6 +240,11 @@ __device__ __forceinline__ void bulk_load(void* smem_dst, const void* gsrc, unsi
                  "l"(gsrc), "r"(bytes), "r"(smem_addr(bar))
                  : "memory");
 }
+// Programmatic dependent launch: wait for the preceding grid (its memory
+// visible), and allow the next grid to launch.  Both are no-ops when the
+// kernel was not launched with programmatic stream serialization.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() {

@@ -6,6 +6,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "pe3d_device.cuh"
 
 namespace pe3d {
@@ -93,6 +95,9 @@ struct LaunchCtx {
     // Peer-direct output of the depth sweep (fused K1 -> K2 transpose): when
     // n_peers > 0, tiles [q*peer_tiles, (q+1)*peer_tiles) of every column go to
     // peer_dst[q], laid out [tile][column][8] (n_theta columns).
+    // Launch the step-loop sweeps with programmatic stream serialization
+    // (PDL): a sweep's independent prologue overlaps the previous sweep's tail.
+    int pdl;
     int n_peers;
     int peer_tiles;
     cplx* peer_dst[MAX_PEERS];
@@ -121,6 +126,23 @@ __host__ __device__ __forceinline__ int64_t k1_tab_elems(int n_freq, int n_tiles
     if (n_tiles <= K1_TAB_MAX_TILES) return int64_t(n_freq) * k1_stride((n_tiles + 31) / 32 * 32);
     if (n_tiles % 128 == 0 && n_tiles / 128 <= K1C_MAX_SUB) return int64_t(n_freq) * (n_tiles / 128) * K1C_STRIDE;
     return 0;
+}
+
+// cudaLaunchKernelEx with the programmatic-serialization attribute when pdl is set.
+template <class... KArgs, class... Args>
+inline cudaError_t launch_pdl(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t stream, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
 cudaError_t launch_slab_signal(unsigned long long* const* flags, int n, cudaStream_t s);

@@ -489,6 +489,7 @@ k_azimuth_warp(const cplx* __restrict__ src, cplx* __restrict__ dst, const cplx*
     cp_async_commit();
     double fk0 = fdev[f].k0;
     cplx fcy = fdev[f].cy_rhs;
+    griddep_wait();                                 // the field belongs to the previous sweep until here
 #pragma unroll
     for (int p = 0; p < STAGES - 1; ++p) {
         if (it0 + p < it1) fetch(it0 + p, p);
@@ -500,6 +501,7 @@ k_azimuth_warp(const cplx* __restrict__ src, cplx* __restrict__ dst, const cplx*
     bool diagonal = false;
     for (int64_t item = it0; item < it1; ++item) {
         __syncthreads();                            // previous item's stage fully stored
+        if (item == it1 - 1) griddep_launch();      // last item: the next sweep may start launching
         const bool new_f = f != cur_f;
         if (new_f && cur_f >= 0) {
             for (int e = tid; e < E; e += NTHR) T[e] = table[int64_t(f) * E + e];
@@ -1210,9 +1212,8 @@ static cudaError_t launch_warp_ring(const LaunchCtx& c, const cplx* src, cplx* d
     int per = int((items + ctas - 1) / ctas);
     if (items <= 2 * ctas) per = 1;
     const int grid = int((items + per - 1) / per);
-    kern<<<grid, nthr, bytes, c.stream>>>(src, dst, table_step, E, c.fdev, c.n_tiles, c.n_depth, items, per, r_new,
-                                          c.delta_theta, ea);
-    return cudaGetLastError();
+    return launch_pdl(c.pdl != 0, kern, dim3(grid), dim3(nthr), bytes, c.stream, src, dst, table_step, E, c.fdev,
+                      c.n_tiles, c.n_depth, items, per, r_new, c.delta_theta, ea);
 }
 
 template <int L, int RT, int STAGES>
