@@ -858,6 +858,7 @@ k_depth_tma_cluster(const __grid_constant__ CUtensorMap tm_src, const __grid_con
         }
     };
     if constexpr (TAB) load_freq(f);
+    griddep_wait();                                 // the field belongs to the previous sweep until here
 
     int pf = int(g0 / n_theta), pc = int(g0 - int64_t(pf) * n_theta);
     if (lane == 0) {
@@ -964,6 +965,7 @@ k_depth_tma_cluster(const __grid_constant__ CUtensorMap tm_src, const __grid_con
             PHASE(0);
         }
         cplx* cur = stage + slot * 256;
+        if (it == n_cols - 1) griddep_launch();     // last column: the next sweep may start launching
         PHASE(1);
         mbar_wait(&bars[slot], parity);
         PHASE(2);
@@ -1179,11 +1181,13 @@ static cudaError_t launch_depth_tma_cluster(const LaunchCtx& c, const cplx* src,
     cfg.blockDim = dim3(nthreads);
     cfg.dynamicSmemBytes = bytes;
     cfg.stream = c.stream;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = CL;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
     static int resident[17] = {0};                  // co-resident clusters, per cluster size
@@ -1199,6 +1203,10 @@ static cudaError_t launch_depth_tma_cluster(const LaunchCtx& c, const cplx* src,
     const int per = int((total + resident[CL] - 1) / resident[CL]);
     const int clusters = int((total + per - 1) / per);
     cfg.gridDim = dim3(clusters * CL);
+    // PDL only when the grid leaves most co-resident cluster slots free (cfg2:
+    // 128 of 222); a full persistent grid launched early loses co-residency
+    // (see launch_cluster_ring, pe3d_ring.cu)
+    cfg.numAttrs = (c.pdl && 4 * clusters <= 3 * resident[CL]) ? 2 : 1;
     return cudaLaunchKernelEx(&cfg, kern, tm_src, tm_dst, src, c.loc_tab, c.mul_tab, c.fdev, k1, c.n_theta,
                               c.n_tiles, total, per, c.sector);
 }

@@ -728,6 +728,7 @@ k_azimuth_cluster(const cplx* __restrict__ src, cplx* __restrict__ dst, const cp
             }
         }
     };
+    griddep_wait();                                 // the field belongs to the previous sweep until here
 #pragma unroll
     for (int p = 0; p < STAGES - 1; ++p) {
         if (it0 + p < it1) fetch(it0 + p, p);
@@ -740,6 +741,7 @@ k_azimuth_cluster(const cplx* __restrict__ src, cplx* __restrict__ dst, const cp
     cplx Rs = cone(), Rr = cone();                  // R^s, R^(CL-1-s)
     bool diagonal = false;
     for (int64_t item = it0; item < it1; ++item) {
+        if (item == it1 - 1) griddep_launch();      // last item: the next sweep may start launching
         const int kk = int(item - it0);
         const int buf = kk & 1;
         const unsigned par = unsigned(kk >> 1) & 1u;
@@ -1234,11 +1236,13 @@ static cudaError_t launch_cluster_ring(const LaunchCtx& c, const cplx* src, cplx
     cfg.blockDim = dim3(nthr);
     cfg.dynamicSmemBytes = bytes;
     cfg.stream = c.stream;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = CL;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
     // persistent: as many clusters as can be co-resident (queried once per cluster size)
@@ -1256,6 +1260,10 @@ static cudaError_t launch_cluster_ring(const LaunchCtx& c, const cplx* src, cplx
     const int per = int((items + resident[CL] - 1) / resident[CL]);
     const int clusters = int((items + per - 1) / per);
     cfg.gridDim = dim3(clusters * CL);
+    // no PDL here: this persistent grid launched early is placed around the
+    // depth sweep's retiring CTAs and loses co-residency (cfg5, 32 of 33
+    // cluster slots: 309 -> 390 us per step)
+    cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kern, src, dst, table_step, E, c.fdev, c.n_theta, c.n_tiles, c.n_depth, items, per,
                               r_new, c.delta_theta, ea);
 }
