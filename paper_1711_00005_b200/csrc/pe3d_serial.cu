@@ -268,24 +268,39 @@ __global__ void k_solve_batch(int n, int members, int cyclic, StridedC sub, Stri
 // rule from per-member (first failing row, |pivot|) records.
 __global__ void k_reduce_failures(const int* __restrict__ fail_row, const double* __restrict__ fail_mag, int n_freq,
                                   int members, int step, int sweep, int rank1_row, DevError* err) {
+    // one warp per (frequency, 64-member tile): the tile's failure is its
+    // lowest failing row, then the smallest pivot magnitude, then the lowest
+    // member -- the order of the reference's sequential scan of the tile
     const int tiles = (members + 63) / 64;
-    const int gid = blockIdx.x * blockDim.x + threadIdx.x;
-    if (gid >= n_freq * tiles) return;
-    const int f = gid / tiles, tile = gid % tiles;
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (gw >= n_freq * tiles) return;
+    const int f = gw / tiles, tile = gw % tiles;
     const int lo = tile * 64, hi = min(members, lo + 64);
-    int best_row = 0x7fffffff, best = -1;
+    int best_row = 0x7fffffff, best = 0x7fffffff;
     double best_mag = 0.0;
-    for (int w = lo; w < hi; ++w) {
+    for (int w = lo + lane; w < hi; w += 32) {
         const int r = fail_row[int64_t(f) * members + w];
         const double mg = fail_mag[int64_t(f) * members + w];
         if (r < best_row || (r == best_row && r != 0x7fffffff && mg < best_mag)) { best_row = r; best_mag = mg; best = w; }
     }
-    if (best_row != 0x7fffffff) report_failure(err, fail_key(step, sweep, f, best), best_row, best_row == rank1_row);
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        const int r = __shfl_xor_sync(0xffffffffu, best_row, d);
+        const double mg = __shfl_xor_sync(0xffffffffu, best_mag, d);
+        const int w = __shfl_xor_sync(0xffffffffu, best, d);
+        if (r < best_row || (r == best_row && r != 0x7fffffff && (mg < best_mag || (!(best_mag < mg) && w < best)))) {
+            best_row = r;
+            best_mag = mg;
+            best = w;
+        }
+    }
+    if (lane == 0 && best_row != 0x7fffffff)
+        report_failure(err, fail_key(step, sweep, f, best), best_row, best_row == rank1_row);
 }
 
 cudaError_t launch_reduce_failures(const int* fail_row, const double* fail_mag, int n_freq, int members, int step,
                                    int sweep, int rank1_row, DevError* err, cudaStream_t stream) {
-    const int total = n_freq * ((members + 63) / 64);
+    const int total = n_freq * ((members + 63) / 64) * 32;       // one warp per (frequency, tile)
     k_reduce_failures<<<(total + 127) / 128, 128, 0, stream>>>(fail_row, fail_mag, n_freq, members, step, sweep,
                                                                rank1_row, err);
     return cudaGetLastError();
