@@ -391,6 +391,27 @@ def test_depth_setup_table_bitwise_equal_to_in_kernel_setup(monkeypatch, shape):
         assert x.clamped_samples == y.clamped_samples
 
 
+@pytest.mark.parametrize("shape", ["cfg4", "cfg2"])
+def test_programmatic_launch_bitwise_equal(monkeypatch, shape):
+    """The step sweeps launched with programmatic dependent launch (default)
+    against plain stream-ordered launches (PE3D_NO_PDL): bitwise equal TL,
+    final slabs and clamped counts -- the 1024-row column sweep with eight
+    chains (8 frequencies) and the 2048-row cluster sweep (cfg2)."""
+    if shape == "cfg4":
+        freqs = (50.0, 70.0, 90.0, 120.0, 150.0, 200.0, 300.0, 500.0)
+        cfg = configs.build("cfg4", n_range=8, frequencies=freqs, output_stride=4)
+    else:
+        freqs = (100.0,)
+        cfg = configs.build("cfg2", n_range=8, output_stride=4)
+    got = march_frequencies(cfg, list(freqs))
+    monkeypatch.setenv("PE3D_NO_PDL", "1")
+    ref = march_frequencies(cfg, list(freqs))
+    for x, y in zip(ref, got):
+        assert x.tl_field.tobytes() == y.tl_field.tobytes()
+        assert x.final_slab.values.tobytes() == y.final_slab.values.tobytes()
+        assert x.clamped_samples == y.clamped_samples
+
+
 def test_parallel_factorization_matches_reference_recurrence(monkeypatch):
     """The depth tables from the continuant scan (one CTA per frequency)
     against the reference-order single-thread Thomas recurrence."""
