@@ -16,7 +16,12 @@
 // with b_l = inv_l rhs_l and m_l = -cp_l = -off inv_l (m_0 = 0), split over
 // threads (8 rows each), chained by affine scans and re-run with the exact
 // carries.  Memory: one 128-B line per (tile, column) in, one out
-// (32 B per grid point); columns stream through a cp.async ring.
+// (32 B per grid point); columns stream through a TMA stage ring
+// (k_depth_tma, k_depth_tma_cluster; k_depth_scan is the cp.async fallback).
+// Each frequency's per-CTA setup (folded coefficients, scan multipliers) is
+// built once per march by k_depth_setup / k_depth_setup_cluster; the sweeps
+// run with programmatic dependent launch, so their table loads overlap the
+// previous sweep's tail (griddep_wait before the first field access).
 
 #include "pe3d_device.cuh"
 #include "pe3d_internal.h"
