@@ -412,6 +412,26 @@ def test_programmatic_launch_bitwise_equal(monkeypatch, shape):
         assert x.clamped_samples == y.clamped_samples
 
 
+@pytest.mark.parametrize("name,freq,n_steps", [("cfg4", 500.0, 300), ("cfg2", 100.0, 150), ("cfg3", 25.0, 150)])
+def test_full_size_long_march_vs_oracle(name, freq, n_steps):
+    """BASELINE grids at full size over longer marches than the golden
+    fixtures (cfg4's highest frequency for 300 steps, cfg2 and cfg3 for 150),
+    against the oracle run here: the contract (field relative L2 <= 1e-9,
+    |dTL| <= 1e-4 dB where TL < 150 dB) at every output range, i.e. the
+    rounding drift of the scan formulations stays inside it."""
+    if name == "cfg4":
+        cfg = configs.build(name, n_range=n_steps, frequencies=(freq,), output_stride=50)
+    else:
+        cfg = configs.build(name, n_range=n_steps, output_stride=50)
+    got = march_frequencies(cfg, [freq], keep_snapshots=True)[0]
+    ref = O.run_frequency(cfg, freq, keep_snapshots=True)
+    assert got.tl_field.shape == ref.tl_field.shape
+    for k in range(ref.tl_field.shape[0]):
+        assert rel_l2(got.snapshots[k], ref.snapshots[k]) <= FIELD_TOL, f"sample {k}"
+        assert tl_err(got.tl_field[k], ref.tl_field[k]) <= TL_TOL, f"sample {k}"
+    assert rel_l2(got.final_slab.values, ref.final) <= FIELD_TOL
+
+
 def test_parallel_factorization_matches_reference_recurrence(monkeypatch):
     """The depth tables from the continuant scan (one CTA per frequency)
     against the reference-order single-thread Thomas recurrence."""
