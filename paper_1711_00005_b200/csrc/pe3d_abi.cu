@@ -15,6 +15,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <new>
+#include <string>
 #include <vector>
 
 #include "../../include/pe3d_b200.h"
@@ -485,6 +486,13 @@ static int march_device_impl(void* handle, const pe3d_grid* g, const pe3d_coeffs
         add(tabs, sizeof(tabs));
         const int chains = step_chains(p.ctx, false);
         add(&chains, sizeof(chains));
+        // the A/B switches pick kernels and launch attributes baked into the graph
+        for (const char* name : {"PE3D_NO_PDL", "PE3D_CLUSTER_L", "PE3D_DEPTH_NO_CLUSTER", "PE3D_DEPTH_NO_TMA",
+                                 "PE3D_DEPTH_WIDE_SCAN", "PE3D_RING_BLOCK", "PE3D_RING_STAGES"}) {
+            const char* v = getenv(name);
+            const std::string val = v ? std::string("=") + v : std::string("-");
+            add(val.data(), val.size() + 1);
+        }
         const TlSink none{nullptr, 0, 0};
         add(sink ? sink : &none, sizeof(TlSink));
         if (!(h->graph_exec && key == h->graph_key)) {
