@@ -1110,6 +1110,21 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
     return fn;
 }
 
+// Generic tiled FLOAT64 map with the 128-B swizzle (used by the azimuth sweep's
+// ring maps, pe3d_ring.cu); false when the driver entry point or the encoder refuses.
+bool encode_swizzled_map(CUtensorMap* tm, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
+                         const uint32_t* box) {
+    auto enc = tensor_map_encoder();
+    if (!enc || rank < 1 || rank > 5) return false;
+    cuuint64_t d[5], st[4];
+    cuuint32_t b[5], e[5];
+    for (int i = 0; i < rank; ++i) { d[i] = dims[i]; b[i] = box[i]; e[i] = 1; }
+    for (int i = 0; i + 1 < rank; ++i) st[i] = strides[i];
+    return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, cuuint32_t(rank), const_cast<void*>(base), d, st, b, e,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 static bool field_tensor_map(CUtensorMap* tm, const void* base, const LaunchCtx& c) {
     auto enc = tensor_map_encoder();
     if (!enc) return false;

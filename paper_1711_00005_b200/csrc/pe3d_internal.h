@@ -3,6 +3,7 @@
 // pe3d_slab.cu).  Not part of the public ABI.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -145,6 +146,8 @@ inline cudaError_t launch_pdl(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 
     return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
+bool encode_swizzled_map(CUtensorMap* tm, const void* base, int rank, const uint64_t* dims,
+                         const uint64_t* strides, const uint32_t* box);
 cudaError_t launch_slab_signal(unsigned long long* const* flags, int n, cudaStream_t s);
 cudaError_t launch_slab_wait(const unsigned long long* flag, unsigned long long target, cudaStream_t s);
 void ring_shape(int n_theta, int* L, int* RW);

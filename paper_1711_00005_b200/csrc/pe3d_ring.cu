@@ -23,6 +23,7 @@
 #include <cooperative_groups.h>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 
 namespace pe3d {
 
@@ -60,8 +61,10 @@ __device__ __forceinline__ cplx cpow_int(cplx z, int n) {
 }
 
 // Ring table of one (step, frequency): [0] rho, [1] scale = -rho/off,
-// [2] 1/(1 - rho^N), [3] (diagonal flag, 0), then pw[k] = rho^k (k = 0..L),
-// then qp[j] = rho^(jL) (j = 0..n_qp-1).
+// [2] 1/(1 - rho^N), [3] (diagonal flag, 0), [4] b1, [5] b2 (the epilogue's
+// next-temp weights, see ring_epilogue), then pw[k] = rho^k (k = 0..L), then
+// qp[j] = rho^(jL) (j = 0..n_qp-1).
+constexpr int RING_HDR = 6;
 struct RingLayout {
     int L, G, n_chunks, n_qp, E;
 };
@@ -72,7 +75,7 @@ __host__ __device__ inline RingLayout ring_layout(int n_theta, int L, int RW) {
     r.G = 32 / RW;
     r.n_chunks = (n_theta + L - 1) / L;
     r.n_qp = (r.n_chunks > r.G ? r.n_chunks : r.G) + 1;
-    r.E = 4 + (L + 1) + r.n_qp;
+    r.E = RING_HDR + (L + 1) + r.n_qp;
     return r;
 }
 
@@ -84,11 +87,11 @@ __global__ void k_ring_setup(cplx* __restrict__ table, const FreqDev* __restrict
     if (gid >= n_freq * n_steps) return;
     const int s = gid / n_freq, f = gid % n_freq;
     const int j_new = first_index + s + 1;
-    const double r_new = r_start + j_new * delta_r;             // Grid3D.range_at
+    const double r_new = __dadd_rn(r_start, __dmul_rn(double(j_new), delta_r));   // Grid3D.range_at (no FMA, as the host)
     const FreqDev fd = fdev[f];
     const RingFactor rf = ring_factor(fd, azimuth_scale(fd.k0, r_new, delta_theta));
     cplx* T = table + int64_t(gid) * lay.E;
-    cplx* pw = T + 4;
+    cplx* pw = T + RING_HDR;
     cplx* qp = pw + lay.L + 1;
     cplx p = cone();
     for (int k = 0; k <= lay.L; ++k) { pw[k] = p; p = cmul(p, rf.rho); }
@@ -103,6 +106,11 @@ __global__ void k_ring_setup(cplx* __restrict__ table, const FreqDev* __restrict
     T[1] = rf.scale;
     T[2] = crecip(wrap);
     T[3] = mk(rf.diagonal ? 1.0 : 0.0, 0.0);
+    // next temp = b1 x + b2 (x+ + x-) (same arithmetic as the sweeps' own)
+    const cplx alpha = crmul(azimuth_scale(fd.k0, r_new, delta_theta), fd.cy_rhs);
+    const cplx b2 = cmul(rf.scale, alpha);
+    T[4] = csub(rf.scale, cadd(b2, b2));
+    T[5] = b2;
 }
 
 // Given u on this thread's azimuth chunk of RT depth rows, write the TL
@@ -205,7 +213,7 @@ __device__ __forceinline__ void ring_solve(cplx (&v)[RT][L], const cplx* __restr
     const int q_last = n_chunks - 1;
     const int nv_last = n_theta - q_last * L;
     const int n_qp = (n_chunks > G ? n_chunks : G) + 1;
-    const cplx* pw = T + 4;
+    const cplx* pw = T + RING_HDR;
     const cplx* qp = pw + L + 1;
     const cplx rho = T[0], inv_wrap = T[2];
     if (T[3].re != 0.0) {             // off == 0: B = diag * I, x = v (the scale is applied by the epilogue)
@@ -456,7 +464,7 @@ k_azimuth_warp(const cplx* __restrict__ src, cplx* __restrict__ dst, const cplx*
     constexpr int PER = ITEM / NTHR;                // 16-B chunks per thread per item
     extern __shared__ cplx smem[];
     cplx* T = smem + STAGES * ITEM;                 // ring table of the current frequency
-    const cplx* pw = T + 4;                         // rho^k, k = 0..L
+    const cplx* pw = T + RING_HDR;                         // rho^k, k = 0..L
     const cplx* qp = pw + L + 1;                    // R^j, j = 0..32
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int q = lane, swz = q & 7;
@@ -671,14 +679,14 @@ k_azimuth_cluster(const cplx* __restrict__ src, cplx* __restrict__ dst, const cp
     constexpr int ITEM = NS * 8;                    // elements per segment of an item
     constexpr int NTHR = 32 * 8 / RT;
     constexpr int PER = ITEM / NTHR;
-    constexpr int TE = 4 + (L + 1) + 33;            // table entries used: header, rho^0..L, R^0..32
+    constexpr int TE = RING_HDR + (L + 1) + 33;     // table entries used: header, rho^0..L, R^0..32
     extern __shared__ cplx smem[];
     cplx* T = smem + STAGES * ITEM;
     cplx* segW = T + TE;                            // [2][16][8] forward totals of every segment
     cplx* segX = segW + 2 * 16 * 8;                 // [2][16][8] backward totals
     cplx* Rp = segX + 2 * 16 * 8;                   // [17] R^k, k = 0..16
     uint64_t* bars = reinterpret_cast<uint64_t*>(Rp + 17);   // [0..1] forward, [2..3] backward
-    const cplx* pw = T + 4;
+    const cplx* pw = T + RING_HDR;
     const cplx* qp = pw + L + 1;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int q = lane, swz = q & 7;
@@ -966,6 +974,315 @@ k_azimuth_cluster(const cplx* __restrict__ src, cplx* __restrict__ dst, const cp
     cluster_barrier();                              // no CTA leaves while peers may still address it
 }
 
+// ------------------------------------- TMA azimuth sweep (warp-specialised)
+// The Blackwell form of k_azimuth_warp / k_azimuth_cluster for the standard
+// field layout: one producer warp moves whole ring segments with the tensor
+// engine (TMA load of segment n+S while the consumer warps solve segment n,
+// TMA store of the solved temp straight from the stage), the 8/RT consumer
+// warps run the ring-per-warp solve of k_azimuth_warp on their RT rows, and
+// stage slots are handed over by full/empty mbarriers -- no CTA-wide barrier
+// and no per-thread copies in the item loop.
+//
+// Stage layout of one segment (NS = 32L azimuths x 8 rows): the 128-B line
+// k*32 + q holds azimuth m = q*L + k (lane q's k-th point) with its row r at
+// 16-B chunk r ^ (q & 7).  The 5-D tensor map {16 doubles, q: 32 (stride
+// L*128 B), k: L (stride 128 B), segment (stride NS*128 B), item (stride
+// n_theta*128 B)} with box {16, 32, L, 1, 1} and the 128-B swizzle writes
+// exactly this transposed layout, so the lane-per-chunk reads (fixed k,
+// q = 0..31) hit 8 distinct chunks per 8-lane phase: conflict free.  The
+// ring table of the item's (step, frequency) rides along into a per-slot
+// table on the same mbarrier (tab_elems entries: header, rho^0..L, and the
+// R^j run the solve reads).
+//
+// CLUSTER (rings of CL*NS points): CTA s of a cluster stages segment s and
+// the segments are joined exactly as in k_azimuth_cluster, with one pair of
+// exchange mbarriers per consumer warp (a warp's RT rows are exchanged only
+// with the same warp of the peer CTAs), double-buffered by item parity.
+template <int L>
+__device__ __forceinline__ int tma_slot(int q, int k, int r) { return ((k * 32 + q) << 3) + (r ^ (q & 7)); }
+
+template <int L, int RT, int S, bool CLUSTER, int MINB>
+__global__ void __launch_bounds__(32 * (8 / RT + 1), MINB)
+k_azimuth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ CUtensorMap tm_dst,
+              const cplx* __restrict__ table, int E, int tab_elems, int n_theta, int n_tiles, int n_depth,
+              int64_t total_items, int items_per_unit, EpilogueArgs ea) {
+    namespace cg = cooperative_groups;
+    constexpr int NW = 8 / RT;                      // consumer warps; warp NW is the TMA producer
+    constexpr int NS = 32 * L;                      // segment length
+    constexpr int ITEM = NS * 8;                    // elements per segment
+    constexpr unsigned ITEM_BYTES = ITEM * sizeof(cplx);
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    cplx* stage = reinterpret_cast<cplx*>(smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u));
+    const int tab_pad = (tab_elems + 7) & ~7;
+    cplx* tabs = stage + S * ITEM;                  // [S][tab_pad]
+    cplx* segW = tabs + S * tab_pad;                // cluster: [2][16][8] forward totals
+    cplx* segX = segW + (CLUSTER ? 2 * 16 * 8 : 0); // cluster: [2][16][8] backward totals
+    uint64_t* full = reinterpret_cast<uint64_t*>(segX + (CLUSTER ? 2 * 16 * 8 : 0));
+    uint64_t* empty = full + S;
+    uint64_t* xbar = empty + S;                     // cluster: [NW][4]: fwd buf 0/1, bwd buf 0/1
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int CL = 1, s = 0;
+    if constexpr (CLUSTER) {
+        cg::cluster_group cluster = cg::this_cluster();
+        CL = int(cluster.num_blocks());
+        s = int(cluster.block_rank());
+    }
+    // item indices fit an int (checked by the launcher): no 64-bit division in the loop
+    const int unit = CLUSTER ? int(blockIdx.x) / CL : int(blockIdx.x);
+    const int it0 = unit * items_per_unit;
+    const int it1 = it0 + items_per_unit < int(total_items) ? it0 + items_per_unit : int(total_items);
+    if (it0 >= it1) return;                         // uniform over a cluster
+    const int N = it1 - it0;
+    if (tid == 0) {
+#pragma unroll
+        for (int k = 0; k < S; ++k) {
+            mbar_init(&full[k], 1);
+            mbar_init(&empty[k], NW);
+        }
+        if (CLUSTER)
+            for (int b = 0; b < 4 * NW; ++b) mbar_init(&xbar[b], 1);
+        mbar_fence_init();
+    }
+    if (CLUSTER) cluster_barrier();                 // peers' barriers initialised before any st.async
+    else __syncthreads();
+
+    if (warp == NW) {
+        // ------------------------------------------------ producer warp
+        if (lane == 0) {
+            griddep_wait();                         // the field belongs to the previous sweep until here
+            const unsigned tab_bytes = unsigned(tab_elems) * unsigned(sizeof(cplx));
+            auto load = [&](int n, int slot) {
+                const int item = it0 + n;
+                const int f = item / n_tiles;
+                mbar_expect_tx(&full[slot], ITEM_BYTES + tab_bytes);
+                tma_load_5d(stage + slot * ITEM, &tm_src, 0, 0, 0, s, item, &full[slot]);
+                bulk_load(tabs + slot * tab_pad, table + int64_t(f) * E, tab_bytes, &full[slot]);
+            };
+            for (int p = 0; p < S && p < N; ++p) load(p, p);
+            for (int n = 0; n < N; ++n) {
+                const int slot = n % S;
+                mbar_wait(&empty[slot], unsigned(n / S) & 1u);      // consumers wrote the temp (or are done)
+                if (ea.write_temp) {
+                    tma_store_5d(&tm_dst, 0, 0, 0, s, it0 + n, stage + slot * ITEM);
+                    bulk_commit();
+                }
+                if (n + S < N) {
+                    bulk_wait_read<0>();            // the store has left the slot
+                    load(n + S, slot);
+                }
+            }
+            bulk_wait_read<0>();
+        }
+        __syncwarp();
+        griddep_launch();
+    } else {
+        // ------------------------------------------------ consumer warps
+        const int q = lane, swz = q & 7;
+        const int m0 = q * L, mseg = s * NS;
+        const unsigned exch_bytes = unsigned(CL) * RT * unsigned(sizeof(cplx));
+        auto push = [&](cplx* table_, uint64_t* bar, int row, cplx val) {
+            if (lane < CL) st_async_cplx(mapa_shared(smem_addr(table_ + s * 8 + row), lane), val,
+                                         mapa_shared(smem_addr(bar), lane));
+        };
+        int f = it0 / n_tiles, tile = it0 - f * n_tiles;
+        for (int n = 0; n < N; ++n) {
+            const int slot = n % S;
+            const int buf = n & 1;
+            const unsigned xpar = unsigned(n >> 1) & 1u;
+            if (n == N - 1) griddep_launch();       // last item: the next sweep may start launching
+            if (CLUSTER && lane == 0) {
+                mbar_expect_tx(&xbar[warp * 4 + buf], exch_bytes);
+                mbar_expect_tx(&xbar[warp * 4 + 2 + buf], exch_bytes);
+            }
+            mbar_wait(&full[slot], unsigned(n / S) & 1u);
+            const cplx* T = tabs + slot * tab_pad;
+            const cplx* pw = T + RING_HDR;          // rho^k, k = 0..L
+            const cplx* qp = pw + L + 1;            // R^j, j = 0..32 (cluster: R^(32k) = qp[32k])
+            const cplx rho = T[0], scale = T[1], inv_wrap = T[2], b1 = T[4], b2 = T[5];
+            const bool diagonal = T[3].re != 0.0;
+            cplx* stg = stage + slot * ITEM;
+            cplx v[RT][L];
+#pragma unroll
+            for (int h = 0; h < RT; ++h)
+#pragma unroll
+                for (int k = 0; k < L; ++k) v[h][k] = stg[tma_slot<L>(q, k, warp * RT + h)];
+
+            cplx prev_edge[RT], next_edge[RT];     // cluster: x at mseg-1 and mseg+NS (cyclic)
+            if (!diagonal) {
+                // ---- forward cyclic recurrence w_m = v_m + rho w_{m-1}
+                cplx Y[RT];
+#pragma unroll
+                for (int h = 0; h < RT; ++h) {
+                    Y[h] = czero();
+#pragma unroll
+                    for (int k = 0; k < L; ++k) { Y[h] = cfma(rho, Y[h], v[h][k]); v[h][k] = Y[h]; }
+                }
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const cplx m = lane >= d ? qp[d] : czero();
+#pragma unroll
+                    for (int h = 0; h < RT; ++h) Y[h] = cfma(m, shfl_up(Y[h], d), Y[h]);
+                }
+                cplx carry_w[RT];
+                if constexpr (CLUSTER) {
+                    cplx* tW = segW + buf * 128;
+#pragma unroll
+                    for (int h = 0; h < RT; ++h) push(tW, &xbar[warp * 4 + buf], warp * RT + h, shfl_idx(Y[h], 31));
+                    mbar_wait_cluster(&xbar[warp * 4 + buf], xpar);
+                    // half-warp hh serves row warp*RT+hh; lane j < CL weighs segment j's total
+                    const int hh = lane >> 4, j = lane & 15;
+                    const bool use = j < CL && hh < RT;
+                    const cplx w = use ? tW[j * 8 + warp * RT + (hh < RT ? hh : 0)] : czero();
+                    cplx cin = (use && j < s) ? cmul(qp[32 * (j < s ? s - 1 - j : 0)], w) : czero();
+                    cplx wend = use ? cmul(qp[32 * (j < CL ? CL - 1 - j : 0)], w) : czero();
+#pragma unroll
+                    for (int o = 1; o < 16; o <<= 1) {
+                        cin = cadd(cin, shfl_xor(cin, o));
+                        wend = cadd(wend, shfl_xor(wend, o));
+                    }
+                    const cplx cw = cfma(qp[32 * s], cmul(wend, inv_wrap), cin);   // w_(mseg-1), cyclic
+#pragma unroll
+                    for (int h = 0; h < RT; ++h) carry_w[h] = shfl_idx(cw, 16 * h);
+                } else {
+#pragma unroll
+                    for (int h = 0; h < RT; ++h) carry_w[h] = cmul(shfl_idx(Y[h], 31), inv_wrap);   // cyclic closure
+                }
+                const cplx qpq = qp[q];
+#pragma unroll
+                for (int h = 0; h < RT; ++h) {
+                    cplx ex = shfl_up(Y[h], 1);
+                    if (lane == 0) ex = czero();
+                    const cplx c_in = cfma(qpq, carry_w[h], ex);
+#pragma unroll
+                    for (int k = 0; k < L; ++k) v[h][k] = cfma(pw[k + 1], c_in, v[h][k]);
+                }
+                // ---- backward cyclic recurrence x_m = w_m + rho x_{m+1}
+                cplx X[RT];
+#pragma unroll
+                for (int h = 0; h < RT; ++h) {
+                    X[h] = czero();
+#pragma unroll
+                    for (int k = L - 1; k >= 0; --k) { X[h] = cfma(rho, X[h], v[h][k]); v[h][k] = X[h]; }
+                }
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const cplx m = lane + d < 32 ? qp[d] : czero();
+#pragma unroll
+                    for (int h = 0; h < RT; ++h) X[h] = cfma(m, shfl_down(X[h], d), X[h]);
+                }
+                cplx carry_x[RT];
+                if constexpr (CLUSTER) {
+                    cplx* tX = segX + buf * 128;
+#pragma unroll
+                    for (int h = 0; h < RT; ++h) push(tX, &xbar[warp * 4 + 2 + buf], warp * RT + h, shfl_idx(X[h], 0));
+                    mbar_wait_cluster(&xbar[warp * 4 + 2 + buf], xpar);
+                    const int hh = lane >> 4, j = lane & 15;
+                    const bool use = j < CL && hh < RT;
+                    const cplx xs = use ? tX[j * 8 + warp * RT + (hh < RT ? hh : 0)] : czero();
+                    cplx dn = (use && j > s) ? cmul(qp[32 * ((j > s && j < CL) ? j - s - 1 : 0)], xs) : czero();
+                    cplx x0 = use ? cmul(qp[32 * (j < CL ? j : 0)], xs) : czero();
+#pragma unroll
+                    for (int o = 1; o < 16; o <<= 1) {
+                        dn = cadd(dn, shfl_xor(dn, o));
+                        x0 = cadd(x0, shfl_xor(x0, o));
+                    }
+                    const cplx cx = cfma(qp[32 * (CL - 1 - s)], cmul(x0, inv_wrap), dn);   // x_(mseg+NS), cyclic
+#pragma unroll
+                    for (int h = 0; h < RT; ++h) carry_x[h] = shfl_idx(cx, 16 * h);
+                } else {
+#pragma unroll
+                    for (int h = 0; h < RT; ++h) carry_x[h] = cmul(shfl_idx(X[h], 0), inv_wrap);    // cyclic closure
+                }
+                const cplx qup = qp[31 - q];
+#pragma unroll
+                for (int h = 0; h < RT; ++h) {
+                    cplx nx = shfl_down(X[h], 1);
+                    if (lane == 31) nx = czero();
+                    const cplx c_up = cfma(qup, carry_x[h], nx);
+#pragma unroll
+                    for (int k = 0; k < L; ++k) v[h][k] = cfma(pw[L - k], c_up, v[h][k]);
+                    if constexpr (CLUSTER) {
+                        next_edge[h] = carry_x[h];
+                        prev_edge[h] = cfma(rho, shfl_idx(v[h][0], 0), carry_w[h]);   // x_(mseg-1) = w + rho x_mseg
+                    }
+                }
+            } else if constexpr (CLUSTER) {
+                // off == 0 (B = diag I): x = v; the edges are the neighbours' raw values
+                cplx* tW = segW + buf * 128;
+                cplx* tX = segX + buf * 128;
+#pragma unroll
+                for (int h = 0; h < RT; ++h) {
+                    push(tW, &xbar[warp * 4 + buf], warp * RT + h, shfl_idx(v[h][L - 1], 31));
+                    push(tX, &xbar[warp * 4 + 2 + buf], warp * RT + h, shfl_idx(v[h][0], 0));
+                }
+                mbar_wait_cluster(&xbar[warp * 4 + buf], xpar);
+                mbar_wait_cluster(&xbar[warp * 4 + 2 + buf], xpar);
+#pragma unroll
+                for (int h = 0; h < RT; ++h) {
+                    prev_edge[h] = tW[((s + CL - 1) % CL) * 8 + warp * RT + h];
+                    next_edge[h] = tX[((s + 1) % CL) * 8 + warp * RT + h];
+                }
+            }
+            // ---- boundary (surface and pad rows), TL / snapshot / final, next temp
+            const int l0 = tile * 8 + warp * RT;
+#pragma unroll
+            for (int h = 0; h < RT; ++h) {
+                const int l = l0 + h;
+                if (l + ea.row_offset == 0 || l >= n_depth) {
+#pragma unroll
+                    for (int k = 0; k < L; ++k) v[h][k] = czero();
+                    if constexpr (CLUSTER) {
+                        prev_edge[h] = czero();
+                        next_edge[h] = czero();
+                    }
+                }
+                if (l < n_depth && (ea.tl || ea.snap || ea.final_out)) {
+                    long long zeros = 0;
+#pragma unroll
+                    for (int k = 0; k < L; ++k) {
+                        const int m = mseg + m0 + k;
+                        const cplx uf = cmul(scale, v[h][k]);
+                        const int64_t so = (int64_t(f) * ea.n_samples + ea.sample) * n_theta * n_depth +
+                                           (int64_t(m) * n_depth + l);
+                        if (ea.tl) {
+                            const double mag = cabs(uf) * ea.w_abs[f];
+                            if (mag == 0.0) ++zeros;
+                            ea.tl[so] = (mag == 0.0) ? TL_FLOOR_DB : -20.0 * log10(mag);
+                        }
+                        if (ea.snap) stc(ea.snap + so, uf);
+                        if (ea.final_out) stc(ea.final_out + (int64_t(f) * n_theta + m) * n_depth + l, uf);
+                    }
+                    if (ea.tl && zeros)
+                        atomicAdd(reinterpret_cast<unsigned long long*>(ea.clamped + f), (unsigned long long)zeros);
+                }
+                if (ea.write_temp) {
+                    cplx prev = shfl_up(v[h][L - 1], 1), next = shfl_down(v[h][0], 1);
+                    if constexpr (CLUSTER) {
+                        if (lane == 0) prev = prev_edge[h];
+                        if (lane == 31) next = next_edge[h];
+                    } else {
+                        const cplx wrap_prev = shfl_idx(v[h][L - 1], 31), wrap_next = shfl_idx(v[h][0], 0);
+                        if (lane == 0) prev = wrap_prev;
+                        if (lane == 31) next = wrap_next;
+                    }
+                    const int r = (warp * RT + h) ^ swz;
+#pragma unroll
+                    for (int k = 0; k < L; ++k) {
+                        const cplx um = k ? v[h][k - 1] : prev;
+                        const cplx up = (k + 1 < L) ? v[h][(k + 1) % L] : next;
+                        stg[((k * 32 + q) << 3) + r] = cfma(b1, v[h][k], cmul(b2, cadd(up, um)));   // own slots only
+                    }
+                }
+            }
+            fence_proxy_async_smem();               // the temp is read by the TMA store (async proxy)
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[slot]);
+            if (++tile == n_tiles) { tile = 0; ++f; }
+        }
+    }
+    if (CLUSTER) cluster_barrier();                 // no CTA leaves while peers may still address it
+}
+
 // Direct variant (one CTA per (frequency, row group), registers only) for
 // rings too wide for a shared-memory stage (RW < 8).
 template <int L, int RW>
@@ -1192,6 +1509,98 @@ static cudaError_t set_smem(K kern, size_t bytes) {
     return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
 }
 
+// TMA ring maps over the standard field layout: {16 doubles, q: 32, k: L,
+// segment: n_theta / (32L), item: F * n_tiles} (see k_azimuth_tma).
+static bool ring_tensor_map(CUtensorMap* tm, const void* base, int n_theta, int L, int64_t items) {
+    const int NS = 32 * L;
+    const uint64_t dims[5] = {16, 32, uint64_t(L), uint64_t(n_theta / NS), uint64_t(items)};
+    const uint64_t strides[4] = {uint64_t(L) * 128, 128, uint64_t(NS) * 128, uint64_t(n_theta) * 128};
+    const uint32_t box[5] = {16, 32, uint32_t(L), 1, 1};
+    return encode_swizzled_map(tm, base, 5, dims, strides, box);
+}
+
+// Occupancy of a kernel configuration, cached per (kernel, device, smem bytes)
+// in a small thread-safe table (the launchers run from several handles).
+struct OccKey { const void* kern; int dev; size_t bytes; int cluster; };
+static int cached_occupancy(const void* kern, size_t bytes, int cluster, int nthr, cudaLaunchConfig_t* cfg) {
+    static std::mutex mu;
+    static OccKey keys[64];
+    static int vals[64];
+    static int n = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
+    for (int i = 0; i < n; ++i)
+        if (keys[i].kern == kern && keys[i].dev == dev && keys[i].bytes == bytes && keys[i].cluster == cluster)
+            return vals[i];
+    int v = 0;
+    cudaError_t e;
+    if (cluster > 1) e = cudaOccupancyMaxActiveClusters(&v, kern, cfg);
+    else e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kern, nthr, bytes);
+    if (e != cudaSuccess || v < 1) return 0;
+    if (n < 64) { keys[n] = OccKey{kern, dev, bytes, cluster}; vals[n] = v; ++n; }
+    return v;
+}
+
+template <int L, int RT, int S, bool CLUSTER, int MINB = 1>
+static cudaError_t launch_tma_ring(const LaunchCtx& c, const cplx* src, cplx* dst, const cplx* table_step, int E,
+                                   const EpilogueArgs& ea) {
+    constexpr int NS = 32 * L, NW = 8 / RT;
+    const int CL = c.n_theta / NS;
+    if (c.n_theta % NS != 0 || (CLUSTER ? (CL < 2 || CL > 16) : CL != 1)) return cudaErrorNotSupported;
+    const int64_t items = int64_t(c.n_freq) * c.n_tiles;
+    if (items > 0x7fffffff) return cudaErrorNotSupported;
+    CUtensorMap tm_src, tm_dst;
+    if (!ring_tensor_map(&tm_src, src, c.n_theta, L, items) || !ring_tensor_map(&tm_dst, dst, c.n_theta, L, items))
+        return cudaErrorNotSupported;
+    const int tab_elems = RING_HDR + L + 1 + (CLUSTER ? std::max(32, 32 * (CL - 1) + 1) : 32);
+    if (tab_elems > E) return cudaErrorNotSupported;
+    const int tab_pad = (tab_elems + 7) & ~7;
+    const size_t bytes = 1024 + sizeof(cplx) * (size_t(S) * NS * 8 + size_t(S) * tab_pad + (CLUSTER ? 512 : 0)) +
+                         sizeof(uint64_t) * (2 * S + (CLUSTER ? 4 * NW : 0));
+    if (bytes > 227 * 1024) return cudaErrorNotSupported;
+    auto kern = k_azimuth_tma<L, RT, S, CLUSTER, MINB>;
+    cudaError_t e = set_smem(kern, bytes);
+    if (e != cudaSuccess) return e;
+    const int nthr = 32 * (NW + 1);
+    if constexpr (!CLUSTER) {
+        const int per_sm = cached_occupancy(reinterpret_cast<const void*>(kern), bytes, 1, nthr, nullptr);
+        if (per_sm < 1) return cudaErrorInvalidConfiguration;
+        const int64_t ctas = int64_t(c.num_sms) * per_sm;
+        int per = int((items + ctas - 1) / ctas);
+        if (items <= 2 * ctas) per = 1;               // few items: let the block scheduler balance the tail
+        const int grid = int((items + per - 1) / per);
+        return launch_pdl(c.pdl != 0, kern, dim3(grid), dim3(nthr), bytes, c.stream, tm_src, tm_dst, table_step, E,
+                          tab_elems, c.n_theta, c.n_tiles, c.n_depth, items, per, ea);
+    } else {
+        if (CL > 8) {
+            e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            if (e != cudaSuccess) return e;
+        }
+        cudaLaunchConfig_t cfg = {};
+        cfg.blockDim = dim3(nthr);
+        cfg.dynamicSmemBytes = bytes;
+        cfg.stream = c.stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = CL;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        cfg.gridDim = dim3(CL * c.num_sms);
+        const int resident = cached_occupancy(reinterpret_cast<const void*>(kern), bytes, CL, nthr, &cfg);
+        if (resident < 1) return cudaErrorInvalidConfiguration;
+        if (getenv("PE3D_DEBUG_CLUSTER"))
+            fprintf(stderr, "pe3d: TMA cluster ring L=%d CL=%d resident clusters=%d\n", L, CL, resident);
+        const int per = int((items + resident - 1) / resident);
+        const int clusters = int((items + per - 1) / per);
+        cfg.gridDim = dim3(clusters * CL);
+        return cudaLaunchKernelEx(&cfg, kern, tm_src, tm_dst, table_step, E, tab_elems, c.n_theta, c.n_tiles,
+                                  c.n_depth, items, per, ea);
+    }
+}
+
 template <int L, int RT, int STAGES>
 static cudaError_t launch_warp_ring(const LaunchCtx& c, const cplx* src, cplx* dst, const cplx* table_step, int E,
                                    double r_new, const EpilogueArgs& ea) {
@@ -1225,7 +1634,7 @@ static cudaError_t launch_cluster_ring(const LaunchCtx& c, const cplx* src, cplx
     constexpr int NS = 32 * L;
     const int CL = c.n_theta / NS;
     const int nthr = 32 * 8 / RT;
-    const size_t bytes = sizeof(cplx) * (size_t(STAGES) * NS * 8 + 4 + (L + 1) + 33 + 4 * 128 + 17) + 4 * sizeof(uint64_t);
+    const size_t bytes = sizeof(cplx) * (size_t(STAGES) * NS * 8 + RING_HDR + (L + 1) + 33 + 4 * 128 + 17) + 4 * sizeof(uint64_t);
     cudaError_t e = set_smem(kern, bytes);
     if (e != cudaSuccess) return e;
     if (CL > 8) {
@@ -1271,6 +1680,37 @@ static cudaError_t launch_cluster_ring(const LaunchCtx& c, const cplx* src, cplx
 cudaError_t launch_azimuth_scan(const LaunchCtx& c, const cplx* src, cplx* dst, const cplx* table_step, double r_new,
                                 const EpilogueArgs& ea) {
     const RingPlan plan = ring_plan(c.n_theta);
+    const bool standard = ea.chunk_gap == 0 && (ea.chunk_cols == 0 || ea.chunk_cols == c.n_theta) && !ea.peer[0] &&
+                          ea.row_offset == 0;
+    if (standard && ea.periodic && (plan.kind == 0 || plan.kind == 2) && !getenv("PE3D_RING_CPASYNC")) {
+        // TMA + warp-specialised sweep; falls through to the cp.async kernels
+        // only when the tensor map cannot describe the ring
+        cudaError_t e = cudaErrorNotSupported;
+        const int E = plan.lay.E;
+        if (plan.kind == 0) {
+            switch (plan.L) {
+                case 2: e = launch_tma_ring<2, 2, 3, false>(c, src, dst, table_step, E, ea); break;
+                case 4: e = launch_tma_ring<4, 2, 3, false>(c, src, dst, table_step, E, ea); break;
+                case 8: {
+                    // variants for A/B timing (PE3D_RING_TMA): 0 = 3 stages, 2 CTAs/SM (default);
+                    // 1 = 2 stages, 3 CTAs/SM; 2 = one row per warp (8 consumer warps), 2 CTAs/SM
+                    const char* v = getenv("PE3D_RING_TMA");
+                    const int var = v ? atoi(v) : 0;
+                    if (var == 1) e = launch_tma_ring<8, 2, 2, false, 3>(c, src, dst, table_step, E, ea);
+                    else if (var == 2) e = launch_tma_ring<8, 1, 2, false, 2>(c, src, dst, table_step, E, ea);
+                    else e = launch_tma_ring<8, 2, 3, false, 2>(c, src, dst, table_step, E, ea);
+                    break;
+                }
+                case 16: e = launch_tma_ring<16, 1, 2, false>(c, src, dst, table_step, E, ea); break;
+                default: break;
+            }
+        } else if (plan.L == 16) {
+            e = launch_tma_ring<16, 1, 2, true>(c, src, dst, table_step, E, ea);
+        } else {
+            e = launch_tma_ring<8, 2, 2, true>(c, src, dst, table_step, E, ea);
+        }
+        if (e != cudaErrorNotSupported) return e;
+    }
     if (plan.kind == 2 && ea.periodic) {
         // 512-azimuth segments: single-stage CTAs (64 KB, 128 registers), two per
         // SM, so the second CTA hides the first one's loads (measured faster at
