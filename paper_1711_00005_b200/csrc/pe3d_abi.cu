@@ -136,7 +136,14 @@ cudaError_t enqueue_group(Handle* h, const pe3d_grid* g, const MarchPlan& p, int
     cg.fdev = c.fdev + f0;
     cg.loc_tab = c.loc_tab + int64_t(f0) * c.n_tiles * 8;
     cg.mul_tab = c.mul_tab + int64_t(f0) * c.n_tiles * 8;
-    if (c.k1_tab) cg.k1_tab = c.k1_tab + pe3d::k1_tab_elems(f0, c.n_tiles);
+    if (c.k1_tab)
+        cg.k1_tab = c.k1_tab + (c.split ? int64_t(f0) * c.split * pe3d::k1_stride(128) : pe3d::k1_tab_elems(f0, c.n_tiles));
+    if (c.split) {
+        cg.sp_tot = c.sp_tot + int64_t(f0) * c.split * c.n_theta * 2;
+        cg.sp_aq = c.sp_aq + int64_t(f0) * c.n_tiles * 16;
+        cg.sp_pa = c.sp_pa + int64_t(f0) * c.split * 3;
+        cg.sp_cd = c.sp_cd + int64_t(f0) * c.split * 2 * c.n_theta;
+    }
     cg.stream = st;
     // programmatic dependent launch of the step sweeps: each sweep's table
     // loads and CTA launch overlap the previous sweep's tail (8 frequencies
@@ -156,6 +163,10 @@ cudaError_t enqueue_group(Handle* h, const pe3d_grid* g, const MarchPlan& p, int
         const double r_new = g->r_start + j_new * g->delta_r;      // Grid3D.range_at
         cudaError_t e = prof.run(0, [&] { return pe3d::launch_depth_scan(ck1, A, B); });
         if (e != cudaSuccess) return e;
+        if (c.split) {                                      // exact sub-column carries for the azimuth sweep
+            e = prof.run(2, [&] { return pe3d::launch_split_carry(cg); });
+            if (e != cudaSuccess) return e;
+        }
         pe3d::EpilogueArgs ea{};
         const bool record = ((s + 1) % g->output_stride) == 0;
         const int k = (s + 1) / g->output_stride;          // sample index
@@ -345,12 +356,11 @@ int pe3d_handle_destroy(void* handle) {
     Handle* h = static_cast<Handle*>(handle);
     if (!h) return PE3D_OK;
     cudaSetDevice(h->device);
-    for (DevBuf* b : {&h->field_a, &h->field_b, &h->field_c, &h->loc_tab, &h->mul_tab, &h->k1_tab, &h->fdev, &h->w_abs, &h->err,
-                      &h->az_cp, &h->az_inv, &h->az_q, &h->az_ring, &h->fail_row, &h->fail_mag, &h->ring_tab, &h->h_local,
-                      &h->h_local2, &h->h_u0, &h->h_final, &h->h_tl, &h->h_snap, &h->h_clamped, &h->sb_in, &h->sb_x,
-                      &h->sb_cp, &h->sb_inv, &h->sb_y, &h->sb_q, &h->med_prof, &h->med_lat, &h->med_local, &h->slab_flags})
-        b->release();
+    for (DevBuf* b : h->buffers()) b->release();
     if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
+    for (int k = 0; k <= Handle::MAX_CHAINS; ++k)
+        if (h->tl_side[k]) cudaStreamDestroy(h->tl_side[k]);
+    for (cudaEvent_t e : h->tl_ev) cudaEventDestroy(e);
     for (int k = 0; k < Handle::MAX_CHAINS; ++k) {
         if (h->chain_stream[k]) cudaStreamDestroy(h->chain_stream[k]);
         if (h->chain_join[k]) cudaEventDestroy(h->chain_join[k]);
@@ -439,6 +449,17 @@ static int march_device_impl(void* handle, const pe3d_grid* g, const pe3d_coeffs
     c.k1_tab = k1_table ? h->k1_tab.as<cplx>() : nullptr;
     c.err = h->err.as<pe3d::DevError>();
     c.stream = stream;
+    if (!p.serial && g->n_steps > 0) c.split = pe3d::depth_split_plan(c, g->topology == PE3D_PERIODIC);
+    if (c.split) {
+        CK(h->sp_tot.ensure(int64_t(F) * c.split * NT * 2 * sizeof(cplx)), "alloc split");
+        CK(h->sp_aq.ensure(int64_t(F) * n_tiles * 16 * sizeof(cplx)), "alloc split");
+        CK(h->sp_pa.ensure(int64_t(F) * c.split * 3 * sizeof(cplx)), "alloc split");
+        CK(h->sp_cd.ensure(int64_t(F) * c.split * 2 * NT * sizeof(cplx)), "alloc split");
+        c.sp_tot = h->sp_tot.as<cplx>();
+        c.sp_aq = h->sp_aq.as<cplx>();
+        c.sp_pa = h->sp_pa.as<cplx>();
+        c.sp_cd = h->sp_cd.as<cplx>();
+    }
 
     const cplx* local = reinterpret_cast<const cplx*>(d_local);
     Prof prof{h, (g->flags & PE3D_FLAG_PROFILE) != 0, stream, {}};
@@ -486,9 +507,15 @@ static int march_device_impl(void* handle, const pe3d_grid* g, const pe3d_coeffs
         add(tabs, sizeof(tabs));
         const int chains = step_chains(p.ctx, false);
         add(&chains, sizeof(chains));
+        // any workspace reallocation (also by other entry points on this handle)
+        // may have moved a buffer the graph's kernels address
+        const uint64_t gen = h->alloc_generation();
+        add(&gen, sizeof(gen));
+        add(&p.ctx.split, sizeof(p.ctx.split));
         // the A/B switches pick kernels and launch attributes baked into the graph
         for (const char* name : {"PE3D_NO_PDL", "PE3D_CLUSTER_L", "PE3D_DEPTH_NO_CLUSTER", "PE3D_DEPTH_NO_TMA",
-                                 "PE3D_DEPTH_WIDE_SCAN", "PE3D_RING_BLOCK", "PE3D_RING_STAGES"}) {
+                                 "PE3D_DEPTH_WIDE_SCAN", "PE3D_RING_BLOCK", "PE3D_RING_STAGES", "PE3D_RING_CPASYNC",
+                                 "PE3D_RING_TMA", "PE3D_DEPTH_NO_SPLIT"}) {
             const char* v = getenv(name);
             const std::string val = v ? std::string("=") + v : std::string("-");
             add(val.data(), val.size() + 1);
@@ -931,6 +958,8 @@ int pe3d_march_medium_host(void* handle, const pe3d_grid* g, const pe3d_coeffs* 
         add(&s, sizeof(s));
         const int flags2[2] = {pre ? 1 : 0, scan_path ? 1 : 0};
         add(flags2, sizeof(flags2));
+        const uint64_t gen = h->alloc_generation();        // fdev, err, az_*, fail_mag ... not moved since capture
+        add(&gen, sizeof(gen));
         if (!(h->graph_exec && key == h->graph_key)) {
             if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
             h->graph_exec = nullptr;

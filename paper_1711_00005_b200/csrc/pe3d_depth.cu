@@ -396,12 +396,19 @@ struct DepthDst {
 // last tile), completion on a per-warp mbarrier, and one TMA bulk store of
 // the solved column from the same stage.  The warps issue no per-line
 // copies at all; a 3-deep per-warp stage ring keeps two columns in flight.
-template <int STAGES, int MINB, int MAXT, int NTH = 0, bool TAB = false>
+//
+// SPLIT (long columns, LaunchCtx::split): the launch sees every 1024-row
+// sub-column s of frequency f as a column of virtual frequency f*split + s;
+// rows across sub-column edges enter the depth stencil as halo values read
+// from the input one column ahead (edge threads), the sub-column is solved
+// with zero carries, and its bottom y and top x go to sp_tot for
+// k_split_carry.
+template <int STAGES, int MINB, int MAXT, int NTH = 0, bool TAB = false, bool SPLIT = false>
 __global__ void __launch_bounds__(MAXT, MINB)
 k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ DepthDst tm_dst,
             const cplx* __restrict__ loc_tab, const cplx* __restrict__ mul_tab, const FreqDev* __restrict__ fdev,
             const cplx* __restrict__ k1_tab, int n_theta, int n_tiles, int64_t total_cols, int cols_per_cta,
-            int sector) {
+            int sector, const cplx* __restrict__ src_raw, int split, cplx* __restrict__ sp_tot) {
     constexpr int RPT = 8;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     const int nthreads = NTH ? NTH : int(blockDim.x);   // compile-time when NTH: constant table offsets
@@ -493,6 +500,16 @@ k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ 
             }
         }
     }
+    // SPLIT: the stencil rows across the sub-column edges, one column ahead
+    // (thread 0: the row above the sub-column, the last thread: the row below)
+    const bool edge_thread = SPLIT && (t == 0 || t == nthreads - 1);
+    auto halo_load = [&](int hf, int hc) -> cplx {
+        const int hs = hf % split;
+        if (t == 0) return hs > 0 ? ldc(src_raw + ((int64_t(hf) * n_tiles - 1) * n_theta + hc) * 8 + 7) : czero();
+        return hs < split - 1 ? ldc(src_raw + ((int64_t(hf) * n_tiles + n_tiles) * n_theta + hc) * 8) : czero();
+    };
+    cplx hal = czero();
+    if (edge_thread) hal = halo_load(f, col);
 
     auto setup_freq = [&]() {
         if constexpr (TAB) {
@@ -545,6 +562,9 @@ k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ 
         }
         cplx* cur = stage + slot * 256;
         if (it == n_cols - 1) griddep_launch();     // last column: the next sweep may start launching
+        cplx hal_next = czero();
+        if (edge_thread && it + 1 < n_cols)
+            hal_next = col + 1 == n_theta ? halo_load(f + 1, 0) : halo_load(f, col + 1);
         PHASE(1);
         mbar_wait(&bars[slot], parity);
         PHASE(2);
@@ -563,6 +583,11 @@ k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ 
         if (lane == 0) up = warp > 0 ? sUp[warp - 1] : czero();
         if (lane == 31) dn = warp < nwarps - 1 ? sDn[warp + 1] : czero();
         if (t == 0) up = czero();
+        if (SPLIT) {
+            if (t == 0) up = hal;
+            if (t == nthreads - 1) dn = hal;
+            hal = hal_next;
+        }
 
         cplx b[RPT];
         if (sector && (col == 0 || col == n_theta - 1)) {
@@ -597,6 +622,7 @@ k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ 
         if (lane == 0) y = C;
 #pragma unroll
         for (int i = 0; i < RPT; ++i) { y = cfma(M[i], y, b[i]); b[i] = y; }
+        if (SPLIT && t == nthreads - 1) stc(sp_tot + (int64_t(f) * n_theta + col) * 2, y);   // zero-carry bottom y
 
         cplx X = czero();
 #pragma unroll
@@ -619,6 +645,7 @@ k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ 
         if (lane == 31) xv = D;
 #pragma unroll
         for (int i = RPT - 1; i >= 0; --i) { xv = cfma(M[i], xv, b[i]); b[i] = xv; }
+        if (SPLIT && t == 0) stc(sp_tot + (int64_t(f) * n_theta + col) * 2 + 1, xv);          // zero-carry top x
 
         PHASE(9);
         // ---- solved column back through the stage, one TMA store per warp
@@ -653,8 +680,9 @@ k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ 
 // every frequency it meets -- folded RHS coefficients, the column-independent
 // Kogge-Stone multipliers and warp products -- written as the k1_tab record
 // (pe3d_internal.h), so the sweep's frequency setup is loads only.
+// fdiv > 1: records of the virtual frequencies of split columns (fdev[f / fdiv]).
 __global__ void k_depth_setup(const cplx* __restrict__ loc_tab, const cplx* __restrict__ mul_tab,
-                              const FreqDev* __restrict__ fdev, int n_tiles, cplx* __restrict__ k1_tab) {
+                              const FreqDev* __restrict__ fdev, int n_tiles, cplx* __restrict__ k1_tab, int fdiv) {
     constexpr int RPT = 8;
     const int f = blockIdx.x;
     const int nthreads = blockDim.x, t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -667,7 +695,7 @@ __global__ void k_depth_setup(const cplx* __restrict__ loc_tab, const cplx* __re
     cplx* pincf = mb + 4 * nthreads;
     cplx* pincb = pincf + nthreads;
     cplx* spw = pincb + nthreads;
-    const FreqDev fd = fdev[f];
+    const FreqDev fd = fdev[f / fdiv];
     const cplx kappa = crecip(cneg(fd.off_z));
     const cplx beta = cmul(kappa, crmul(fd.s_z, fd.cx_rhs));
     cplx P = cone();
@@ -1113,7 +1141,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 // Generic tiled FLOAT64 map with the 128-B swizzle (used by the azimuth sweep's
 // ring maps, pe3d_ring.cu); false when the driver entry point or the encoder refuses.
 bool encode_swizzled_map(CUtensorMap* tm, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
-                         const uint32_t* box) {
+                         const uint32_t* box, int swizzle_bytes) {
     auto enc = tensor_map_encoder();
     if (!enc || rank < 1 || rank > 5) return false;
     cuuint64_t d[5], st[4];
@@ -1121,8 +1149,8 @@ bool encode_swizzled_map(CUtensorMap* tm, const void* base, int rank, const uint
     for (int i = 0; i < rank; ++i) { d[i] = dims[i]; b[i] = box[i]; e[i] = 1; }
     for (int i = 0; i + 1 < rank; ++i) st[i] = strides[i];
     return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, cuuint32_t(rank), const_cast<void*>(base), d, st, b, e,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+               CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 static bool field_tensor_map(CUtensorMap* tm, const void* base, const LaunchCtx& c) {
@@ -1152,7 +1180,7 @@ static bool depth_dst_maps(DepthDst* d, const void* dst, const LaunchCtx& c) {
     return true;
 }
 
-template <int STAGES, int MINB, int MAXT>
+template <int STAGES, int MINB, int MAXT, bool SPLIT = false>
 static cudaError_t launch_depth_tma_cfg(const LaunchCtx& c, const cplx* src, cplx* dst) {
     CUtensorMap tm_src;
     DepthDst tm_dst;
@@ -1163,9 +1191,11 @@ static cudaError_t launch_depth_tma_cfg(const LaunchCtx& c, const cplx* src, cpl
                          sizeof(uint64_t) * (nwarps * STAGES + 1);
     if (bytes > 227 * 1024) return cudaErrorNotSupported;
     const cplx* k1 = (c.k1_tab && c.n_tiles <= K1_TAB_MAX_TILES && nthreads == round32(c.n_tiles)) ? c.k1_tab : nullptr;
-    auto kern = (MAXT == 128 && nthreads == 128)
-                    ? (k1 ? k_depth_tma<STAGES, MINB, MAXT, 128, true> : k_depth_tma<STAGES, MINB, MAXT, 128>)
-                    : (k1 ? k_depth_tma<STAGES, MINB, MAXT, 0, true> : k_depth_tma<STAGES, MINB, MAXT>);
+    if (SPLIT && !(k1 && MAXT == 128 && nthreads == 128)) return cudaErrorNotSupported;
+    auto kern = SPLIT ? k_depth_tma<STAGES, MINB, MAXT, 128, true, true>
+                      : (MAXT == 128 && nthreads == 128)
+                            ? (k1 ? k_depth_tma<STAGES, MINB, MAXT, 128, true> : k_depth_tma<STAGES, MINB, MAXT, 128>)
+                            : (k1 ? k_depth_tma<STAGES, MINB, MAXT, 0, true> : k_depth_tma<STAGES, MINB, MAXT>);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
     if (e != cudaSuccess) return e;
     const int64_t total = int64_t(c.n_freq) * c.n_theta;
@@ -1179,7 +1209,7 @@ static cudaError_t launch_depth_tma_cfg(const LaunchCtx& c, const cplx* src, cpl
     const int per = int((total + ctas - 1) / ctas);
     const int grid = int((total + per - 1) / per);
     return launch_pdl(c.pdl != 0, kern, dim3(grid), dim3(nthreads), bytes, c.stream, tm_src, tm_dst, c.loc_tab,
-                      c.mul_tab, c.fdev, k1, c.n_theta, c.n_tiles, total, per, c.sector);
+                      c.mul_tab, c.fdev, k1, c.n_theta, c.n_tiles, total, per, c.sector, src, c.split, c.sp_tot);
 }
 
 static cudaError_t launch_depth_tma_cluster(const LaunchCtx& c, const cplx* src, cplx* dst, int CL) {
@@ -1242,7 +1272,125 @@ static cudaError_t launch_depth_tma(const LaunchCtx& c, const cplx* src, cplx* d
     return launch_depth_tma_cfg<2, 1, 512>(c, src, dst);
 }
 
+// ------------------------------------------------------ split long columns
+// Responses of one 1024-row sub-column to unit carries, once per march (one
+// thread per (f, s), rows [1024 s, 1024 (s + 1))): with y_l = m_l y_(l-1) + b_l
+// and x_l = m_l x_(l+1) + y_l, a carry c entering at the top adds
+// a_l c to x_l (p_l = m_l p_(l-1), p_(top-1) = 1; a_l = m_l a_(l+1) + p_l,
+// a_(bottom+1) = 0) and a carry d entering from below adds q_l d
+// (q_l = m_l q_(l+1), q_(bottom+1) = 1).  sp_pa[fs] = (P_s = prod m_l over the
+// sub-column = p_bottom = q_top, A_s = a_top, (a_span, q_span)).
+//
+// The responses decay geometrically away from the sub-column edges (|m_l| <
+// 1): rows where both |a_l| and |q_l| are below SPLIT_TAU take no correction
+// (a dropped term is below 1e-30 of the carry, i.e. of the field's scale;
+// the contract is 1e-9).  a_span = rows from the top with |a_l| >= tau,
+// q_span = rows from the bottom with |q_l| >= tau; a and q are zeroed
+// outside, so the azimuth sweep can skip whole tiles.
+constexpr double SPLIT_TAU = 1e-30;
+__global__ void k_split_setup(const cplx* __restrict__ mul_tab, int n_virtual, cplx* __restrict__ sp_aq,
+                              cplx* __restrict__ sp_pa) {
+    const int fs = blockIdx.x * blockDim.x + threadIdx.x;
+    if (fs >= n_virtual) return;
+    const cplx* m = mul_tab + int64_t(fs) * 1024;
+    cplx* aq = sp_aq + int64_t(fs) * 2048;          // (a_l, q_l) pairs of the sub-column's rows
+    cplx p = cone();
+    for (int l = 0; l < 1024; ++l) {
+        p = cmul(ldc(m + l), p);
+        stc(aq + 2 * l, p);                         // p_l, overwritten by a_l below
+    }
+    cplx a = czero(), q = cone();
+    int a_span = 0, q_span = 0;
+    for (int l = 1023; l >= 0; --l) {
+        const cplx ml = ldc(m + l);
+        a = cfma(ml, a, ldc(aq + 2 * l));
+        q = cmul(ml, q);
+        if (a_span == 0 && cabs(a) >= SPLIT_TAU) a_span = l + 1;
+        if (cabs(q) >= SPLIT_TAU) q_span = 1024 - l;
+        stc(aq + 2 * l, a);
+        stc(aq + 2 * l + 1, q);
+    }
+    const cplx A = a;
+    for (int l = 0; l < 1024; ++l) {                // exact zeros outside the spans
+        if (l >= a_span) stc(aq + 2 * l, czero());
+        if (l < 1024 - q_span) stc(aq + 2 * l + 1, czero());
+    }
+    stc(sp_pa + 3 * fs, p);
+    stc(sp_pa + 3 * fs + 1, A);
+    stc(sp_pa + 3 * fs + 2, mk(double(a_span), double(q_span)));
+}
+
+// Exact carries of every sub-column from the zero-carry totals, one thread
+// per (f, column):  cin_0 = 0, cin_(s+1) = T_s + P_s cin_s;  din_(CL-1) = 0,
+// din_(s-1) = X_s + A_s cin_s + P_s din_s.  Written lane-ordered for the
+// azimuth sweep's stage (azimuth m = seg*NS + q*L + k at seg*NS + k*32 + q).
+constexpr int SPLIT_MAX = 8;
+__global__ void __launch_bounds__(256) k_split_carry(const cplx* __restrict__ sp_tot, const cplx* __restrict__ sp_pa,
+                                                     cplx* __restrict__ sp_cd, int n_freq, int n_theta, int split,
+                                                     int L) {
+    griddep_wait();                                 // the depth sweep's totals
+    const int64_t gid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (gid >= int64_t(n_freq) * n_theta) return;
+    const int f = int(gid / n_theta), m = int(gid - int64_t(f) * n_theta);
+    const int NS = 32 * L;
+    const int seg = m / NS, w = m - seg * NS;
+    const int mp = seg * NS + (w % L) * 32 + w / L;
+    cplx cin[SPLIT_MAX], T[SPLIT_MAX], X[SPLIT_MAX], P[SPLIT_MAX], A[SPLIT_MAX];
+#pragma unroll
+    for (int s = 0; s < SPLIT_MAX; ++s) {
+        if (s < split) {
+            const int64_t fs = int64_t(f) * split + s;
+            T[s] = ldc(sp_tot + (fs * n_theta + m) * 2);
+            X[s] = ldc(sp_tot + (fs * n_theta + m) * 2 + 1);
+            P[s] = ldc(sp_pa + 3 * fs);
+            A[s] = ldc(sp_pa + 3 * fs + 1);
+        }
+    }
+    cplx c = czero();
+#pragma unroll
+    for (int s = 0; s < SPLIT_MAX; ++s) {
+        if (s < split) {
+            cin[s] = c;
+            c = cfma(P[s], c, T[s]);
+        }
+    }
+    cplx d = czero();
+#pragma unroll
+    for (int s = SPLIT_MAX - 1; s >= 0; --s) {
+        if (s < split) {
+            cplx* o = sp_cd + (int64_t(f) * split + s) * 2 * n_theta;
+            stc(o + mp, cin[s]);
+            stc(o + n_theta + mp, d);
+            d = cfma(A[s], cin[s], cfma(P[s], d, X[s]));
+        }
+    }
+}
+
+int depth_split_plan(const LaunchCtx& c, int periodic) {
+    const int CL = c.n_tiles / 128;
+    if (!periodic || c.sector || c.n_peers > 0 || !c.k1_tab || c.n_tiles % 128 != 0 || CL < 2 || CL > SPLIT_MAX)
+        return 0;
+    if (ring_segment(c.n_theta) == 0 || !tensor_map_encoder()) return 0;
+    for (const char* name : {"PE3D_DEPTH_NO_SPLIT", "PE3D_RING_CPASYNC", "PE3D_DEPTH_NO_TMA", "PE3D_DEPTH_WIDE_SCAN"})
+        if (getenv(name)) return 0;
+    return CL;
+}
+
+cudaError_t launch_split_carry(const LaunchCtx& c) {
+    const int64_t n = int64_t(c.n_freq) * c.n_theta;
+    return launch_pdl(c.pdl != 0, k_split_carry, dim3(unsigned((n + 255) / 256)), dim3(256), 0, c.stream, c.sp_tot,
+                      c.sp_pa, c.sp_cd, c.n_freq, c.n_theta, c.split, ring_segment(c.n_theta) / 32);
+}
+
 cudaError_t launch_depth_scan(const LaunchCtx& c, const cplx* src, cplx* dst) {
+    if (c.split >= 2) {
+        // every 1024-row sub-column as a column of its own virtual frequency
+        LaunchCtx v = c;
+        v.n_freq = c.n_freq * c.split;
+        v.n_tiles = 128;
+        v.n_depth = 1024;
+        return launch_depth_tma_cfg<3, 3, 128, true>(v, src, dst);
+    }
     const int64_t total = int64_t(c.n_freq) * c.n_theta;
     auto go = [&](auto kern, int nthreads, size_t elems, int per_sm) -> cudaError_t {
         const size_t sm = sizeof(cplx) * elems;
@@ -1273,8 +1421,17 @@ cudaError_t launch_depth_scan(const LaunchCtx& c, const cplx* src, cplx* dst) {
 // recurrence when PE3D_FACTOR_SERIAL is set (it was 0.46 ms per cfg4 march).
 static cudaError_t launch_depth_setup(const LaunchCtx& c) {
     if (!c.k1_tab) return cudaSuccess;
+    if (c.split >= 2) {
+        // 1024-row sub-columns as virtual frequencies, plus the carry responses
+        k_depth_setup<<<c.n_freq * c.split, 128, 0, c.stream>>>(c.loc_tab, c.mul_tab, c.fdev, 128, c.k1_tab, c.split);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        k_split_setup<<<(c.n_freq * c.split + 31) / 32, 32, 0, c.stream>>>(c.mul_tab, c.n_freq * c.split, c.sp_aq,
+                                                                             c.sp_pa);
+        return cudaGetLastError();
+    }
     if (c.n_tiles <= K1_TAB_MAX_TILES)
-        k_depth_setup<<<c.n_freq, round32(c.n_tiles), 0, c.stream>>>(c.loc_tab, c.mul_tab, c.fdev, c.n_tiles, c.k1_tab);
+        k_depth_setup<<<c.n_freq, round32(c.n_tiles), 0, c.stream>>>(c.loc_tab, c.mul_tab, c.fdev, c.n_tiles, c.k1_tab, 1);
     else if (k1_tab_elems(c.n_freq, c.n_tiles) > 0)
         k_depth_setup_cluster<<<c.n_freq * (c.n_tiles / 128), 128, 0, c.stream>>>(c.loc_tab, c.mul_tab, c.fdev,
                                                                                  c.n_tiles, c.k1_tab);

@@ -22,11 +22,13 @@ using pe3d::cplx;
 struct DevBuf {
     void* ptr = nullptr;
     size_t bytes = 0;
+    uint64_t gen = 0;           // bumped on every (re)allocation: part of the cached graph's key
     cudaError_t ensure(size_t want) {
         if (want <= bytes) return cudaSuccess;
         if (ptr) cudaFree(ptr);
         ptr = nullptr;
         bytes = 0;
+        ++gen;
         cudaError_t e = cudaMalloc(&ptr, want);
         if (e == cudaSuccess) bytes = want;
         return e;
@@ -55,6 +57,21 @@ struct Handle {
     DevBuf med_prof, med_lat, med_local;
     // slab march: ordering counters of the peer-direct transposes
     DevBuf slab_flags;
+    // split long columns (LaunchCtx::split): totals, carry responses, carries
+    DevBuf sp_tot, sp_aq, sp_pa, sp_cd;
+    // every workspace buffer (release, allocation generation)
+    std::vector<DevBuf*> buffers() {
+        return {&field_a, &field_b, &field_c, &loc_tab, &mul_tab, &fdev, &w_abs, &err, &k1_tab, &az_cp, &az_inv,
+                &az_q, &az_ring, &fail_row, &fail_mag, &ring_tab, &h_local, &h_local2, &h_u0, &h_final, &h_tl,
+                &h_snap, &h_clamped, &sb_in, &sb_x, &sb_cp, &sb_inv, &sb_y, &sb_q, &med_prof, &med_lat, &med_local,
+                &slab_flags, &sp_tot, &sp_aq, &sp_pa, &sp_cd};
+    }
+    // changes whenever any workspace buffer was reallocated since the last call
+    uint64_t alloc_generation() {
+        uint64_t g = 0;
+        for (DevBuf* b : buffers()) g += b->gen;
+        return g;
+    }
     // one cached step-loop graph (reused when a march repeats with identical arguments)
     std::vector<unsigned char> graph_key;
     cudaGraphExec_t graph_exec = nullptr;

@@ -99,6 +99,20 @@ struct LaunchCtx {
     // Launch the step-loop sweeps with programmatic stream serialization
     // (PDL): a sweep's independent prologue overlaps the previous sweep's tail.
     int pdl;
+    // Split long columns (SURVEY §8(a) a11-a12 for n_depth = 128*8*split rows,
+    // cfg5): when split >= 2 the depth sweep solves every 1024-row sub-column on
+    // its own with zero carries (virtual frequency fs = f*split + s, the
+    // k_depth_tma kernel of 1024-row columns), records per (fs, column) its
+    // zero-carry bottom y and top x in sp_tot, k_split_carry turns those into
+    // the exact carries entering every sub-column (sp_cd, lane-ordered for the
+    // azimuth sweep), and the azimuth sweep applies x = x0 + a_l cin + q_l din
+    // to every element it loads (sp_aq: per (f, row) responses to unit carries;
+    // sp_pa: per (f, s) product of the multipliers and the top response).
+    int split;
+    cplx* sp_tot;           // [F*split][n_theta][2]
+    cplx* sp_aq;            // [F][n_tiles*8][2]
+    cplx* sp_pa;            // [F*split][3]: P_s, A_s, (a_span, q_span) rows needing the correction
+    cplx* sp_cd;            // [F][split][2][n_theta]
     int n_peers;
     int peer_tiles;
     cplx* peer_dst[MAX_PEERS];
@@ -147,7 +161,7 @@ inline cudaError_t launch_pdl(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 
 }
 
 bool encode_swizzled_map(CUtensorMap* tm, const void* base, int rank, const uint64_t* dims,
-                         const uint64_t* strides, const uint32_t* box);
+                         const uint64_t* strides, const uint32_t* box, int swizzle_bytes);
 cudaError_t launch_slab_signal(unsigned long long* const* flags, int n, cudaStream_t s);
 cudaError_t launch_slab_wait(const unsigned long long* flag, unsigned long long target, cudaStream_t s);
 void ring_shape(int n_theta, int* L, int* RW);
@@ -155,6 +169,11 @@ int ring_table_elems(int n_theta);   // complex entries per (step, frequency) ri
 cudaError_t launch_factor_depth(const LaunchCtx& c, const cplx* local, int64_t local_fstride, int step_for_error);
 cudaError_t launch_factor_depth_scan(const LaunchCtx& c, const cplx* local, int64_t local_fstride, int step_for_error);
 cudaError_t launch_depth_scan(const LaunchCtx& c, const cplx* src, cplx* dst);
+// Split-column plan for a march (0: no split) and the per-step carry kernel.
+int depth_split_plan(const LaunchCtx& c, int periodic);
+cudaError_t launch_split_carry(const LaunchCtx& c);
+// segment length of the TMA ring kernel serving n_theta (the lane order of sp_cd)
+int ring_segment(int n_theta);
 cudaError_t launch_ring_setup(const LaunchCtx& c, cplx* table, int n_steps, int first_index, double r_start,
                               double delta_r);
 cudaError_t launch_azimuth_scan(const LaunchCtx& c, const cplx* src, cplx* dst, const cplx* table_step, double r_new,

@@ -998,14 +998,30 @@ k_azimuth_cluster(const cplx* __restrict__ src, cplx* __restrict__ dst, const cp
 // the segments are joined exactly as in k_azimuth_cluster, with one pair of
 // exchange mbarriers per consumer warp (a warp's RT rows are exchanged only
 // with the same warp of the peer CTAs), double-buffered by item parity.
-template <int L>
 __device__ __forceinline__ int tma_slot(int q, int k, int r) { return ((k * 32 + q) << 3) + (r ^ (q & 7)); }
 
-template <int L, int RT, int S, bool CLUSTER, int MINB>
-__global__ void __launch_bounds__(32 * (8 / RT + 1), MINB)
+//
+// CORR (split long columns, LaunchCtx::split): the depth sweep left the
+// zero-carry sub-column solutions x0; with every segment the producer also
+// copies the exact carries cin/din of the item's (f, sub-column, segment)
+// (k_split_carry, already in lane order) and the rows' unit-carry responses
+// (a_l, q_l), and the consumers load x = x0 + a_l cin + q_l din.  (Measured
+// and not kept: three extra "fixer" warps applying the correction to the
+// staged segment in place, releasing it on a second mbarrier -- cfg5 azimuth
+// sweep 149 -> 181 us; the fixers' pass lands on the item pipeline's path.)
+//
+// (Measured and not kept: half-tile items -- 4 rows, 64-B swizzle, two
+// cluster CTAs per SM instead of one: cfg5 azimuth sweep 136 us either way,
+// 147 -> 237 us with the split-column correction.)
+template <int RT>
+__host__ __device__ constexpr int ring_tma_threads() { return 32 * (8 / RT + 1); }
+
+template <int L, int RT, int S, bool CLUSTER, int MINB, bool CORR = false>
+__global__ void __launch_bounds__(ring_tma_threads<RT>(), MINB)
 k_azimuth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ CUtensorMap tm_dst,
               const cplx* __restrict__ table, int E, int tab_elems, int n_theta, int n_tiles, int n_depth,
-              int64_t total_items, int items_per_unit, EpilogueArgs ea) {
+              int64_t total_items, int n_units, EpilogueArgs ea, const cplx* __restrict__ sp_cd,
+              const cplx* __restrict__ sp_aq, const cplx* __restrict__ sp_pa, int split, int tile_perm) {
     namespace cg = cooperative_groups;
     constexpr int NW = 8 / RT;                      // consumer warps; warp NW is the TMA producer
     constexpr int NS = 32 * L;                      // segment length
@@ -1015,11 +1031,18 @@ k_azimuth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant_
     cplx* stage = reinterpret_cast<cplx*>(smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u));
     const int tab_pad = (tab_elems + 7) & ~7;
     cplx* tabs = stage + S * ITEM;                  // [S][tab_pad]
-    cplx* segW = tabs + S * tab_pad;                // cluster: [2][16][8] forward totals
+    // CORR: per slot the carries cin[NS], din[NS] of the item's (f, sub-column,
+    // segment) and the (a_l, q_l) of its 8 rows, copied with every item (measured
+    // faster than keeping one copy per run of items of a sub-column: 149 vs 158 us
+    // at cfg5)
+    constexpr int CORRE = CORR ? 2 * NS + 16 : 0;
+    cplx* corr = tabs + S * tab_pad;                // [S][CORRE]
+    cplx* segW = corr + S * CORRE;                  // cluster: [2][16][8] forward totals
     cplx* segX = segW + (CLUSTER ? 2 * 16 * 8 : 0); // cluster: [2][16][8] backward totals
     uint64_t* full = reinterpret_cast<uint64_t*>(segX + (CLUSTER ? 2 * 16 * 8 : 0));
     uint64_t* empty = full + S;
     uint64_t* xbar = empty + S;                     // cluster: [NW][4]: fwd buf 0/1, bwd buf 0/1
+    int* need = reinterpret_cast<int*>(xbar + (CLUSTER ? 4 * NW : 0));   // CORR: [S] the slot's item is corrected
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     int CL = 1, s = 0;
     if constexpr (CLUSTER) {
@@ -1027,12 +1050,17 @@ k_azimuth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant_
         CL = int(cluster.num_blocks());
         s = int(cluster.block_rank());
     }
-    // item indices fit an int (checked by the launcher): no 64-bit division in the loop
+    // item indices fit an int (checked by the launcher): no 64-bit division in the loop.
+    // CTA u of the plain kernel takes items u, u + G, u + 2G, ... (strided: at any time
+    // the grid streams through one contiguous stretch of the field; cfg4 azimuth sweep
+    // 100.8 -> 96.3 us against contiguous ranges; the ring table rides with every
+    // item, so frequency switches cost nothing).  Cluster u takes the contiguous range
+    // [u * per, (u + 1) * per) (strided measured 137 -> 148 us at cfg5).
     const int unit = CLUSTER ? int(blockIdx.x) / CL : int(blockIdx.x);
-    const int it0 = unit * items_per_unit;
-    const int it1 = it0 + items_per_unit < int(total_items) ? it0 + items_per_unit : int(total_items);
-    if (it0 >= it1) return;                         // uniform over a cluster
-    const int N = it1 - it0;
+    const int G = CLUSTER ? 1 : n_units;
+    const int first = CLUSTER ? unit * n_units : unit;
+    if (first >= int(total_items)) return;          // uniform over a cluster
+    const int N = CLUSTER ? min(n_units, int(total_items) - first) : (int(total_items) - unit + G - 1) / G;
     if (tid == 0) {
 #pragma unroll
         for (int k = 0; k < S; ++k) {
@@ -1051,19 +1079,49 @@ k_azimuth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant_
         if (lane == 0) {
             griddep_wait();                         // the field belongs to the previous sweep until here
             const unsigned tab_bytes = unsigned(tab_elems) * unsigned(sizeof(cplx));
+            int span_fs = -1, a_span = 0, q_span = 0;
             auto load = [&](int n, int slot) {
-                const int item = it0 + n;
+                const int item = first + n * G;
                 const int f = item / n_tiles;
-                mbar_expect_tx(&full[slot], ITEM_BYTES + tab_bytes);
-                tma_load_5d(stage + slot * ITEM, &tm_src, 0, 0, 0, s, item, &full[slot]);
+                const int titem = f * n_tiles + (item - f * n_tiles) * tile_perm % n_tiles;   // permuted tile
+                bool corr_item = false;
+                if constexpr (CORR) {
+                    // rows [r0, r0 + 8) of the sub-column: inside a carry-response span?
+                    const int tile = titem - f * n_tiles, tps = n_tiles / split;
+                    const int sub = tile / tps, r0 = (tile - sub * tps) * 8;
+                    const int fs = f * split + sub;
+                    if (fs != span_fs) {
+                        const cplx sp = ldc(sp_pa + 3 * fs + 2);
+                        span_fs = fs;
+                        a_span = int(sp.re);
+                        q_span = int(sp.im);
+                    }
+                    corr_item = (sub > 0 && r0 < a_span) || (sub < split - 1 && r0 + 8 > tps * 8 - q_span);
+                    need[slot] = corr_item ? 1 : 0;    // published by the arrive below (release)
+                }
+                const unsigned corr_bytes = corr_item ? CORRE * unsigned(sizeof(cplx)) : 0u;
+                mbar_expect_tx(&full[slot], ITEM_BYTES + tab_bytes + corr_bytes);
+                tma_load_5d(stage + slot * ITEM, &tm_src, 0, 0, 0, s, titem, &full[slot]);
                 bulk_load(tabs + slot * tab_pad, table + int64_t(f) * E, tab_bytes, &full[slot]);
+                if (CORR && corr_item) {
+                    const int tile = titem - f * n_tiles;
+                    const int sub = tile / (n_tiles / split);
+                    const cplx* cd = sp_cd + (int64_t(f) * split + sub) * 2 * n_theta + s * NS;
+                    cplx* dstc = corr + slot * CORRE;
+                    bulk_load(dstc, cd, NS * unsigned(sizeof(cplx)), &full[slot]);
+                    bulk_load(dstc + NS, cd + n_theta, NS * unsigned(sizeof(cplx)), &full[slot]);
+                    bulk_load(dstc + 2 * NS, sp_aq + (int64_t(f) * n_tiles + tile) * 16, 16 * unsigned(sizeof(cplx)),
+                              &full[slot]);
+                }
             };
             for (int p = 0; p < S && p < N; ++p) load(p, p);
             for (int n = 0; n < N; ++n) {
                 const int slot = n % S;
                 mbar_wait(&empty[slot], unsigned(n / S) & 1u);      // consumers wrote the temp (or are done)
                 if (ea.write_temp) {
-                    tma_store_5d(&tm_dst, 0, 0, 0, s, it0 + n, stage + slot * ITEM);
+                    const int item = first + n * G, f = item / n_tiles;
+                    tma_store_5d(&tm_dst, 0, 0, 0, s, f * n_tiles + (item - f * n_tiles) * tile_perm % n_tiles,
+                                 stage + slot * ITEM);
                     bulk_commit();
                 }
                 if (n + S < N) {
@@ -1077,15 +1135,16 @@ k_azimuth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant_
         griddep_launch();
     } else {
         // ------------------------------------------------ consumer warps
-        const int q = lane, swz = q & 7;
+        const int q = lane;
         const int m0 = q * L, mseg = s * NS;
         const unsigned exch_bytes = unsigned(CL) * RT * unsigned(sizeof(cplx));
         auto push = [&](cplx* table_, uint64_t* bar, int row, cplx val) {
             if (lane < CL) st_async_cplx(mapa_shared(smem_addr(table_ + s * 8 + row), lane), val,
                                          mapa_shared(smem_addr(bar), lane));
         };
-        int f = it0 / n_tiles, tile = it0 - f * n_tiles;
         for (int n = 0; n < N; ++n) {
+            const int item = first + n * G;
+            const int f = item / n_tiles, tile = (item - f * n_tiles) * tile_perm % n_tiles;
             const int slot = n % S;
             const int buf = n & 1;
             const unsigned xpar = unsigned(n >> 1) & 1u;
@@ -1105,7 +1164,17 @@ k_azimuth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant_
 #pragma unroll
             for (int h = 0; h < RT; ++h)
 #pragma unroll
-                for (int k = 0; k < L; ++k) v[h][k] = stg[tma_slot<L>(q, k, warp * RT + h)];
+                for (int k = 0; k < L; ++k) v[h][k] = stg[tma_slot(q, k, warp * RT + h)];
+            if (CORR && need[slot]) {               // x = x0 + a_l cin + q_l din (split long columns)
+                const cplx* cs = corr + slot * CORRE;
+                const cplx* aq = cs + 2 * NS;
+#pragma unroll
+                for (int h = 0; h < RT; ++h) {
+                    const cplx a = aq[2 * (warp * RT + h)], qr = aq[2 * (warp * RT + h) + 1];
+#pragma unroll
+                    for (int k = 0; k < L; ++k) v[h][k] = cfma(a, cs[k * 32 + q], cfma(qr, cs[NS + k * 32 + q], v[h][k]));
+                }
+            }
 
             cplx prev_edge[RT], next_edge[RT];     // cluster: x at mseg-1 and mseg+NS (cyclic)
             if (!diagonal) {
@@ -1265,19 +1334,17 @@ k_azimuth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant_
                         if (lane == 0) prev = wrap_prev;
                         if (lane == 31) next = wrap_next;
                     }
-                    const int r = (warp * RT + h) ^ swz;
 #pragma unroll
                     for (int k = 0; k < L; ++k) {
                         const cplx um = k ? v[h][k - 1] : prev;
                         const cplx up = (k + 1 < L) ? v[h][(k + 1) % L] : next;
-                        stg[((k * 32 + q) << 3) + r] = cfma(b1, v[h][k], cmul(b2, cadd(up, um)));   // own slots only
+                        stg[tma_slot(q, k, warp * RT + h)] = cfma(b1, v[h][k], cmul(b2, cadd(up, um)));   // own slots
                     }
                 }
             }
             fence_proxy_async_smem();               // the temp is read by the TMA store (async proxy)
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[slot]);
-            if (++tile == n_tiles) { tile = 0; ++f; }
         }
     }
     if (CLUSTER) cluster_barrier();                 // no CTA leaves while peers may still address it
@@ -1493,6 +1560,11 @@ static RingPlan ring_plan(int n_theta) {
 
 int ring_table_elems(int n_theta) { return ring_plan(n_theta).lay.E; }
 
+int ring_segment(int n_theta) {
+    const RingPlan p = ring_plan(n_theta);
+    return (p.kind == 0 || p.kind == 2) ? 32 * p.L : 0;
+}
+
 cudaError_t launch_ring_setup(const LaunchCtx& c, cplx* table, int n_steps, int first_index, double r_start,
                               double delta_r) {
     const RingLayout lay = ring_plan(c.n_theta).lay;
@@ -1511,12 +1583,12 @@ static cudaError_t set_smem(K kern, size_t bytes) {
 
 // TMA ring maps over the standard field layout: {16 doubles, q: 32, k: L,
 // segment: n_theta / (32L), item: F * n_tiles} (see k_azimuth_tma).
-static bool ring_tensor_map(CUtensorMap* tm, const void* base, int n_theta, int L, int64_t items) {
+static bool ring_tensor_map(CUtensorMap* tm, const void* base, int n_theta, int L, int64_t tiles) {
     const int NS = 32 * L;
-    const uint64_t dims[5] = {16, 32, uint64_t(L), uint64_t(n_theta / NS), uint64_t(items)};
+    const uint64_t dims[5] = {16, 32, uint64_t(L), uint64_t(n_theta / NS), uint64_t(tiles)};
     const uint64_t strides[4] = {uint64_t(L) * 128, 128, uint64_t(NS) * 128, uint64_t(n_theta) * 128};
     const uint32_t box[5] = {16, 32, uint32_t(L), 1, 1};
-    return encode_swizzled_map(tm, base, 5, dims, strides, box);
+    return encode_swizzled_map(tm, base, 5, dims, strides, box, 128);
 }
 
 // Occupancy of a kernel configuration, cached per (kernel, device, smem bytes)
@@ -1542,27 +1614,31 @@ static int cached_occupancy(const void* kern, size_t bytes, int cluster, int nth
     return v;
 }
 
-template <int L, int RT, int S, bool CLUSTER, int MINB = 1>
+template <int L, int RT, int S, bool CLUSTER, int MINB = 1, bool CORR = false>
 static cudaError_t launch_tma_ring(const LaunchCtx& c, const cplx* src, cplx* dst, const cplx* table_step, int E,
                                    const EpilogueArgs& ea) {
     constexpr int NS = 32 * L, NW = 8 / RT;
     const int CL = c.n_theta / NS;
     if (c.n_theta % NS != 0 || (CLUSTER ? (CL < 2 || CL > 16) : CL != 1)) return cudaErrorNotSupported;
-    const int64_t items = int64_t(c.n_freq) * c.n_tiles;
+    const int64_t tiles = int64_t(c.n_freq) * c.n_tiles;
+    const int64_t items = tiles;
     if (items > 0x7fffffff) return cudaErrorNotSupported;
     CUtensorMap tm_src, tm_dst;
-    if (!ring_tensor_map(&tm_src, src, c.n_theta, L, items) || !ring_tensor_map(&tm_dst, dst, c.n_theta, L, items))
+    if (!ring_tensor_map(&tm_src, src, c.n_theta, L, tiles) || !ring_tensor_map(&tm_dst, dst, c.n_theta, L, tiles))
         return cudaErrorNotSupported;
     const int tab_elems = RING_HDR + L + 1 + (CLUSTER ? std::max(32, 32 * (CL - 1) + 1) : 32);
     if (tab_elems > E) return cudaErrorNotSupported;
     const int tab_pad = (tab_elems + 7) & ~7;
-    const size_t bytes = 1024 + sizeof(cplx) * (size_t(S) * NS * 8 + size_t(S) * tab_pad + (CLUSTER ? 512 : 0)) +
-                         sizeof(uint64_t) * (2 * S + (CLUSTER ? 4 * NW : 0));
+    const size_t corre = CORR ? 2 * NS + 16 : 0;    // per slot: the carries and the rows' (a_l, q_l)
+    const size_t bytes = 1024 +
+                         sizeof(cplx) * (size_t(S) * NS * 8 + size_t(S) * tab_pad + S * corre + (CLUSTER ? 512 : 0)) +
+                         sizeof(uint64_t) * (2 * S + (CLUSTER ? 4 * NW : 0)) + sizeof(int) * S;
     if (bytes > 227 * 1024) return cudaErrorNotSupported;
-    auto kern = k_azimuth_tma<L, RT, S, CLUSTER, MINB>;
+    if (CORR && (c.split < 2 || c.n_tiles % c.split != 0 || !c.sp_cd || !c.sp_aq)) return cudaErrorNotSupported;
+    auto kern = k_azimuth_tma<L, RT, S, CLUSTER, MINB, CORR>;
     cudaError_t e = set_smem(kern, bytes);
     if (e != cudaSuccess) return e;
-    const int nthr = 32 * (NW + 1);
+    const int nthr = ring_tma_threads<RT>();
     if constexpr (!CLUSTER) {
         const int per_sm = cached_occupancy(reinterpret_cast<const void*>(kern), bytes, 1, nthr, nullptr);
         if (per_sm < 1) return cudaErrorInvalidConfiguration;
@@ -1571,7 +1647,8 @@ static cudaError_t launch_tma_ring(const LaunchCtx& c, const cplx* src, cplx* ds
         if (items <= 2 * ctas) per = 1;               // few items: let the block scheduler balance the tail
         const int grid = int((items + per - 1) / per);
         return launch_pdl(c.pdl != 0, kern, dim3(grid), dim3(nthr), bytes, c.stream, tm_src, tm_dst, table_step, E,
-                          tab_elems, c.n_theta, c.n_tiles, c.n_depth, items, per, ea);
+                          tab_elems, c.n_theta, c.n_tiles, c.n_depth, items, grid, ea, (const cplx*)c.sp_cd,
+                          (const cplx*)c.sp_aq, (const cplx*)c.sp_pa, c.split, 1);
     } else {
         if (CL > 8) {
             e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -1596,8 +1673,18 @@ static cudaError_t launch_tma_ring(const LaunchCtx& c, const cplx* src, cplx* ds
         const int per = int((items + resident - 1) / resident);
         const int clusters = int((items + per - 1) / per);
         cfg.gridDim = dim3(clusters * CL);
+        // split columns: the corrected tiles (near sub-column edges) are contiguous; a
+        // coprime stride P through each frequency's tiles spreads them over the clusters'
+        // contiguous item ranges (P ~ 0.618 n_tiles, gcd(P, n_tiles) = 1)
+        int perm = 1;
+        if (CORR) {
+            auto gcd = [](int a, int b) { while (b) { const int t = a % b; a = b; b = t; } return a; };
+            perm = int(0.618 * c.n_tiles) | 1;
+            while (gcd(perm, c.n_tiles) != 1) perm += 2;
+        }
         return cudaLaunchKernelEx(&cfg, kern, tm_src, tm_dst, table_step, E, tab_elems, c.n_theta, c.n_tiles,
-                                  c.n_depth, items, per, ea);
+                                  c.n_depth, items, per, ea, (const cplx*)c.sp_cd, (const cplx*)c.sp_aq,
+                                  (const cplx*)c.sp_pa, c.split, perm);
     }
 }
 
@@ -1682,6 +1769,18 @@ cudaError_t launch_azimuth_scan(const LaunchCtx& c, const cplx* src, cplx* dst, 
     const RingPlan plan = ring_plan(c.n_theta);
     const bool standard = ea.chunk_gap == 0 && (ea.chunk_cols == 0 || ea.chunk_cols == c.n_theta) && !ea.peer[0] &&
                           ea.row_offset == 0;
+    if (c.split >= 2) {
+        // split long columns: only the TMA kernels apply the sub-column carries
+        if (!standard || !ea.periodic) return cudaErrorNotSupported;
+        const int E = plan.lay.E;
+        if (plan.kind == 0 && plan.L == 8) return launch_tma_ring<8, 2, 2, false, 2, true>(c, src, dst, table_step, E, ea);
+        if (plan.kind == 0 && plan.L == 16) return launch_tma_ring<16, 1, 2, false, 1, true>(c, src, dst, table_step, E, ea);
+        if (plan.kind == 0 && plan.L == 4) return launch_tma_ring<4, 2, 3, false, 1, true>(c, src, dst, table_step, E, ea);
+        if (plan.kind == 0 && plan.L == 2) return launch_tma_ring<2, 2, 3, false, 1, true>(c, src, dst, table_step, E, ea);
+        if (plan.kind == 2 && plan.L == 16) return launch_tma_ring<16, 1, 2, true, 1, true>(c, src, dst, table_step, E, ea);
+        if (plan.kind == 2 && plan.L == 8) return launch_tma_ring<8, 2, 2, true, 1, true>(c, src, dst, table_step, E, ea);
+        return cudaErrorNotSupported;
+    }
     if (standard && ea.periodic && (plan.kind == 0 || plan.kind == 2) && !getenv("PE3D_RING_CPASYNC")) {
         // TMA + warp-specialised sweep; falls through to the cp.async kernels
         // only when the tensor map cannot describe the ring

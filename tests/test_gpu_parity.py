@@ -381,6 +381,8 @@ def test_depth_setup_table_bitwise_equal_to_in_kernel_setup(monkeypatch, shape):
     else:
         grid = make_grid(n_range=6, n_azimuth=512, n_depth=2048, delta_r=2.0, delta_z=0.5, r_start=2.0)
         cfg = Config(grid, make_env(grid), SourceSpec(freqs, 0.3 * grid.depth_extent), RunOptions(output_stride=3))
+    if shape == "long":
+        monkeypatch.setenv("PE3D_DEPTH_NO_SPLIT", "1")     # the cluster sweep (the split sweep needs the table)
     monkeypatch.setenv("PE3D_NO_K1_TABLE", "1")
     ref = march_frequencies(cfg, list(freqs))
     monkeypatch.delenv("PE3D_NO_K1_TABLE")
@@ -389,6 +391,28 @@ def test_depth_setup_table_bitwise_equal_to_in_kernel_setup(monkeypatch, shape):
         assert x.tl_field.tobytes() == y.tl_field.tobytes()
         assert x.final_slab.values.tobytes() == y.final_slab.values.tobytes()
         assert x.clamped_samples == y.clamped_samples
+
+
+@pytest.mark.parametrize("n_depth,n_azimuth", [(2048, 256), (4096, 512), (3072, 1024)])
+def test_split_columns_match_cluster_sweep_and_oracle(monkeypatch, n_depth, n_azimuth):
+    """Long columns solved as independent 1024-row sub-columns with exact
+    carries applied by the azimuth sweep (LaunchCtx::split, the default for
+    cfg2/cfg5 shapes) against the lock-step cluster sweep
+    (PE3D_DEPTH_NO_SPLIT) and the CPU oracle: several frequencies (chains and
+    frequency switches), TL at every output range."""
+    freqs = (40.0, 75.0)
+    grid = make_grid(n_range=8, n_azimuth=n_azimuth, n_depth=n_depth, delta_r=2.0, delta_z=0.5, r_start=2.0)
+    cfg = Config(grid, make_env(grid), SourceSpec(freqs, 0.3 * grid.depth_extent), RunOptions(output_stride=2))
+    got = march_frequencies(cfg, list(freqs), keep_snapshots=True)
+    monkeypatch.setenv("PE3D_DEPTH_NO_SPLIT", "1")
+    ref = march_frequencies(cfg, list(freqs), keep_snapshots=True)
+    for x, y in zip(got, ref):
+        assert rel_l2(x.final_slab.values, y.final_slab.values) <= 1e-12
+        assert tl_err(x.tl_field, y.tl_field) <= 1e-9
+        assert x.clamped_samples == y.clamped_samples
+    o = O.run_frequency(cfg, freqs[1], keep_snapshots=True)
+    assert rel_l2(got[1].final_slab.values, o.final) <= FIELD_TOL
+    assert tl_err(got[1].tl_field, o.tl_field) <= TL_TOL
 
 
 @pytest.mark.parametrize("shape", ["cfg4", "cfg2"])
@@ -655,7 +679,9 @@ def test_slab_march_peer_vs_copy_transport(monkeypatch, nranks):
     grid = cfg.grid
     small = Config(Grid3D(5, 512, 2048, grid.delta_r, 2 * math.pi / 512, grid.delta_z, grid.r_start),
                    cfg.environment, SourceSpec((500.0,), 300.0), RunOptions(output_stride=2))
+    monkeypatch.setenv("PE3D_DEPTH_NO_SPLIT", "1")      # the slab march runs the lock-step cluster depth sweep
     ref = march_frequencies(small, [500.0])[0]
+    monkeypatch.delenv("PE3D_DEPTH_NO_SPLIT")
     monkeypatch.delenv("PE3D_SLAB_COPY", raising=False)
     peer = slab_march(small, 500.0, nranks)
     monkeypatch.setenv("PE3D_SLAB_COPY", "1")
@@ -665,10 +691,10 @@ def test_slab_march_peer_vs_copy_transport(monkeypatch, nranks):
         assert got.tl_field.tobytes() == ref.tl_field.tobytes()
 
 
-def test_slab_march_ipc_peer_one_rank():
+def test_slab_march_ipc_peer_one_rank(monkeypatch):
     """The IPC entry points of the peer transport (export, all-gather of the
     handles, barrier, pe3d_march_slab_p2p) with one rank: bitwise the plain
-    march."""
+    march (with the cluster depth sweep the slab march also runs)."""
     import socket
     import torch.distributed as dist
     from paper_1711_00005_b200 import slab
@@ -676,7 +702,9 @@ def test_slab_march_ipc_peer_one_rank():
     grid = cfg.grid
     small = Config(Grid3D(4, 256, 2048, grid.delta_r, 2 * math.pi / 256, grid.delta_z, grid.r_start),
                    cfg.environment, SourceSpec((500.0,), 300.0), RunOptions(output_stride=2))
+    monkeypatch.setenv("PE3D_DEPTH_NO_SPLIT", "1")
     ref = march_frequencies(small, [500.0])[0]
+    monkeypatch.delenv("PE3D_DEPTH_NO_SPLIT")
     with socket.socket() as sk:
         sk.bind(("127.0.0.1", 0))
         port = sk.getsockname()[1]
