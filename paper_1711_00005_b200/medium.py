@@ -107,7 +107,7 @@ class RandomPerturbation:
         # Gaussian correlation exp(-d^2/L^2) <-> spectral filter exp(-(pi k L)^2 / 2)
         filt = np.exp(-0.5 * (math.pi ** 2) * ((kx * self.corr_h) ** 2 + (ky * self.corr_h) ** 2
                                                 + (kz * self.corr_v) ** 2))
-        field_ = np.fft.irfftn(spectrum * filt, s=noise.shape)
+        field_ = np.fft.irfftn(spectrum * filt, s=noise.shape, axes=(0, 1, 2))
         field_ *= self.sigma / field_.std()
         object.__setattr__(self, "lattice", np.ascontiguousarray(field_))
         object.__setattr__(self, "spacing_h", dh)
