@@ -82,6 +82,8 @@ typedef struct {
 #define PE3D_FLAG_NO_GRAPH   1   /* launch the step loop directly instead of a CUDA graph */
 #define PE3D_FLAG_SERIAL     2   /* use the thread-per-system kernels (reference op order) */
 #define PE3D_FLAG_PROFILE    4   /* no graph; CUDA events around every launch (see pe3d_profile_last) */
+#define PE3D_FLAG_STARTER_COLUMN 8  /* pe3d_march_*: u0 is [F][n_depth], the same column at every azimuth
+                                       (the reference's Gaussian starter, ref environment.py:270-284) */
 
 /* Per-frequency step coefficients (ref operators.py:31-62, StepCoefficients). */
 typedef struct {
@@ -262,6 +264,24 @@ PE3D_API int pe3d_profile_last(void* handle, double* ms, int32_t* launches);
  * (measurement only).
  */
 PE3D_API int pe3d_last_launches(void* handle, int64_t* launches);
+
+/*
+ * pe3d_profile_launches -- the individual CUDA-event times (ms, launch order)
+ * of kernel class `cls` in the last PE3D_FLAG_PROFILE march on this handle;
+ * writes min(count, capacity) entries and the full count to *count
+ * (measurement only: steady-state launches for the bench's roofline).
+ */
+PE3D_API int pe3d_profile_launches(void* handle, int32_t cls, double* ms, int32_t capacity, int32_t* count);
+
+/*
+ * pe3d_host_alloc / pe3d_host_free -- page-locked host memory for the
+ * caller's TL and slab stacks (cudaHostAlloc).  A page-locked TL stack lets
+ * pe3d_march_host stream the samples to the host while the march runs; the
+ * Python drop-in (run_frequency / frequency_farm, ref marching.py:144-193,
+ * parallel.py:143-185) returns its results in such memory.
+ */
+PE3D_API int pe3d_host_alloc(uint64_t bytes, void** ptr);
+PE3D_API int pe3d_host_free(void* ptr);
 
 #ifdef __cplusplus
 }

@@ -22,7 +22,7 @@ LIB_PATH = Path(__file__).resolve().parent / LIB_NAME
 ABI_VERSION = 1
 
 PERIODIC, SECTOR = 0, 1
-FLAG_NO_GRAPH, FLAG_SERIAL, FLAG_PROFILE = 1, 2, 4
+FLAG_NO_GRAPH, FLAG_SERIAL, FLAG_PROFILE, FLAG_STARTER_COLUMN = 1, 2, 4, 8
 
 # Every symbol include/pe3d_b200.h declares (checked by tests/test_abi.py).
 EXPORTED_SYMBOLS = (
@@ -30,6 +30,7 @@ EXPORTED_SYMBOLS = (
     "pe3d_sample_count", "pe3d_march_host", "pe3d_march_device", "pe3d_step_general_host",
     "pe3d_solve_batch_host", "pe3d_profile_last", "pe3d_march_medium_host", "pe3d_slab_unique_id",
     "pe3d_march_slab", "pe3d_slab_p2p_export", "pe3d_march_slab_p2p", "pe3d_last_launches",
+    "pe3d_profile_launches", "pe3d_host_alloc", "pe3d_host_free",
 )
 SLAB_IPC_BYTES = 192
 
@@ -89,6 +90,9 @@ _SIGNATURES = {
                                         Strided, _P, C.POINTER(ErrorRecord)]),
     "pe3d_profile_last": (C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_int32)]),
     "pe3d_last_launches": (C.c_int, [_P, C.POINTER(C.c_int64)]),
+    "pe3d_profile_launches": (C.c_int, [_P, C.c_int32, C.POINTER(C.c_double), C.c_int32, C.POINTER(C.c_int32)]),
+    "pe3d_host_alloc": (C.c_int, [C.c_uint64, C.POINTER(C.c_void_p)]),
+    "pe3d_host_free": (C.c_int, [_P]),
     "pe3d_march_medium_host": (C.c_int, [_P, C.POINTER(GridParams), C.POINTER(Coeffs), C.POINTER(Medium),
                                          _P, _P, _P, _P, _P, C.POINTER(ErrorRecord)]),
     "pe3d_slab_unique_id": (C.c_int, [_P, C.c_int32]),
@@ -202,3 +206,62 @@ def make_medium(medium, keep_alive: list) -> Medium:
         m.lat_nx, m.lat_ny, m.lat_nz = lat.shape
         m.lat_extent_h, m.lat_spacing_h, m.lat_spacing_v = p.extent_h, p.spacing_h, p.spacing_v
     return m
+
+
+# ---------------------------------------------------------------- page-locked host arrays
+# The drop-in returns TL stacks and final slabs in page-locked memory, so that
+# pe3d_march_host streams the TL samples to the host while the march runs
+# (a pageable stack is copied after the march).  Blocks come from
+# pe3d_host_alloc; when the last array viewing a block is garbage-collected
+# the block returns to a small free list and is reused by the next march
+# (page-locking gigabytes costs ~0.1 s/GB, a reused block nothing).
+
+_PINNED_FREE: list = []                # (bytes, ptr) of idle blocks
+_pin_lock = threading.RLock()          # a block may be released by the GC inside the pool's own lock
+_PINNED_KEEP_BYTES = 24 << 30          # idle blocks kept for reuse (larger ones are released)
+
+
+class _PinnedBlock:
+    """Owner of one page-locked block; numpy arrays over it keep it alive."""
+
+    def __init__(self, ptr: int, nbytes: int, shape, dtype):
+        self.ptr, self.nbytes = ptr, nbytes
+        self.__array_interface__ = {"shape": tuple(shape), "typestr": np.dtype(dtype).str,
+                                    "data": (ptr, False), "version": 3}
+
+    def __del__(self):
+        try:
+            _pinned_release(self.ptr, self.nbytes)
+        except Exception:                  # interpreter shutdown
+            pass
+
+
+def _pinned_release(ptr: int, nbytes: int) -> None:
+    with _pin_lock:
+        _PINNED_FREE.append((nbytes, ptr))
+        _PINNED_FREE.sort()
+        while sum(b for b, _ in _PINNED_FREE) > _PINNED_KEEP_BYTES:
+            b, p = _PINNED_FREE.pop()
+            if _lib is not None:
+                _lib.pe3d_host_free(C.c_void_p(p))
+
+
+def pinned_empty(shape, dtype=np.float64) -> np.ndarray:
+    """An uninitialised C-contiguous array in page-locked host memory."""
+    nbytes = int(np.prod(shape, dtype=np.int64)) * np.dtype(dtype).itemsize
+    if nbytes == 0:
+        return np.empty(shape, dtype=dtype)
+    lib = load_library()
+    ptr = None
+    with _pin_lock:
+        for i, (b, p) in enumerate(_PINNED_FREE):
+            if nbytes <= b <= 2 * nbytes:            # best fit, at most half wasted
+                ptr, nbytes_block = p, b
+                del _PINNED_FREE[i]
+                break
+    if ptr is None:
+        out = C.c_void_p()
+        if lib.pe3d_host_alloc(C.c_uint64(nbytes), C.byref(out)) != 0 or not out.value:
+            raise NativeError(f"cannot page-lock {nbytes} bytes of host memory")
+        ptr, nbytes_block = out.value, nbytes
+    return np.asarray(_PinnedBlock(ptr, nbytes_block, shape, dtype))

@@ -115,6 +115,10 @@ static cudaError_t tl_join(Handle* h, const TlSink& sk, int n_copy_streams, cuda
     cudaError_t first = cudaSuccess;
     for (int c = 0; c <= Handle::MAX_CHAINS; ++c) {
         if (c >= n_copy_streams && c != Handle::MAX_CHAINS) continue;
+        // a chain's copy stream joined the step loop (and a graph capture) only if
+        // the loop records a sample (k >= 1); joining an idle one would wait on
+        // work outside the capture
+        if (c != Handle::MAX_CHAINS && sk.S <= 1) continue;
         cudaError_t e = cudaEventRecord(tl_event(h, c, sk.R, sk), h->tl_side[c]);
         if (e == cudaSuccess) e = cudaStreamWaitEvent(st, tl_event(h, c, sk.R, sk), 0);
         if (e != cudaSuccess && first == cudaSuccess) first = e;
@@ -483,6 +487,7 @@ static int march_device_impl(void* handle, const pe3d_grid* g, const pe3d_coeffs
     ea0.sample = 0;
     ea0.periodic = g->topology == PE3D_PERIODIC;
     ea0.write_temp = g->n_steps > 0;
+    ea0.src_column = (g->flags & PE3D_FLAG_STARTER_COLUMN) != 0;
     if (sink) CK(tl_prepare(h, *sink), "tl streams");
     CK(prof.run(2, [&] { return pe3d::launch_finish(c, reinterpret_cast<const cplx*>(d_u0), 0, h->field_a.as<cplx>(),
                                                      g->r_input, ea0); }),
@@ -566,9 +571,10 @@ int pe3d_march_host(void* handle, const pe3d_grid* g, const pe3d_coeffs* coeffs,
     CK(cudaSetDevice(h->device), "cudaSetDevice");
     const int64_t F = g->n_freq, slab = int64_t(g->n_theta) * g->n_depth;
     const int64_t S = pe3d_sample_count(g->n_steps, g->output_stride);
+    const int64_t u0_elems = F * ((g->flags & PE3D_FLAG_STARTER_COLUMN) ? g->n_depth : slab);
     cudaStream_t s = h->stream;
     CK(h->h_local.ensure(F * g->n_depth * sizeof(cplx)), "alloc");
-    CK(h->h_u0.ensure(F * slab * sizeof(cplx)), "alloc");
+    CK(h->h_u0.ensure(u0_elems * sizeof(cplx)), "alloc");
     CK(h->h_clamped.ensure(F * sizeof(int64_t)), "alloc");
     if (u_final) CK(h->h_final.ensure(F * slab * sizeof(cplx)), "alloc");
     // A page-locked TL stack (and no snapshots): stream the samples out while
@@ -583,7 +589,7 @@ int pe3d_march_host(void* handle, const pe3d_grid* g, const pe3d_coeffs* coeffs,
     if (tl) CK(h->h_tl.ensure(F * (sink.host ? sink.R : S) * slab * sizeof(double)), "alloc");
     if (snapshots) CK(h->h_snap.ensure(F * S * slab * sizeof(cplx)), "alloc");
     CK(cudaMemcpyAsync(h->h_local.ptr, local, F * g->n_depth * sizeof(cplx), cudaMemcpyHostToDevice, s), "H2D");
-    CK(cudaMemcpyAsync(h->h_u0.ptr, u0, F * slab * sizeof(cplx), cudaMemcpyHostToDevice, s), "H2D");
+    CK(cudaMemcpyAsync(h->h_u0.ptr, u0, u0_elems * sizeof(cplx), cudaMemcpyHostToDevice, s), "H2D");
     st = march_device_impl(handle, g, coeffs, h->h_local.as<pe3d_c128>(), h->h_u0.as<pe3d_c128>(),
                            u_final ? h->h_final.as<pe3d_c128>() : nullptr, tl ? h->h_tl.as<double>() : nullptr,
                            snapshots ? h->h_snap.as<pe3d_c128>() : nullptr, h->h_clamped.as<int64_t>(), s, err,
@@ -775,7 +781,8 @@ int pe3d_march_medium_host(void* handle, const pe3d_grid* g, const pe3d_coeffs* 
     CK(h->med_prof.ensure(2 * md->n_profile * sizeof(double)), "alloc");
     const int64_t n_lat = md->lattice ? int64_t(md->lat_nx) * md->lat_ny * md->lat_nz : 0;
     if (n_lat) CK(h->med_lat.ensure(n_lat * sizeof(double)), "alloc");
-    CK(h->h_u0.ensure(F * slab * sizeof(cplx)), "alloc");
+    const int64_t u0_elems = F * ((g->flags & PE3D_FLAG_STARTER_COLUMN) ? NZ : slab);
+    CK(h->h_u0.ensure(u0_elems * sizeof(cplx)), "alloc");
     CK(h->h_clamped.ensure(F * sizeof(int64_t)), "alloc");
     if (u_final) CK(h->h_final.ensure(F * slab * sizeof(cplx)), "alloc");
     if (tl) CK(h->h_tl.ensure(int64_t(F) * S * slab * sizeof(double)), "alloc");
@@ -794,7 +801,7 @@ int pe3d_march_medium_host(void* handle, const pe3d_grid* g, const pe3d_coeffs* 
     CK(cudaMemcpyAsync(h->med_prof.as<double>() + md->n_profile, md->profile_c, md->n_profile * sizeof(double),
                        cudaMemcpyHostToDevice, s), "H2D");
     if (n_lat) CK(cudaMemcpyAsync(h->med_lat.ptr, md->lattice, n_lat * sizeof(double), cudaMemcpyHostToDevice, s), "H2D");
-    CK(cudaMemcpyAsync(h->h_u0.ptr, u0, F * slab * sizeof(cplx), cudaMemcpyHostToDevice, s), "H2D");
+    CK(cudaMemcpyAsync(h->h_u0.ptr, u0, u0_elems * sizeof(cplx), cudaMemcpyHostToDevice, s), "H2D");
     CK(cudaMemsetAsync(h->h_clamped.ptr, 0, F * sizeof(int64_t), s), "memset");
     cudaStreamSynchronize(s);   // host staging (vectors) must outlive the copies
 
@@ -856,6 +863,7 @@ int pe3d_march_medium_host(void* handle, const pe3d_grid* g, const pe3d_coeffs* 
     ea0.sample = 0;
     ea0.periodic = periodic;
     ea0.write_temp = g->n_steps > 0;
+    ea0.src_column = (g->flags & PE3D_FLAG_STARTER_COLUMN) != 0;
     CK(pe3d::launch_finish(c, h->h_u0.as<cplx>(), 0, A, g->r_input, ea0), "prepare");
     const int64_t E = periodic ? pe3d::ring_table_elems(NT) : 0;
     // The step loop.  Scan path: the medium at r_(j+1) is evaluated on the
@@ -998,6 +1006,27 @@ int pe3d_last_launches(void* handle, int64_t* launches) {
     if (!h || !launches) return PE3D_BAD_ARGUMENT;
     *launches = h->last_launches;
     return PE3D_OK;
+}
+
+int pe3d_profile_launches(void* handle, int32_t cls, double* ms, int32_t capacity, int32_t* count) {
+    Handle* h = static_cast<Handle*>(handle);
+    if (!h || cls < 0 || cls > 2 || capacity < 0) return PE3D_BAD_ARGUMENT;
+    const std::vector<double>& v = h->prof_list[cls];
+    if (count) *count = int32_t(v.size());
+    for (int32_t i = 0; ms && i < capacity && i < int32_t(v.size()); ++i) ms[i] = v[i];
+    return PE3D_OK;
+}
+
+int pe3d_host_alloc(uint64_t bytes, void** ptr) {
+    if (!ptr) return PE3D_BAD_ARGUMENT;
+    *ptr = nullptr;
+    if (bytes == 0) return PE3D_OK;
+    return cudaHostAlloc(ptr, size_t(bytes), cudaHostAllocDefault) == cudaSuccess ? PE3D_OK : PE3D_CUDA_ERROR;
+}
+
+int pe3d_host_free(void* ptr) {
+    if (!ptr) return PE3D_OK;
+    return cudaFreeHost(ptr) == cudaSuccess ? PE3D_OK : PE3D_CUDA_ERROR;
 }
 
 int pe3d_profile_last(void* handle, double* ms, int32_t* launches) {

@@ -78,6 +78,7 @@ struct Handle {
     // PE3D_FLAG_PROFILE accounting
     double prof_ms[3] = {0, 0, 0};
     int32_t prof_n[3] = {0, 0, 0};
+    std::vector<double> prof_list[3];     // per launch, in launch order
     // kernels launched by the last march (graph replays included)
     int64_t graph_launches = 0, last_launches = 0;
     // concurrent step-loop chains over disjoint frequency groups
@@ -111,13 +112,14 @@ struct Prof {
     }
     void collect() {
         if (!on) return;
-        for (int k = 0; k < 3; ++k) { h->prof_ms[k] = 0; h->prof_n[k] = 0; }
+        for (int k = 0; k < 3; ++k) { h->prof_ms[k] = 0; h->prof_n[k] = 0; h->prof_list[k].clear(); }
         for (auto& p : ev) {
             float ms = 0;
             cudaEventSynchronize(p.second.second);
             cudaEventElapsedTime(&ms, p.second.first, p.second.second);
             h->prof_ms[p.first] += ms;
             h->prof_n[p.first] += 1;
+            h->prof_list[p.first].push_back(ms);
             cudaEventDestroy(p.second.first);
             cudaEventDestroy(p.second.second);
         }

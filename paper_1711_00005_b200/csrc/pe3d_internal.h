@@ -47,6 +47,9 @@ struct EpilogueArgs {
     // straight into the depth-sweep input of the rank owning azimuth chunk
     // m / chunk_cols (this rank's chunk of it).
     cplx* peer[MAX_PEERS];
+    // march prologue only: the starter u0 is one column per frequency ([F][n_depth],
+    // PE3D_FLAG_STARTER_COLUMN) instead of a [F][n_theta][n_depth] slab
+    int src_column;
 };
 
 // Destination of the next temp of ring element (m, row r) of local tile t.

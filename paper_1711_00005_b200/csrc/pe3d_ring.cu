@@ -1422,7 +1422,7 @@ k_finish(const cplx* __restrict__ src, int src_tiled, cplx* __restrict__ dst, co
         const int m = m0 + k;
         if (k < nvalid && l < n_depth) {
             v = src_tiled ? ldc(src + tile_off + ring_off(m, ea.chunk_cols, ea.chunk_gap) + row0 + i)
-                          : ldc(src + (int64_t(f) * n_theta + m) * n_depth + l);
+                          : ldc(src + (int64_t(f) * (ea.src_column ? 1 : n_theta) + (ea.src_column ? 0 : m)) * n_depth + l);
             if (l + ea.row_offset == 0 || (!ea.periodic && (m == 0 || m == n_theta - 1))) v = czero();
         }
         u[0][k] = v;
@@ -1459,7 +1459,8 @@ k_prepare(const cplx* __restrict__ u0, cplx* __restrict__ dst, const FreqDev* __
             else ok = false;
         }
         if (!periodic && (m == 0 || m == n_theta - 1)) ok = false;    // sector edges (marching.py:87-89)
-        sx[a][dl] = ok ? ldc(u0 + (int64_t(f) * n_theta + m) * n_depth + l) : czero();
+        sx[a][dl] = ok ? ldc(u0 + (ea.src_column ? int64_t(f) * n_depth + l : (int64_t(f) * n_theta + m) * n_depth + l))
+                       : czero();
     }
     __syncthreads();
     const FreqDev fd = fdev[f];

@@ -28,8 +28,8 @@ import numpy as np
 
 from . import _native
 from .environment import (
-    PERIODIC, SECTOR, Environment, FieldSlab, Grid3D, gaussian_starter, is_range_independent,
-    local_term_grid, wavenumber,
+    PERIODIC, SECTOR, Environment, FieldSlab, Grid3D, gaussian_starter, gaussian_starter_column,
+    is_range_independent, local_term_grid, refraction_index_grid, wavenumber,
 )
 from .errors import DomainError
 from .operators import StepCoefficients
@@ -112,8 +112,21 @@ def _device_medium(env) -> bool:
 
 
 def _local_column(env, grid: Grid3D, r: float, k0: float) -> np.ndarray:
-    """n^2 - 1 over depth for a range-independent medium."""
-    return np.ascontiguousarray(local_term_grid(env, grid, r, k0)[0])
+    """n^2 - 1 over depth for a range-independent medium (the same
+    elementwise arithmetic as local_term_grid, ref operators.py:93, on one
+    column of the azimuth-independent index grid)."""
+    n = np.asarray(refraction_index_grid(env, grid, r, k0)[0], dtype=np.complex128)
+    return np.ascontiguousarray(n ** 2 - 1.0)
+
+
+def _starter_columns(grid: Grid3D, source, k0s) -> np.ndarray:
+    """The Gaussian starter of every frequency as one depth column each
+    (azimuth independent, surface zero; ref environment.py:270-284) -- the
+    march reads them with PE3D_FLAG_STARTER_COLUMN."""
+    cols = np.empty((len(k0s), grid.n_depth), dtype=np.complex128)
+    for i, k0 in enumerate(k0s):
+        cols[i] = gaussian_starter_column(grid, source, k0)
+    return cols
 
 
 def range_step(state: MarchState, device: int = 0) -> MarchState:
@@ -184,36 +197,40 @@ def march_frequencies(config, frequencies: Sequence[float], n_steps: Optional[in
     F, NT, NZ = len(frequencies), grid.n_azimuth, grid.n_depth
     slab_elems = NT * NZ
 
-    u0 = np.empty((F, NT, NZ), dtype=np.complex128)
-    for i, k0 in enumerate(k0s):
-        u0[i] = gaussian_starter(grid, source, k0).values
-    tl = np.empty((F, S, NT, NZ), dtype=np.float64)
+    # TL stack and final slabs in page-locked memory: the TL samples stream to
+    # the host while the march runs (pe3d_march_host)
+    tl = _native.pinned_empty((F, S, NT, NZ), np.float64)
     snaps = np.empty((F, S, NT, NZ), dtype=np.complex128) if keep_snapshots else None
-    final = np.empty((F, NT, NZ), dtype=np.complex128)
+    final = _native.pinned_empty((F, NT, NZ), np.complex128)
     clamped = np.zeros(F, dtype=np.int64)
     h = _native.handle(device)
 
     if is_range_independent(env):
+        cols = _starter_columns(grid, source, k0s)
         per_freq = slab_elems * (S * (8 + (16 if keep_snapshots else 0)) + 16 * 6)
         chunk = max(1, min(F, BATCH_BYTES // max(per_freq, 1)))
         for lo in range(0, F, chunk):
             hi = min(F, lo + chunk)
             local = np.ascontiguousarray(np.stack([_local_column(env, grid, grid.r_start, k0)
                                                    for k0 in k0s[lo:hi]]))
-            g = _grid_params(grid, hi - lo, steps, stride, 0, grid.r_start, flags)
+            g = _grid_params(grid, hi - lo, steps, stride, 0, grid.r_start, flags | _native.FLAG_STARTER_COLUMN)
             cf = _native.make_coeffs(k0s[lo:hi], coeffs[lo:hi])
-            _native.call("pe3d_march_host", h, g, cf, _native.ptr(local), _native.ptr(u0[lo:hi]),
+            _native.call("pe3d_march_host", h, g, cf, _native.ptr(local), _native.ptr(cols[lo:hi]),
                          _native.ptr(final[lo:hi]), _native.ptr(tl[lo:hi]),
                          _native.ptr(snaps[lo:hi]) if keep_snapshots else None,
                          _native.ptr(clamped[lo:hi]))
     elif _device_medium(env):
         keep: list = []
         med = _native.make_medium(env.medium, keep)
-        g = _grid_params(grid, F, steps, stride, 0, grid.r_start, flags)
+        g = _grid_params(grid, F, steps, stride, 0, grid.r_start, flags | _native.FLAG_STARTER_COLUMN)
         cf = _native.make_coeffs(k0s, coeffs)
-        _native.call("pe3d_march_medium_host", h, g, cf, med, _native.ptr(u0), _native.ptr(final),
+        _native.call("pe3d_march_medium_host", h, g, cf, med, _native.ptr(_starter_columns(grid, source, k0s)),
+                     _native.ptr(final),
                      _native.ptr(tl), _native.ptr(snaps) if keep_snapshots else None, _native.ptr(clamped))
     else:
+        u0 = np.empty((F, NT, NZ), dtype=np.complex128)
+        for i, k0 in enumerate(k0s):
+            u0[i] = gaussian_starter(grid, source, k0).values
         _march_general(config, k0s, coeffs, u0, steps, stride, tl, snaps, final, clamped, h)
 
     wall = time.perf_counter() - t0

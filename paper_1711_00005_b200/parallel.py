@@ -17,7 +17,7 @@ from __future__ import annotations
 from dataclasses import dataclass
 from typing import List, Optional
 
-from .errors import InvariantError, Pe3dError
+from .errors import InvariantError
 from .marching import march_frequencies
 
 
@@ -74,9 +74,9 @@ def _march_isolating(config, jobs, device, n_steps=None):
     try:
         res = march_frequencies(config, freqs, device=device, n_steps=n_steps)
         return [(i, "ok", r) for (i, _), r in zip(jobs, res)]
-    except Pe3dError:
+    except Exception as exc:            # any failure of the batch (StepError, host memory, ...)
         if len(jobs) == 1:
-            raise
+            return [(jobs[0][0], "error", f"{type(exc).__name__}: {exc}")]
     outcomes = []
     for i, f in jobs:
         try:
@@ -106,10 +106,7 @@ def frequency_farm(config, frequencies, workers: int = 1, schedule: str = "stati
     jobs = list(enumerate(frequencies))
     results: list = [None] * len(frequencies)
     failures = []
-    try:
-        outcomes = _march_isolating(config, jobs, device)
-    except Exception as exc:
-        outcomes = [(jobs[0][0], "error", f"{type(exc).__name__}: {exc}")]
+    outcomes = _march_isolating(config, jobs, device)    # one outcome per job, failures included
     for index, status, payload in outcomes:
         if status == "ok":
             results[index] = payload

@@ -470,12 +470,14 @@ def test_parallel_factorization_matches_reference_recurrence(monkeypatch):
 
 
 @pytest.mark.parametrize("n_steps,stride,chains,topology", [
-    (0, 1, "2", PERIODIC), (6, 6, "2", PERIODIC), (6, 2, "1", PERIODIC), (21, 3, "2", PERIODIC),
+    (0, 1, "2", PERIODIC), (5, 10, "2", PERIODIC), (5, 10, "1", PERIODIC), (6, 6, "2", PERIODIC),
+    (6, 2, "1", PERIODIC), (21, 3, "2", PERIODIC),
     (21, 3, "3", PERIODIC), (21, 3, "8", PERIODIC), (13, 2, "1", SECTOR)])
 def test_tl_streaming_to_pinned_host(monkeypatch, n_steps, stride, chains, topology):
     """pe3d_march_host with a page-locked TL stack streams the samples through
     a device ring (R = min(S, 4) slots, copies overlapping the march, ring
-    wrap-around when S > 4): bitwise the stack copied after the march."""
+    wrap-around when S > 4; a graphed loop that records no sample, S = 1):
+    bitwise the stack copied after the march."""
     import ctypes as C
     import torch
     from paper_1711_00005_b200.marching import _grid_params, _local_column
@@ -726,3 +728,40 @@ def test_slab_march_cfg5_full_size_vs_reference(golden):
     got = u[fx["mi"], fx["li"]]
     assert np.linalg.norm(got - fx["samples"][2]) <= FIELD_TOL * np.linalg.norm(fx["samples"][2])
     assert abs(np.linalg.norm(u) - fx["norms"][2]) <= FIELD_TOL * fx["norms"][2]
+
+
+@pytest.mark.parametrize("name", ["cfg4", "cfg3"])
+def test_starter_column_flag_bitwise_equal_to_slab(name):
+    """PE3D_FLAG_STARTER_COLUMN (u0 as one depth column per frequency, what the
+    drop-in passes for the reference's azimuth-independent Gaussian starter,
+    ref environment.py:270-284) against the full [F][n_theta][n_depth] slab:
+    bitwise equal TL, final slabs and clamped counts -- the range-independent
+    march and the device-medium march."""
+    from paper_1711_00005_b200.environment import gaussian_starter, gaussian_starter_column
+    from paper_1711_00005_b200.marching import _grid_params, _local_column
+    freqs = (50.0, 130.0) if name == "cfg4" else (25.0,)
+    cfg = configs.build(name, n_range=7, frequencies=freqs, output_stride=3)
+    grid, env, source, _ = cfg
+    k0s = [wavenumber(f, env.c0) for f in freqs]
+    coeffs = _native.make_coeffs(k0s, [StepCoefficients.for_step(k0, grid.delta_r) for k0 in k0s])
+    F, NT, NZ, S = len(freqs), grid.n_azimuth, grid.n_depth, 1 + 7 // 3
+    slab = np.ascontiguousarray(np.stack([gaussian_starter(grid, source, k0).values for k0 in k0s]))
+    cols = np.ascontiguousarray(np.stack([gaussian_starter_column(grid, source, k0) for k0 in k0s]))
+    out = []
+    for u0, flags in ((slab, 0), (cols, _native.FLAG_STARTER_COLUMN)):
+        tl = np.empty((F, S, NT, NZ))
+        fin = np.empty((F, NT, NZ), dtype=np.complex128)
+        cl = np.zeros(F, dtype=np.int64)
+        g = _grid_params(grid, F, 7, 3, 0, grid.r_start, flags)
+        if name == "cfg4":
+            local = np.ascontiguousarray(np.stack([_local_column(env, grid, grid.r_start, k0) for k0 in k0s]))
+            _native.call("pe3d_march_host", _native.handle(), g, coeffs, _native.ptr(local), _native.ptr(u0),
+                         _native.ptr(fin), _native.ptr(tl), None, _native.ptr(cl))
+        else:
+            keep = []
+            med = _native.make_medium(env.medium, keep)
+            _native.call("pe3d_march_medium_host", _native.handle(), g, coeffs, med, _native.ptr(u0),
+                         _native.ptr(fin), _native.ptr(tl), None, _native.ptr(cl))
+        out.append((tl, fin, cl))
+    for x, y in zip(*out):
+        assert x.tobytes() == y.tobytes()
