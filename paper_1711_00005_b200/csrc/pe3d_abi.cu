@@ -557,7 +557,9 @@ static int march_device_impl(void* handle, const pe3d_grid* g, const pe3d_coeffs
     CK(cudaGetLastError(), "launch");
     prof.collect();
     h->last_launches = prof.launches;
-    return decode_error(h, stream, err);
+    HostFail hf;
+    if (!p.serial && g->topology == PE3D_PERIODIC) hf = azimuth_failures(g, coeffs);   // the ring sweep has no pivots
+    return decode_error(h, stream, err, &hf);
 }
 
 int pe3d_march_host(void* handle, const pe3d_grid* g, const pe3d_coeffs* coeffs, const pe3d_c128* local,
@@ -987,7 +989,9 @@ int pe3d_march_medium_host(void* handle, const pe3d_grid* g, const pe3d_coeffs* 
     } else {
         CK(step_loop(), "enqueue");
     }
-    st = decode_error(h, s, err);
+    HostFail hf;
+    if (periodic) hf = azimuth_failures(g, coeffs);          // the ring sweep has no pivots
+    st = decode_error(h, s, err, &hf);
     if (st != PE3D_OK) return st;
     if (u_final) CK(cudaMemcpyAsync(u_final, h->h_final.ptr, F * slab * sizeof(cplx), cudaMemcpyDeviceToHost, s), "D2H");
     if (tl) CK(cudaMemcpyAsync(tl, h->h_tl.ptr, int64_t(F) * S * slab * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");

@@ -112,19 +112,42 @@ __host__ __device__ __forceinline__ int64_t tidx(int f, int m, int l, int n_tile
 
 // Error flag shared by all kernels of a march: the first failure (lowest
 // packed key) wins.  key = (step << 40) | (sweep << 39) | (freq << 24) | member
-struct DevError {
+struct __align__(16) DevError {
     unsigned long long key;   // ~0ull = none
-    int32_t pivot;
+    int32_t pivot;            // (key, pivot, rank1) change together: one 128-bit CAS
     int32_t rank1;
+    int32_t aborted;          // slab march: a peer rank's signal never came (k_slab_wait timeout)
+    int32_t pad;
 };
 
 // ------------------------------------------------------------- shared helpers
 
+// Record a failure if its key is lower than the recorded one.  The key and
+// its payload (pivot, rank1) are replaced together by a 128-bit compare-and-
+// swap, so the surviving record is always one failure's own (the lowest key
+// with its pivot), whatever the interleaving of concurrent reports.
 __device__ __forceinline__ void report_failure(DevError* err, unsigned long long key, int pivot, int rank1) {
-    const unsigned long long old = atomicMin(&err->key, key);
-    if (key < old) {            // benign race on the payload: the lowest key's writer wins last
-        err->pivot = pivot;
-        err->rank1 = rank1;
+    const unsigned long long payload =
+        static_cast<unsigned long long>(static_cast<unsigned>(pivot)) | (static_cast<unsigned long long>(rank1) << 32);
+    unsigned long long* p = &err->key;
+    unsigned long long cur_k = *reinterpret_cast<volatile unsigned long long*>(p);
+    unsigned long long cur_p = *reinterpret_cast<volatile unsigned long long*>(p + 1);
+    while (key < cur_k) {
+        unsigned long long got_k, got_p;
+        asm volatile(
+            "{\n"
+            ".reg .b128 cmp, val, old;\n"
+            "mov.b128 cmp, {%2, %3};\n"
+            "mov.b128 val, {%4, %5};\n"
+            "atom.global.cas.b128 old, [%6], cmp, val;\n"
+            "mov.b128 {%0, %1}, old;\n"
+            "}\n"
+            : "=l"(got_k), "=l"(got_p)
+            : "l"(cur_k), "l"(cur_p), "l"(key), "l"(payload), "l"(p)
+            : "memory");
+        if (got_k == cur_k && got_p == cur_p) break;      // swapped
+        cur_k = got_k;
+        cur_p = got_p;
     }
 }
 

@@ -203,10 +203,94 @@ inline bool needs_serial(const pe3d_grid* g, const std::vector<pe3d::FreqDev>& f
     return false;
 }
 
-inline int decode_error(Handle* h, cudaStream_t stream, pe3d_error* err) {
+// ------------------------------------------------------------ azimuth failures
+// The periodic azimuth sweep solves B = diag I + off (S + S^-1) by its
+// circulant factorisation, which has no pivots.  Which steps the REFERENCE
+// would abort on is decided here, on the host, by the reference's own
+// algorithm: the Sherman-Morrison cyclic solve of the constant matrix
+// (ref tridiag.py:186-212 with operators.py:256-262: sub = sup = off,
+// main = diag), its pivot checks (tridiag.py:145-167) and its rank-1
+// denominator check (:205-210), in numpy's arithmetic (pe3d_device.cuh).
+// All Nz members share the matrix, so the failing member is 0 (argmin of
+// equal magnitudes, ref tridiag.py:146-148, lowest tile :274-280).  A strictly
+// diagonally dominant matrix with margin cannot fail those checks, so the
+// O(n) recurrence runs only for the others.
+struct HostFail {
+    unsigned long long key = ~0ull;
+    int32_t pivot = 0, rank1 = 0;
+};
+
+// true when the reference's cyclic solve of (diag, off) of size n raises
+inline bool reference_cyclic_fails(pe3d::cplx diag, pe3d::cplx off, int n, int32_t* pivot, int32_t* rank1) {
+    using namespace pe3d;
+    const double ad = cabs(diag), ao = cabs(off);
+    if (ad - 2.0 * ao > 1e-200 * ad && ad - 2.0 * ao > 1e-280) return false;
+    const cplx alpha = off, beta = off;
+    const cplx gamma = ad > 0.0 ? cneg(diag) : cone();
+    const cplx main0 = csub(diag, gamma);
+    const cplx mainl = csub(diag, cdiv(cmul(alpha, beta), gamma));
+    auto main_at = [&](int k) { return k == 0 ? main0 : (k == n - 1 ? mainl : diag); };
+    std::vector<cplx> cp(n > 1 ? n - 1 : 1), inv(n), x(n);
+    for (int k = 0; k < n; ++k) {
+        const cplx denom = k == 0 ? main_at(0) : csub(main_at(k), cmul(off, cp[k - 1]));
+        if (cabs(denom) < PIVOT_FLOOR) { *pivot = k; *rank1 = 0; return true; }
+        inv[k] = crecip(denom);
+        if (k < n - 1) cp[k] = cmul(off, inv[k]);
+    }
+    // q = A'^-1 (gamma e_0 + beta e_(n-1))
+    for (int k = 0; k < n; ++k) {
+        const cplx spike = k == 0 ? gamma : (k == n - 1 ? beta : czero());
+        x[k] = k == 0 ? cmul(spike, inv[0]) : cmul(csub(spike, cmul(off, x[k - 1])), inv[k]);
+    }
+    for (int k = n - 2; k >= 0; --k) x[k] = csub(x[k], cmul(cp[k], x[k + 1]));
+    const cplx weight = cdiv(alpha, gamma);
+    const cplx denom = cadd(cadd(cone(), x[0]), cmul(weight, x[n - 1]));
+    if (cabs(denom) < PIVOT_FLOOR) { *pivot = n; *rank1 = 1; return true; }
+    return false;
+}
+
+// lowest (step, frequency) at which the reference's periodic azimuth solve
+// would raise, over the steps of a march
+inline HostFail azimuth_failures(const pe3d_grid* g, const pe3d_coeffs* c) {
+    HostFail hf;
+    if (g->topology != PE3D_PERIODIC) return hf;
+    for (int s = 0; s < g->n_steps; ++s) {
+        const int j_new = g->first_index + s + 1;
+        const double r_new = g->r_start + j_new * g->delta_r;          // Grid3D.range_at
+        for (int f = 0; f < g->n_freq; ++f) {
+            const pe3d::cplx cy = pe3d::mk(c[f].cy_lhs.re, c[f].cy_lhs.im);
+            const double sc = pe3d::azimuth_scale(c[f].k0, r_new, g->delta_theta);
+            const pe3d::cplx diag = pe3d::csub(pe3d::cone(), pe3d::crmul(sc, pe3d::crmul(2.0, cy)));
+            const pe3d::cplx off = pe3d::crmul(sc, cy);
+            int32_t pivot, rank1;
+            if (reference_cyclic_fails(diag, off, g->n_theta, &pivot, &rank1)) {
+                const unsigned long long key = pe3d::fail_key(j_new, 1, f, 0);
+                if (key < hf.key) hf = HostFail{key, pivot, rank1};
+            }
+        }
+        if (hf.key != ~0ull) break;                                     // later steps have larger keys
+    }
+    return hf;
+}
+
+inline int decode_error(Handle* h, cudaStream_t stream, pe3d_error* err, const HostFail* hf = nullptr) {
     pe3d::DevError de;
     CK(cudaMemcpyAsync(&de, h->err.ptr, sizeof(de), cudaMemcpyDeviceToHost, stream), "error readback");
     CK(cudaStreamSynchronize(stream), "march");
+    if (hf && hf->key < de.key) {
+        de.key = hf->key;
+        de.pivot = hf->pivot;
+        de.rank1 = hf->rank1;
+    }
+    if (de.aborted) {
+        if (err) {
+            std::memset(err, 0, sizeof(*err));
+            err->range_index = -1;
+            std::snprintf(err->message, sizeof(err->message),
+                          "slab march aborted: a peer rank did not signal within PE3D_SLAB_TIMEOUT_MS");
+        }
+        return PE3D_CUDA_ERROR;
+    }
     if (de.key == NO_ERROR) return PE3D_OK;
     if (err) {
         std::memset(err, 0, sizeof(*err));

@@ -166,7 +166,8 @@ inline cudaError_t launch_pdl(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 
 bool encode_swizzled_map(CUtensorMap* tm, const void* base, int rank, const uint64_t* dims,
                          const uint64_t* strides, const uint32_t* box, int swizzle_bytes);
 cudaError_t launch_slab_signal(unsigned long long* const* flags, int n, cudaStream_t s);
-cudaError_t launch_slab_wait(const unsigned long long* flag, unsigned long long target, cudaStream_t s);
+cudaError_t launch_slab_wait(const unsigned long long* flag, unsigned long long target, DevError* err,
+                             cudaStream_t s);
 void ring_shape(int n_theta, int* L, int* RW);
 int ring_table_elems(int n_theta);   // complex entries per (step, frequency) ring table
 cudaError_t launch_factor_depth(const LaunchCtx& c, const cplx* local, int64_t local_fstride, int step_for_error);

@@ -101,7 +101,8 @@ __global__ void k_ring_setup(cplx* __restrict__ table, const FreqDev* __restrict
     const int q_last = lay.n_chunks - 1;
     const cplx rhoN = cmul(qp[q_last], pw[n_theta - q_last * lay.L]);
     const cplx wrap = csub(cone(), rhoN);
-    if (!rf.diagonal && cabs(wrap) < PIVOT_FLOOR) report_failure(err, fail_key(j_new, 1, f, 0), n_theta, 1);
+    // failures: the reference's own pivot checks of this matrix decide, on the
+    // host (pe3d_host.h azimuth_failures); the circulant factorisation has none
     T[0] = rf.rho;
     T[1] = rf.scale;
     T[2] = crecip(wrap);

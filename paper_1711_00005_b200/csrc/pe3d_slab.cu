@@ -32,12 +32,24 @@ __global__ void k_slab_signal(SlabFlags flags, int n) {
         asm volatile("red.release.sys.global.add.u64 [%0], 1;\n" ::"l"(flags.f[q]) : "memory");
 }
 
-__global__ void k_slab_wait(const unsigned long long* flag, unsigned long long target) {
+// Bounded: after timeout_ns without the peers' signals (a failed rank) the
+// wait gives up, marks the march aborted in the error record (decoded as
+// PE3D_CUDA_ERROR) and every later wait of the march returns at once, so no
+// rank's stream can hang on a peer that will never signal.
+__global__ void k_slab_wait(const unsigned long long* flag, unsigned long long target, DevError* err,
+                            unsigned long long timeout_ns) {
     if (threadIdx.x != 0) return;
-    unsigned long long v;
+    if (*reinterpret_cast<volatile int32_t*>(&err->aborted)) return;
+    unsigned long long v, t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     for (;;) {
         asm volatile("ld.acquire.sys.global.u64 %0, [%1];\n" : "=l"(v) : "l"(flag) : "memory");
         if (v >= target) break;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > timeout_ns) {
+            atomicExch(&err->aborted, 1);
+            return;
+        }
         __nanosleep(256);
     }
     __threadfence_system();
@@ -50,8 +62,12 @@ cudaError_t launch_slab_signal(unsigned long long* const* flags, int n, cudaStre
     return cudaGetLastError();
 }
 
-cudaError_t launch_slab_wait(const unsigned long long* flag, unsigned long long target, cudaStream_t s) {
-    k_slab_wait<<<1, 32, 0, s>>>(flag, target);
+// PE3D_SLAB_TIMEOUT_MS bounds every cross-rank wait (default 20 s)
+cudaError_t launch_slab_wait(const unsigned long long* flag, unsigned long long target, DevError* err,
+                             cudaStream_t s) {
+    const char* env = getenv("PE3D_SLAB_TIMEOUT_MS");
+    const unsigned long long ms = env ? strtoull(env, nullptr, 10) : 20000ull;
+    k_slab_wait<<<1, 32, 0, s>>>(flag, target, err, ms * 1000000ull);
     return cudaGetLastError();
 }
 
@@ -283,6 +299,7 @@ static int slab_impl(Handle* h, const pe3d_grid* g, const pe3d_coeffs* coeffs, i
                                g->r_input, ea0), "prepare");
         if (peer) CK(pe3d::launch_slab_signal(f1.data(), N, s), "signal");
     }
+    const bool stall_test = getenv("PE3D_SLAB_TEST_STALL") != nullptr;
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0), "event");
     CK(cudaEventCreate(&e1), "event");
@@ -294,10 +311,11 @@ static int slab_impl(Handle* h, const pe3d_grid* g, const pe3d_coeffs* coeffs, i
         const unsigned long long target = (unsigned long long)N * (k + 1);
         for (int q = 0; q < R; ++q) {
             if (peer) {
-                CK(pe3d::launch_slab_wait(own(q).flags + 1, target, s), "wait");
+                CK(pe3d::launch_slab_wait(own(q).flags + 1, target, c1.err, s), "wait");
                 const pe3d::LaunchCtx c = k1_ctx(q);
                 CK(pe3d::launch_depth_scan(c, own(q).A, own(q).R), "depth");
-                CK(pe3d::launch_slab_signal(f0.data(), N, s), "signal");
+                if (!(stall_test && k == 1 && q == R - 1))      // PE3D_SLAB_TEST_STALL: a rank that never signals
+                    CK(pe3d::launch_slab_signal(f0.data(), N, s), "signal");
             } else {
                 CK(pe3d::launch_depth_scan(c1, Abuf + q * part, Bbuf + q * part), "depth");
             }
@@ -313,7 +331,7 @@ static int slab_impl(Handle* h, const pe3d_grid* g, const pe3d_coeffs* coeffs, i
             ea.write_temp = (k < g->n_steps - 1);
             if (peer) {
                 if (ea.write_temp) set_peers_k2(ea, q);
-                CK(pe3d::launch_slab_wait(own(q).flags, target, s), "wait");
+                CK(pe3d::launch_slab_wait(own(q).flags, target, c1.err, s), "wait");
                 CK(pe3d::launch_azimuth_scan(c2, own(q).R, own(q).R, h->ring_tab.as<cplx>() + int64_t(k) * E, r_new,
                                              ea),
                    "azimuth");
@@ -327,7 +345,8 @@ static int slab_impl(Handle* h, const pe3d_grid* g, const pe3d_coeffs* coeffs, i
         if (!peer && k < g->n_steps - 1) CK(transpose(Wbuf, Abuf), "transpose");
     }
     CK(cudaEventRecord(e1, s), "event");
-    int st = decode_error(h, s, err);
+    const HostFail hf = azimuth_failures(g, coeffs);          // the ring sweep has no pivots
+    int st = decode_error(h, s, err, &hf);
     float ms = 0.f;
     cudaEventElapsedTime(&ms, e0, e1);
     cudaEventDestroy(e0);
@@ -418,6 +437,9 @@ int pe3d_slab_p2p_export(void* handle, const pe3d_grid* g, int32_t N, int32_t ra
     CK(h->field_b.ensure(size_t(part) * sizeof(cplx)), "alloc");
     CK(h->slab_flags.ensure(2 * sizeof(unsigned long long)), "alloc");
     CK(cudaMemset(h->slab_flags.ptr, 0, 2 * sizeof(unsigned long long)), "memset");
+    // the counters must be zero before any peer can signal (the caller's barrier
+    // follows this call): cudaMemset may return before the device ran it
+    CK(cudaDeviceSynchronize(), "sync");
     cudaIpcMemHandle_t hd[3];
     CK(cudaIpcGetMemHandle(&hd[0], h->field_a.ptr), "ipc handle");
     CK(cudaIpcGetMemHandle(&hd[1], h->field_b.ptr), "ipc handle");

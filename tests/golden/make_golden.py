@@ -32,6 +32,7 @@ sys.path.insert(0, str(REPO))
 sys.path.insert(0, "/root/reference/pkg/src")
 
 import pe3d                                      # noqa: E402  (the reference)
+import pe3d.errors                               # noqa: E402
 import pe3d.marching as ref_marching             # noqa: E402
 from pe3d.selftest import random_system          # noqa: E402
 
@@ -174,6 +175,34 @@ def full_size_fixture(name, frequency, n_steps):
     print(f"{name} f={frequency}: {wall / n_steps:.2f} s/step (reference)")
 
 
+def azimuth_singular_fixture():
+    """Hand-built step coefficients whose periodic azimuth system is singular
+    for the reference's Sherman-Morrison solve (diag = 0: StepError at the
+    azimuth sweep, pivot n - 1) or degenerate without tripping its checks
+    (diag = 2 off: no error) -- ref marching.py:124-131, tridiag.py:145-212."""
+    grid = pe3d.Grid3D(10, 8, 16, 5.0, 2 * math.pi / 8, 4.0, 5.0)
+    env = pe3d.Environment(1500.0, pe3d.SoundSpeedProfile.uniform(1500.0), 6000.0,
+                           pe3d.Absorber(0.75 * grid.depth_extent, 0.01), grid.depth_extent)
+    k0 = 0.2
+    s = 1.0 / ((k0 * grid.range_at(1)) * grid.delta_theta) ** 2
+    base = pe3d.StepCoefficients.for_step(k0, grid.delta_r)
+    out = {"k0": k0, "cx_lhs": base.cx_lhs, "cx_rhs": base.cx_rhs, "delta": base.delta}
+    for tag, c in (("diag0", 1 / (2 * s)), ("diag2off", 1 / (4 * s))):
+        co = pe3d.StepCoefficients(delta=base.delta, cx_lhs=base.cx_lhs, cx_rhs=base.cx_rhs, cy_lhs=complex(c),
+                                   cy_rhs=-complex(c))
+        state = pe3d.MarchState(pe3d.FieldSlab(np.ones((8, 16), complex), grid.r_start), 0, co, env, grid, k0)
+        out[f"{tag}_cy"] = complex(c)
+        try:
+            with np.errstate(all="ignore"):
+                pe3d.range_step(state)
+            out[f"{tag}_error"] = np.array([0, -1, -1, -1])
+        except pe3d.errors.StepError as e:
+            cause = e.__cause__
+            out[f"{tag}_error"] = np.array([1, e.range_index, e.member_index, cause.pivot_index])
+            assert e.sweep == "azimuth"
+    np.savez_compressed(HERE / "azimuth_singular.npz", **out)
+
+
 def output_fixture():
     """TL files written by the reference's own writers (ref output.py:60-122)
     for a fixed small result, plus the inputs that produced them."""
@@ -202,6 +231,7 @@ def main(which=None):
         "small": lambda: (small_march_fixture("periodic"), small_march_fixture("sector")),
         "cfg1": cfg1_full_fixture,
         "output": output_fixture,
+        "azsing": azimuth_singular_fixture,
         "cfg2": lambda: full_size_fixture("cfg2", 100.0, 20),
         "cfg3": lambda: full_size_fixture("cfg3", 25.0, 20),
         "cfg4": lambda: (full_size_fixture("cfg4", 50.0, 10), full_size_fixture("cfg4", 500.0, 10)),

@@ -135,3 +135,49 @@ def test_slab_shape_rules():
     v = np.arange(64 * 256).reshape(64, 256)
     parts = [depth_slab(v, 4, r) for r in range(4)]
     assert np.array_equal(np.concatenate(parts, axis=1), v)
+
+
+def _farm_worker(rank, world, port, queue):
+    import numpy as np
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1711_00005_b200 import configs, parallel
+    cfg = configs.build("cfg4", n_range=6, frequencies=tuple(50.0 + 40.0 * i for i in range(5)), output_stride=3)
+    report = parallel.distributed_frequency_farm(cfg, list(cfg.source.frequencies), device=0)
+    if rank == 0:
+        queue.put((rank, [(r.frequency, np.asarray(r.tl_field).copy(), np.asarray(r.final_slab.values).copy(),
+                           r.clamped_samples) for r in report.results], len(report.failures)))
+    else:
+        queue.put((rank, None, len(report.failures)))
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_gloo_two_processes_real_frequency_farm():
+    """Two real processes (gloo, world size 2) run distributed_frequency_farm
+    with the CUDA kernels -- both on device 0 here, each marching its static
+    block independently (ref parallel.py:85-97, 143-185; no kernel of one
+    process waits for the other's) -- and rank 0's gathered report is bitwise
+    the single-process batched march."""
+    import numpy as np
+    from paper_1711_00005_b200 import configs, march_frequencies
+    ctx = mp.get_context("spawn")
+    queue = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_farm_worker, args=(r, 2, port, queue)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = dict((t[0], t[1:]) for t in (queue.get(timeout=300) for _ in range(2)))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    gathered, n_fail = out[0]
+    assert n_fail == 0 and out[1][1] == 0
+    cfg = configs.build("cfg4", n_range=6, frequencies=tuple(50.0 + 40.0 * i for i in range(5)), output_stride=3)
+    ref = march_frequencies(cfg, list(cfg.source.frequencies))
+    assert [g[0] for g in gathered] == [r.frequency for r in ref]
+    for (f, tl, fin, cl), r in zip(gathered, ref):
+        assert tl.tobytes() == np.asarray(r.tl_field).tobytes()
+        assert fin.tobytes() == r.final_slab.values.tobytes()
+        assert cl == r.clamped_samples

@@ -765,3 +765,78 @@ def test_starter_column_flag_bitwise_equal_to_slab(name):
         out.append((tl, fin, cl))
     for x, y in zip(*out):
         assert x.tobytes() == y.tobytes()
+
+
+def test_slab_wait_times_out_instead_of_hanging(monkeypatch):
+    """A rank that never signals (PE3D_SLAB_TEST_STALL drops one depth-sweep
+    signal of the peer-transport slab march): the bounded cross-rank wait
+    gives up after PE3D_SLAB_TIMEOUT_MS, later waits return at once, and the
+    march fails with a CUDA error instead of hanging the stream."""
+    from paper_1711_00005_b200 import slab_march
+    from paper_1711_00005_b200.errors import NativeError
+    cfg = configs.build("cfg5", n_range=4, output_stride=2)
+    grid = cfg.grid
+    small = Config(Grid3D(4, 256, 2048, grid.delta_r, 2 * math.pi / 256, grid.delta_z, grid.r_start),
+                   cfg.environment, SourceSpec((500.0,), 300.0), RunOptions(output_stride=2))
+    monkeypatch.delenv("PE3D_SLAB_COPY", raising=False)
+    monkeypatch.setenv("PE3D_SLAB_TEST_STALL", "1")
+    monkeypatch.setenv("PE3D_SLAB_TIMEOUT_MS", "300")
+    with pytest.raises(NativeError, match="aborted"):
+        slab_march(small, 500.0, 2)
+    monkeypatch.delenv("PE3D_SLAB_TEST_STALL")
+    ok = slab_march(small, 500.0, 2)                     # the handle recovers
+    assert np.isfinite(ok.final).all()
+
+
+def test_singular_payload_is_the_lowest_members_own():
+    """Many singular members failing at different pivot rows in different
+    tiles: the error names the lowest member AND that member's own pivot
+    (ref tridiag.py:274-280) -- the key and its payload are swapped together."""
+    rng = np.random.default_rng(11)
+    n = 9
+    systems = [TriDiagSystem(*O.random_system(rng, n, False)) for _ in range(300)]
+    expected = None
+    for member, pivot in ((290, 1), (77, 6), (150, 3), (77 + 64, 2), (5 + 128, 8), (9, 4)):
+        main = np.asarray(systems[member].main).copy()
+        sub = np.asarray(systems[member].sub).copy()
+        sup = np.asarray(systems[member].sup).copy()
+        # make elimination row `pivot` exactly singular: zero row and off-diagonals feeding it
+        main[pivot] = 0.0
+        if pivot > 0:
+            sub[pivot - 1] = 0.0
+        systems[member] = TriDiagSystem(sub, main, sup, systems[member].rhs)
+        if expected is None or member < expected[0]:
+            expected = (member, pivot)
+    batch = SolveBatch.from_systems(systems)
+    with pytest.raises(SingularSystemError) as ei:
+        solve_batch(batch)
+    assert (ei.value.member_index, ei.value.pivot_index) == expected
+
+
+def test_azimuth_step_error_matches_reference(golden):
+    """Hand-built coefficients whose periodic azimuth system the reference's
+    Sherman-Morrison solve rejects (diag = 0: StepError(1, "azimuth", member 0)
+    caused by SingularSystemError(pivot n-1)) or accepts although degenerate
+    (diag = 2 off): the same outcome from the B200 range_step, whose
+    circulant sweep leaves the decision to the reference's own pivot checks
+    (ref marching.py:124-131, tridiag.py:145-212; fixture from the reference)."""
+    fx = golden("azimuth_singular.npz")
+    grid = Grid3D(10, 8, 16, 5.0, 2 * math.pi / 8, 4.0, 5.0)
+    env = Environment(1500.0, SoundSpeedProfile.uniform(1500.0), 6000.0, Absorber(0.75 * grid.depth_extent, 0.01),
+                      grid.depth_extent)
+    k0 = float(fx["k0"])
+    for tag in ("diag0", "diag2off"):
+        cy = complex(fx[f"{tag}_cy"])
+        co = StepCoefficients(delta=complex(fx["delta"]), cx_lhs=complex(fx["cx_lhs"]), cx_rhs=complex(fx["cx_rhs"]),
+                              cy_lhs=cy, cy_rhs=-cy)
+        state = MarchState(FieldSlab(np.ones((8, 16), dtype=complex), grid.r_start), 0, co, env, grid, k0)
+        raised, j, member, pivot = (int(x) for x in fx[f"{tag}_error"])
+        if raised:
+            with pytest.raises(StepError) as info:
+                range_step(state)
+            e = info.value
+            assert (e.range_index, e.sweep, e.member_index) == (j, "azimuth", member)
+            assert e.__cause__.pivot_index == pivot
+        else:
+            with np.errstate(all="ignore"):
+                range_step(state)
