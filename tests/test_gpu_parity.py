@@ -321,18 +321,38 @@ def test_cluster_depth_sweep_matches_single_cta(monkeypatch, n_depth, topology):
     assert tl_err(got.tl_field, orc.tl_field) <= TL_TOL
 
 
-def test_cluster_kernels_deterministic():
-    """Race check for the DSMEM exchanges (st.async + mbarrier, double
-    buffered): a march that runs both cluster kernels (4096-row columns,
-    2048-azimuth rings) five times gives bitwise identical results."""
-    cfg = configs.build("cfg5", n_range=6, output_stride=3)
-    grid = cfg.grid
-    small = Config(Grid3D(6, 2048, 4096, grid.delta_r, 2 * math.pi / 2048, grid.delta_z, grid.r_start),
-                   cfg.environment, SourceSpec((500.0,), 600.0), RunOptions(output_stride=3))
-    runs = [march_frequencies(small, [500.0], flags=_native.FLAG_NO_GRAPH)[0] for _ in range(5)]
-    for r in runs[1:]:
-        assert r.final_slab.values.tobytes() == runs[0].final_slab.values.tobytes()
-        assert r.tl_field.tobytes() == runs[0].tl_field.tobytes()
+@pytest.mark.parametrize("family", ["split_cluster", "lockstep_cluster", "warp_chains"])
+def test_async_kernels_race_stress(monkeypatch, family):
+    """Race stress for the asynchronous kernels (compute-sanitizer is closed on
+    this GPU pool, profiles/r02_compute_sanitizer_closed.txt): TMA producer /
+    consumer mbarrier rings, DSMEM st.async exchanges, the split-column
+    carries.  Twenty marches per family, graphed and unGraphed, must be
+    bitwise identical -- the split sweeps with the corrected cluster ring
+    (cfg5 shape), the lock-step cluster sweeps, and the ring-per-warp TMA
+    sweep with 1, 2 and 8 concurrent step chains (cfg4 shape)."""
+    if family == "warp_chains":
+        cfg = configs.build("cfg4", n_range=6, frequencies=(50.0, 80.0, 130.0, 200.0, 310.0, 420.0, 460.0, 500.0),
+                            output_stride=3)
+        freqs = list(cfg.source.frequencies)
+        settings = [(c, fl) for c in ("1", "2", "8") for fl in (0, _native.FLAG_NO_GRAPH)] * 4
+    else:
+        if family == "lockstep_cluster":
+            monkeypatch.setenv("PE3D_DEPTH_NO_SPLIT", "1")
+        cfg5 = configs.build("cfg5", n_range=6, output_stride=3)
+        grid = cfg5.grid
+        cfg = Config(Grid3D(6, 2048, 4096, grid.delta_r, 2 * math.pi / 2048, grid.delta_z, grid.r_start),
+                     cfg5.environment, SourceSpec((500.0,), 600.0), RunOptions(output_stride=3))
+        freqs = [500.0]
+        settings = [(None, fl) for fl in (0, _native.FLAG_NO_GRAPH)] * 10
+    first = None
+    for chains, flags in settings:
+        if chains:
+            monkeypatch.setenv("PE3D_CHAINS", chains)
+        runs = march_frequencies(cfg, freqs, flags=flags)
+        got = [(r.final_slab.values.tobytes(), r.tl_field.tobytes(), r.clamped_samples) for r in runs]
+        if first is None:
+            first = got
+        assert got == first
 
 
 @pytest.mark.parametrize("nranks", [2, 4])
