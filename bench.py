@@ -266,7 +266,7 @@ class DeviceMarch:
         import torch
         import ctypes as C
         from paper_1711_00005_b200 import _native
-        from paper_1711_00005_b200.environment import gaussian_starter, wavenumber
+        from paper_1711_00005_b200.environment import gaussian_starter_column, wavenumber
         from paper_1711_00005_b200.marching import _local_column
         from paper_1711_00005_b200.operators import StepCoefficients
         self.C, self.native, self.torch = C, _native, torch
@@ -276,12 +276,14 @@ class DeviceMarch:
         k0s = [wavenumber(f, env.c0) for f in freqs]
         self.coeffs = _native.make_coeffs(k0s, [StepCoefficients.for_step(k0, grid.delta_r) for k0 in k0s])
         self.local_np = np.ascontiguousarray(np.stack([_local_column(env, grid, grid.r_start, k0) for k0 in k0s]))
-        self.u0_np = np.ascontiguousarray(np.stack([gaussian_starter(grid, source, k0).values for k0 in k0s]))
+        self.cols_np = np.ascontiguousarray(np.stack([gaussian_starter_column(grid, source, k0) for k0 in k0s]))
+        self.slab_shape = (len(freqs), grid.n_azimuth, grid.n_depth)
         dev = torch.device("cuda", local_dev)
         self.dev = dev
         self.d_local = torch.from_numpy(self.local_np.view(np.float64)).to(dev)
-        self.d_u0 = torch.from_numpy(self.u0_np.view(np.float64)).to(dev)
-        self.d_final = torch.empty_like(self.d_u0)
+        # the Gaussian starter as one column per frequency (PE3D_FLAG_STARTER_COLUMN, as the drop-in passes it)
+        self.d_u0 = torch.from_numpy(self.cols_np.view(np.float64)).to(dev)
+        self.d_final = torch.empty(self.slab_shape + (2,), dtype=torch.float64, device=dev)
         self.d_clamped = torch.zeros(len(freqs), dtype=torch.int64, device=dev)
         S = 1 + steps // stride
         self.tl = torch.empty((len(freqs), S, grid.n_azimuth, grid.n_depth), dtype=torch.float64,
@@ -293,7 +295,8 @@ class DeviceMarch:
     def march(self, n_steps, flags=0, outputs=True):
         from paper_1711_00005_b200.marching import _grid_params
         C = self.C
-        g = _grid_params(self.grid, len(self.freqs), n_steps, self.stride, 0, self.grid.r_start, flags)
+        g = _grid_params(self.grid, len(self.freqs), n_steps, self.stride, 0, self.grid.r_start,
+                         flags | self.native.FLAG_STARTER_COLUMN)
         self.native.call("pe3d_march_device", self.h, g, self.coeffs, C.c_void_p(self.d_local.data_ptr()),
                          C.c_void_p(self.d_u0.data_ptr()),
                          C.c_void_p(self.d_final.data_ptr()) if outputs else None,
@@ -508,8 +511,8 @@ def host_march_e2e(m, steps, stride, world, total_points):
     S = 1 + steps // stride
     h_local = torch.from_numpy(m.local_np.view(np.float64)).pin_memory()
     # the drop-in's starter: one Gaussian column per frequency (PE3D_FLAG_STARTER_COLUMN)
-    h_u0 = torch.from_numpy(np.ascontiguousarray(m.u0_np[:, 0, :]).view(np.float64)).pin_memory()
-    h_final = torch.empty(m.u0_np.shape + (2,), dtype=torch.float64).pin_memory()
+    h_u0 = torch.from_numpy(m.cols_np.view(np.float64)).pin_memory()
+    h_final = torch.empty(m.slab_shape + (2,), dtype=torch.float64).pin_memory()
     h_tl = torch.empty((F, S, m.grid.n_azimuth, m.grid.n_depth), dtype=torch.float64).pin_memory()
     h_cl = torch.zeros(F, dtype=torch.int64).pin_memory()
     g = _grid_params(m.grid, F, steps, stride, 0, m.grid.r_start, m.native.FLAG_STARTER_COLUMN)

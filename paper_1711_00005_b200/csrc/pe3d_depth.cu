@@ -1325,7 +1325,7 @@ __global__ void k_split_setup(const cplx* __restrict__ mul_tab, int n_virtual, c
 // din_(s-1) = X_s + A_s cin_s + P_s din_s.  Written lane-ordered for the
 // azimuth sweep's stage (azimuth m = seg*NS + q*L + k at seg*NS + k*32 + q).
 constexpr int SPLIT_MAX = 8;
-__global__ void __launch_bounds__(256) k_split_carry(const cplx* __restrict__ sp_tot, const cplx* __restrict__ sp_pa,
+__global__ void __launch_bounds__(64) k_split_carry(const cplx* __restrict__ sp_tot, const cplx* __restrict__ sp_pa,
                                                      cplx* __restrict__ sp_cd, int n_freq, int n_theta, int split,
                                                      int L) {
     griddep_wait();                                 // the depth sweep's totals
@@ -1378,7 +1378,8 @@ int depth_split_plan(const LaunchCtx& c, int periodic) {
 
 cudaError_t launch_split_carry(const LaunchCtx& c) {
     const int64_t n = int64_t(c.n_freq) * c.n_theta;
-    return launch_pdl(c.pdl != 0, k_split_carry, dim3(unsigned((n + 255) / 256)), dim3(256), 0, c.stream, c.sp_tot,
+    // small CTAs: one thread per column is little work, so spread it over many SMs (latency bound)
+    return launch_pdl(c.pdl != 0, k_split_carry, dim3(unsigned((n + 63) / 64)), dim3(64), 0, c.stream, c.sp_tot,
                       c.sp_pa, c.sp_cd, c.n_freq, c.n_theta, c.split, ring_segment(c.n_theta) / 32);
 }
 

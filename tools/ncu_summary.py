@@ -48,7 +48,9 @@ def main():
         base = re.search(r"(k_\w+)", name).group(1)
         src = list(csv.reader(io.StringIO(ncu("-i", rep, "--page", "source", "--csv", "--print-source", "sass",
                                               "--kernel-name", "regex:" + base + "(<|$)"))))
-        hdr, data = src[1], src[2:]
+        hdr = src[1]
+        iE0 = hdr.index("Instructions Executed")
+        data = [r for r in src[2:] if len(r) == len(hdr) and r[iE0].isdigit()]   # one kernel's rows
         iE = hdr.index("Instructions Executed")
         names = [x for x in hdr if x.startswith("stall_") and "(Not" not in x]
         idx = {n: hdr.index(n) for n in names}
