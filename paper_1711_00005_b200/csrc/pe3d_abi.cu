@@ -518,9 +518,8 @@ static int march_device_impl(void* handle, const pe3d_grid* g, const pe3d_coeffs
         add(&gen, sizeof(gen));
         add(&p.ctx.split, sizeof(p.ctx.split));
         // the A/B switches pick kernels and launch attributes baked into the graph
-        for (const char* name : {"PE3D_NO_PDL", "PE3D_CLUSTER_L", "PE3D_DEPTH_NO_CLUSTER", "PE3D_DEPTH_NO_TMA",
-                                 "PE3D_DEPTH_WIDE_SCAN", "PE3D_RING_BLOCK", "PE3D_RING_STAGES", "PE3D_RING_CPASYNC",
-                                 "PE3D_RING_TMA", "PE3D_DEPTH_NO_SPLIT"}) {
+        for (const char* name : {"PE3D_NO_PDL", "PE3D_CLUSTER_L", "PE3D_DEPTH_NO_CLUSTER", "PE3D_RING_BLOCK",
+                                 "PE3D_RING_CPASYNC", "PE3D_DEPTH_NO_SPLIT"}) {
             const char* v = getenv(name);
             const std::string val = v ? std::string("=") + v : std::string("-");
             add(val.data(), val.size() + 1);
@@ -872,7 +871,7 @@ int pe3d_march_medium_host(void* handle, const pe3d_grid* g, const pe3d_coeffs* 
     // whole grid by a wide kernel on a side stream, one step ahead, so it
     // overlaps the previous step's azimuth sweep; the per-column scan reads
     // it (that kernel has one small CTA per column and is latency bound).
-    const bool pre = scan_path && !getenv("PE3D_MEDIUM_FUSED");
+    const bool pre = scan_path;
     if (pre) {
         if (!h->chain_stream[0]) CK(cudaStreamCreateWithFlags(&h->chain_stream[0], cudaStreamNonBlocking), "stream");
         for (int k = 0; k < 2; ++k)

@@ -1371,7 +1371,7 @@ int depth_split_plan(const LaunchCtx& c, int periodic) {
     if (!periodic || c.sector || c.n_peers > 0 || !c.k1_tab || c.n_tiles % 128 != 0 || CL < 2 || CL > SPLIT_MAX)
         return 0;
     if (ring_segment(c.n_theta) == 0 || !tensor_map_encoder()) return 0;
-    for (const char* name : {"PE3D_DEPTH_NO_SPLIT", "PE3D_RING_CPASYNC", "PE3D_DEPTH_NO_TMA", "PE3D_DEPTH_WIDE_SCAN"})
+    for (const char* name : {"PE3D_DEPTH_NO_SPLIT", "PE3D_RING_CPASYNC"})
         if (getenv(name)) return 0;
     return CL;
 }
@@ -1406,8 +1406,7 @@ cudaError_t launch_depth_scan(const LaunchCtx& c, const cplx* src, cplx* dst) {
                                                per, c.sector);
         return cudaGetLastError();
     };
-    if (c.n_peers > 0 || (c.n_tiles <= 512 && !getenv("PE3D_DEPTH_NO_TMA") &&
-                          !(c.n_tiles > 128 && getenv("PE3D_DEPTH_WIDE_SCAN")))) {
+    if (c.n_peers > 0 || c.n_tiles <= 512) {
         cudaError_t e = launch_depth_tma(c, src, dst);
         if (e != cudaErrorNotSupported || c.n_peers > 0) return e;    // peer output needs the TMA kernels
     }

@@ -1670,8 +1670,6 @@ static cudaError_t launch_tma_ring(const LaunchCtx& c, const cplx* src, cplx* ds
         cfg.gridDim = dim3(CL * c.num_sms);
         const int resident = cached_occupancy(reinterpret_cast<const void*>(kern), bytes, CL, nthr, &cfg);
         if (resident < 1) return cudaErrorInvalidConfiguration;
-        if (getenv("PE3D_DEBUG_CLUSTER"))
-            fprintf(stderr, "pe3d: TMA cluster ring L=%d CL=%d resident clusters=%d\n", L, CL, resident);
         const int per = int((items + resident - 1) / resident);
         const int clusters = int((items + per - 1) / per);
         cfg.gridDim = dim3(clusters * CL);
@@ -1752,7 +1750,6 @@ static cudaError_t launch_cluster_ring(const LaunchCtx& c, const cplx* src, cplx
         if (e != cudaSuccess) return e;
         if (n < 1) return cudaErrorInvalidConfiguration;
         resident[CL] = n;
-        if (getenv("PE3D_DEBUG_CLUSTER")) fprintf(stderr, "pe3d: cluster ring L=%d CL=%d resident clusters=%d\n", L, CL, n);
     }
     const int64_t items = int64_t(c.n_freq) * c.n_tiles;
     const int per = int((items + resident[CL] - 1) / resident[CL]);
@@ -1792,16 +1789,7 @@ cudaError_t launch_azimuth_scan(const LaunchCtx& c, const cplx* src, cplx* dst, 
             switch (plan.L) {
                 case 2: e = launch_tma_ring<2, 2, 3, false>(c, src, dst, table_step, E, ea); break;
                 case 4: e = launch_tma_ring<4, 2, 3, false>(c, src, dst, table_step, E, ea); break;
-                case 8: {
-                    // variants for A/B timing (PE3D_RING_TMA): 0 = 3 stages, 2 CTAs/SM (default);
-                    // 1 = 2 stages, 3 CTAs/SM; 2 = one row per warp (8 consumer warps), 2 CTAs/SM
-                    const char* v = getenv("PE3D_RING_TMA");
-                    const int var = v ? atoi(v) : 0;
-                    if (var == 1) e = launch_tma_ring<8, 2, 2, false, 3>(c, src, dst, table_step, E, ea);
-                    else if (var == 2) e = launch_tma_ring<8, 1, 2, false, 2>(c, src, dst, table_step, E, ea);
-                    else e = launch_tma_ring<8, 2, 3, false, 2>(c, src, dst, table_step, E, ea);
-                    break;
-                }
+                case 8: e = launch_tma_ring<8, 2, 3, false, 2>(c, src, dst, table_step, E, ea); break;   // 2 CTAs/SM
                 case 16: e = launch_tma_ring<16, 1, 2, false>(c, src, dst, table_step, E, ea); break;
                 default: break;
             }
@@ -1821,12 +1809,10 @@ cudaError_t launch_azimuth_scan(const LaunchCtx& c, const cplx* src, cplx* dst, 
     }
     if (plan.kind == 0 && ea.periodic) {
         const int E = plan.lay.E;
-        const int stages = getenv("PE3D_RING_STAGES") ? atoi(getenv("PE3D_RING_STAGES")) : 2;
         switch (plan.L) {
             case 2: return launch_warp_ring<2, 2, 3>(c, src, dst, table_step, E, r_new, ea);
             case 4: return launch_warp_ring<4, 2, 3>(c, src, dst, table_step, E, r_new, ea);
-            case 8: return stages == 3 ? launch_warp_ring<8, 2, 3>(c, src, dst, table_step, E, r_new, ea)
-                                       : launch_warp_ring<8, 2, 2>(c, src, dst, table_step, E, r_new, ea);
+            case 8: return launch_warp_ring<8, 2, 2>(c, src, dst, table_step, E, r_new, ea);
             case 16: return launch_warp_ring<16, 1, 2>(c, src, dst, table_step, E, r_new, ea);
             default: break;
         }
@@ -1887,7 +1873,7 @@ cudaError_t launch_azimuth_scan(const LaunchCtx& c, const cplx* src, cplx* dst, 
 cudaError_t launch_finish(const LaunchCtx& c, const cplx* src, int src_tiled, cplx* dst, double r,
                           const EpilogueArgs& ea) {
     const bool standard = ea.chunk_gap == 0 && (ea.chunk_cols == 0 || ea.chunk_cols == c.n_theta) && !ea.peer[0];
-    if (!src_tiled && standard && c.n_theta % PREP_MB == 0 && !getenv("PE3D_PREPARE_RINGS")) {
+    if (!src_tiled && standard && c.n_theta % PREP_MB == 0) {
         dim3 grid(c.n_theta / PREP_MB, (c.n_tiles * 8 + PREP_DB - 1) / PREP_DB, c.n_freq);
         k_prepare<<<grid, 256, 0, c.stream>>>(src, dst, c.fdev, c.n_theta, c.n_tiles, c.n_depth, r, c.delta_theta, ea);
         return cudaGetLastError();

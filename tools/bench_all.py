@@ -15,10 +15,10 @@ def main():
     for w in ("cfg1", "cfg2", "cfg4", "cfg5"):
         steps = {"cfg1": 400, "cfg2": 1000, "cfg4": 500, "cfg5": 200}[w]
         r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--workload", w, "--steps", str(steps),
-                            "--no-cpu", "--no-e2e"], capture_output=True, text=True)
+                            "--no-cpu", "--no-e2e", "--no-secondary"], capture_output=True, text=True)
         try:
             d = json.loads(r.stdout.strip().splitlines()[-1])
-            print(w, f"{d['value']:.3e} gp-steps/s", f"{d['ms_per_step'] * 1e3:.1f} us/step", d["roofline"]["kernel_ms"])
+            print(w, f"{d['value']:.3e} gp-steps/s", f"{d['ms_per_step'] * 1e3:.1f} us/step", {k: round(v["ms"] * 1e3, 1) for k, v in d["roofline"]["sweeps"].items()})
         except Exception:
             print(w, "FAILED", r.stderr[-500:])
     from paper_1711_00005_b200 import configs, march_frequencies
