@@ -13,7 +13,7 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
-from .errors import DomainError, InvariantError
+from .errors import InvariantError
 
 
 @dataclass(frozen=True)
@@ -37,18 +37,3 @@ class StepCoefficients:
         q = d / 4.0
         return cls(delta=d, cx_lhs=0.25 - q, cx_rhs=0.25 + q, cy_lhs=-q, cy_rhs=+q)
 
-
-def depth_scale(k0: float, delta_z: float) -> float:
-    """s_z = 1/(k0 dz)^2 (ref ``operators.py:90-94``)."""
-    if k0 <= 0 or delta_z <= 0:
-        raise DomainError("k0 and delta_z must be > 0")
-    return 1.0 / (k0 * delta_z) ** 2
-
-
-def azimuth_scale(k0: float, r: float, delta_theta: float) -> float:
-    """s_theta = 1/(k0 r dtheta)^2 (ref ``operators.py:97-102``)."""
-    if r <= 0:
-        raise DomainError(f"range must be > 0, got {r}")
-    if k0 <= 0 or delta_theta <= 0:
-        raise DomainError("k0 and delta_theta must be > 0")
-    return 1.0 / (k0 * r * delta_theta) ** 2
