@@ -427,8 +427,9 @@ k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ 
     cplx* sX = sY + nwarps;
     cplx* sUp = sX + nwarps;
     cplx* sDn = sUp + nwarps;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sDn + nwarps) + warp * STAGES;
-    uint64_t* tbar = reinterpret_cast<uint64_t*>(sDn + nwarps) + nwarps * STAGES;   // frequency-table copy
+    cplx* shalo = sDn + nwarps;                     // SPLIT: [2 edge threads][2 buffers] halo rows
+    uint64_t* bars = reinterpret_cast<uint64_t*>(shalo + 4) + warp * STAGES;
+    uint64_t* tbar = reinterpret_cast<uint64_t*>(shalo + 4) + nwarps * STAGES;   // frequency-table copy
 
     const int64_t g0 = int64_t(blockIdx.x) * cols_per_cta;
     const int64_t g1 = g0 + cols_per_cta < total_cols ? g0 + cols_per_cta : total_cols;
@@ -500,16 +501,24 @@ k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ 
             }
         }
     }
-    // SPLIT: the stencil rows across the sub-column edges, one column ahead
-    // (thread 0: the row above the sub-column, the last thread: the row below)
+    // SPLIT: the stencil rows across the sub-column edges (thread 0: the row
+    // above the sub-column, the last thread: the row below), copied one column
+    // ahead into a double buffer in shared memory (cp.async: the wait happens a
+    // column later, off this column's path); a sub-column edge that is the
+    // real column's surface or bottom gets zero
     const bool edge_thread = SPLIT && (t == 0 || t == nthreads - 1);
-    auto halo_load = [&](int hf, int hc) -> cplx {
+    cplx* my_halo = shalo + (t == 0 ? 0 : 2);
+    auto halo_fetch = [&](int hf, int hc, int buf) {
         const int hs = hf % split;
-        if (t == 0) return hs > 0 ? ldc(src_raw + ((int64_t(hf) * n_tiles - 1) * n_theta + hc) * 8 + 7) : czero();
-        return hs < split - 1 ? ldc(src_raw + ((int64_t(hf) * n_tiles + n_tiles) * n_theta + hc) * 8) : czero();
+        const bool inner = t == 0 ? hs > 0 : hs < split - 1;
+        if (inner)
+            cp_async16(&my_halo[buf], t == 0 ? src_raw + ((int64_t(hf) * n_tiles - 1) * n_theta + hc) * 8 + 7
+                                             : src_raw + ((int64_t(hf) * n_tiles + n_tiles) * n_theta + hc) * 8);
+        else
+            my_halo[buf] = czero();
+        cp_async_commit();
     };
-    cplx hal = czero();
-    if (edge_thread) hal = halo_load(f, col);
+    if (edge_thread) halo_fetch(f, col, 0);
 
     auto setup_freq = [&]() {
         if constexpr (TAB) {
@@ -562,9 +571,15 @@ k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ 
         }
         cplx* cur = stage + slot * 256;
         if (it == n_cols - 1) griddep_launch();     // last column: the next sweep may start launching
-        cplx hal_next = czero();
-        if (edge_thread && it + 1 < n_cols)
-            hal_next = col + 1 == n_theta ? halo_load(f + 1, 0) : halo_load(f, col + 1);
+        cplx hal = czero();
+        if (edge_thread) {
+            cp_async_wait<0>();                     // this column's halo (issued a column ago)
+            hal = my_halo[it & 1];
+            if (it + 1 < n_cols) {
+                if (col + 1 == n_theta) halo_fetch(f + 1, 0, (it + 1) & 1);
+                else halo_fetch(f, col + 1, (it + 1) & 1);
+            }
+        }
         PHASE(1);
         mbar_wait(&bars[slot], parity);
         PHASE(2);
@@ -586,7 +601,6 @@ k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ 
         if (SPLIT) {
             if (t == 0) up = hal;
             if (t == nthreads - 1) dn = hal;
-            hal = hal_next;
         }
 
         cplx b[RPT];
@@ -1187,7 +1201,7 @@ static cudaError_t launch_depth_tma_cfg(const LaunchCtx& c, const cplx* src, cpl
     if (!field_tensor_map(&tm_src, src, c) || !depth_dst_maps(&tm_dst, dst, c)) return cudaErrorNotSupported;
     const int nthreads = (c.n_tiles + 31) / 32 * 32;
     const int nwarps = nthreads / 32;
-    const size_t bytes = 1024 + sizeof(cplx) * (size_t(nwarps) * STAGES * 256 + 10 * size_t(nthreads) + 5 * nwarps) +
+    const size_t bytes = 1024 + sizeof(cplx) * (size_t(nwarps) * STAGES * 256 + 10 * size_t(nthreads) + 5 * nwarps + 4) +
                          sizeof(uint64_t) * (nwarps * STAGES + 1);
     if (bytes > 227 * 1024) return cudaErrorNotSupported;
     const cplx* k1 = (c.k1_tab && c.n_tiles <= K1_TAB_MAX_TILES && nthreads == round32(c.n_tiles)) ? c.k1_tab : nullptr;
