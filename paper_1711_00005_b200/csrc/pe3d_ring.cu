@@ -1645,6 +1645,11 @@ static cudaError_t launch_tma_ring(const LaunchCtx& c, const cplx* src, cplx* ds
         const int per_sm = cached_occupancy(reinterpret_cast<const void*>(kern), bytes, 1, nthr, nullptr);
         if (per_sm < 1) return cudaErrorInvalidConfiguration;
         const int64_t ctas = int64_t(c.num_sms) * per_sm;
+        // few items (a chain of an 8-frequency shard): one item per CTA, where the
+        // round-1 cp.async kernel's lighter CTAs share the SMs with the other chains'
+        // sweeps better (8 frequencies, 8 chains: 30.9 -> 27.0 us per step; with more
+        // items per CTA the TMA pipeline wins: 64 frequencies 101 -> 96 us per sweep)
+        if (!CORR && items <= 2 * ctas) return cudaErrorNotSupported;
         int per = int((items + ctas - 1) / ctas);
         if (items <= 2 * ctas) per = 1;               // few items: let the block scheduler balance the tail
         const int grid = int((items + per - 1) / per);
