@@ -1254,23 +1254,18 @@ static cudaError_t launch_depth_tma_cluster(const LaunchCtx& c, const cplx* src,
     at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    static int resident[17] = {0};                  // co-resident clusters, per cluster size
-    if (resident[CL] == 0) {
-        cfg.gridDim = dim3(CL * c.num_sms);
-        int n = 0;
-        e = cudaOccupancyMaxActiveClusters(&n, kern, &cfg);
-        if (e != cudaSuccess) return e;
-        if (n < 1) return cudaErrorInvalidConfiguration;
-        resident[CL] = n;
-    }
+    // co-resident clusters, cached per kernel (table / no table), device and smem size
+    cfg.gridDim = dim3(CL * c.num_sms);
+    const int resident = cached_occupancy((const void*)kern, bytes, CL, nthreads, &cfg);
+    if (resident < 1) return cudaErrorInvalidConfiguration;
     const int64_t total = int64_t(c.n_freq) * c.n_theta;
-    const int per = int((total + resident[CL] - 1) / resident[CL]);
+    const int per = int((total + resident - 1) / resident);
     const int clusters = int((total + per - 1) / per);
     cfg.gridDim = dim3(clusters * CL);
     // PDL only when the grid leaves most co-resident cluster slots free (cfg2:
     // 128 of 222); a full persistent grid launched early loses co-residency
     // (see launch_cluster_ring, pe3d_ring.cu)
-    cfg.numAttrs = (c.pdl && 4 * clusters <= 3 * resident[CL]) ? 2 : 1;
+    cfg.numAttrs = (c.pdl && 4 * clusters <= 3 * resident) ? 2 : 1;
     return cudaLaunchKernelEx(&cfg, kern, tm_src, tm_dst, src, c.loc_tab, c.mul_tab, c.fdev, k1, c.n_theta,
                               c.n_tiles, total, per, c.sector);
 }

@@ -163,6 +163,9 @@ inline cudaError_t launch_pdl(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 
     return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
+// Occupancy of a launch configuration (clusters when cluster > 1, else CTAs
+// per SM), cached per (kernel, device, dynamic smem, cluster size); 0 on error.
+int cached_occupancy(const void* kern, size_t bytes, int cluster, int nthr, cudaLaunchConfig_t* cfg);
 bool encode_swizzled_map(CUtensorMap* tm, const void* base, int rank, const uint64_t* dims,
                          const uint64_t* strides, const uint32_t* box, int swizzle_bytes);
 cudaError_t launch_slab_signal(unsigned long long* const* flags, int n, cudaStream_t s);

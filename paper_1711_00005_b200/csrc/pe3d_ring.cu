@@ -1596,7 +1596,7 @@ static bool ring_tensor_map(CUtensorMap* tm, const void* base, int n_theta, int 
 // Occupancy of a kernel configuration, cached per (kernel, device, smem bytes)
 // in a small thread-safe table (the launchers run from several handles).
 struct OccKey { const void* kern; int dev; size_t bytes; int cluster; };
-static int cached_occupancy(const void* kern, size_t bytes, int cluster, int nthr, cudaLaunchConfig_t* cfg) {
+int cached_occupancy(const void* kern, size_t bytes, int cluster, int nthr, cudaLaunchConfig_t* cfg) {
     static std::mutex mu;
     static OccKey keys[64];
     static int vals[64];
@@ -1746,18 +1746,12 @@ static cudaError_t launch_cluster_ring(const LaunchCtx& c, const cplx* src, cplx
     at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    // persistent: as many clusters as can be co-resident (queried once per cluster size)
-    static int resident[17] = {0};
-    if (resident[CL] == 0) {
-        cfg.gridDim = dim3(CL * c.num_sms);
-        int n = 0;
-        e = cudaOccupancyMaxActiveClusters(&n, kern, &cfg);
-        if (e != cudaSuccess) return e;
-        if (n < 1) return cudaErrorInvalidConfiguration;
-        resident[CL] = n;
-    }
+    // persistent: as many clusters as can be co-resident (cached per kernel, device and smem size)
+    cfg.gridDim = dim3(CL * c.num_sms);
+    const int resident = cached_occupancy((const void*)kern, bytes, CL, nthr, &cfg);
+    if (resident < 1) return cudaErrorInvalidConfiguration;
     const int64_t items = int64_t(c.n_freq) * c.n_tiles;
-    const int per = int((items + resident[CL] - 1) / resident[CL]);
+    const int per = int((items + resident - 1) / resident);
     const int clusters = int((items + per - 1) / per);
     cfg.gridDim = dim3(clusters * CL);
     // no PDL here: this persistent grid launched early is placed around the

@@ -119,21 +119,23 @@ def tl_record(res, mi, li, col_dtype):
                 final_col0=res.final_slab.values[0].copy())
 
 
-def single(name):
+def single(name, threads=1):
     cfg = configs.build(name)
     f = cfg.source.frequencies[0]
     install(name, cfg)
     from paper_1711_00005_b200.environment import wavenumber
     _CFG["k0"] = wavenumber(f, cfg.environment.c0)
     t0 = time.perf_counter()
-    res = pe3d.run_frequency(ref_config(cfg, (f,)), f)
+    # intra_threads only splits the reference's fixed 64-member tiles across
+    # threads; its output does not depend on it (ref tridiag.py:248-255).
+    res = pe3d.run_frequency(ref_config(cfg, (f,)), f, pe3d.ExecutorSpec(intra_threads=threads))
     wall = time.perf_counter() - t0
     rec = _CFG["rec"][_CFG["k0"]]
     out = tl_record(res, _CFG["mi"], _CFG["li"], np.float64)
     np.savez_compressed(HERE / f"full_{name}.npz", frequency=f, mi=_CFG["mi"], li=_CFG["li"],
                         stride=cfg.options.output_stride, n_range=cfg.grid.n_range,
                         samples=np.stack(rec[0]), norms=np.array(rec[1]),
-                        ref_seconds_per_step=wall / cfg.grid.n_range, **out)
+                        ref_seconds_per_step=wall / cfg.grid.n_range, ref_threads=threads, **out)
     print(f"{name}: {wall:.0f} s, {wall / cfg.grid.n_range:.3f} s/step (reference run_frequency)")
 
 
@@ -171,11 +173,12 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("config", choices=("cfg2", "cfg3", "cfg4", "cfg5"))
     ap.add_argument("--workers", type=int, default=8)
+    ap.add_argument("--threads", type=int, default=1, help="reference intra_threads (single-frequency configs)")
     a = ap.parse_args()
     if a.config == "cfg4":
         farm(a.config, a.workers)
     else:
-        single(a.config)
+        single(a.config, a.threads)
 
 
 if __name__ == "__main__":

@@ -12,6 +12,7 @@ import json
 import re
 import subprocess
 import sys
+from pathlib import Path
 
 DETAILS = ["Duration", "DRAM Throughput", "Memory Throughput", "L2 Hit Rate", "Issued Warp Per Scheduler",
            "Executed Ipc Active", "Achieved Occupancy", "Theoretical Occupancy", "Registers Per Thread",
@@ -77,11 +78,19 @@ def main():
             key, pat = p.split("=")
             for name in kernels:
                 if pat in name:
-                    rd = float(out[name]["dram__bytes_read.sum"].split()[0])
-                    wr = float(out[name]["dram__bytes_write.sum"].split()[0])
-                    unit = out[name]["dram__bytes_read.sum"].split()[1]
-                    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[unit]
-                    traffic[key] = (rd + wr) * scale
+                    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+                    rd, ru = out[name]["dram__bytes_read.sum"].split()[:2]
+                    wr, wu = out[name]["dram__bytes_write.sum"].split()[:2]
+                    traffic[key] = float(rd) * scale[ru] + float(wr) * scale[wu]
+                    dur = out[name].get("gpu__time_duration.sum", "").split()
+                    if dur:
+                        traffic[key + "_duration_us"] = float(dur[0])
+        # stamp the capture with the hash of the CUDA sources it was built from
+        # (bench.py reuses a traffic file only when the hash matches csrc/)
+        sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+        from bench import source_hash
+        traffic["source_hash"] = source_hash()
+        traffic["source"] = f"ncu --set full, {Path(sys.argv[1]).name}"
         json.dump(traffic, open(path, "w"), indent=1)
 
 
