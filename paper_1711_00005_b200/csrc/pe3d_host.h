@@ -41,6 +41,27 @@ struct DevBuf {
     template <class T> T* as() const { return static_cast<T*>(ptr); }
 };
 
+// Page-locked host staging (the march's parameter uploads are memcpy nodes of
+// its graph, so their source must stay valid and in place).
+struct PinBuf {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+    cudaError_t ensure(size_t want) {
+        if (want <= bytes) return cudaSuccess;
+        if (ptr) cudaFreeHost(ptr);
+        ptr = nullptr;
+        bytes = 0;
+        cudaError_t e = cudaHostAlloc(&ptr, want, cudaHostAllocDefault);
+        if (e == cudaSuccess) bytes = want;
+        return e;
+    }
+    void release() {
+        if (ptr) cudaFreeHost(ptr);
+        ptr = nullptr;
+        bytes = 0;
+    }
+};
+
 struct Handle {
     int device = 0;
     int num_sms = 148;
@@ -89,6 +110,11 @@ struct Handle {
     // plus one for the starting sample, and their events
     cudaStream_t tl_side[MAX_CHAINS + 1] = {};
     std::vector<cudaEvent_t> tl_ev;
+    // whole-march graph (pe3d_march_device): parameter staging, and the side
+    // branch that builds the factorisation and ring tables during the prologue
+    PinBuf params_pin;
+    cudaStream_t pro_side = nullptr;
+    cudaEvent_t pro_fork = nullptr, pro_join = nullptr;
 };
 
 // Launch wrapper: in profile mode, bracket each launch with events.

@@ -1504,6 +1504,66 @@ k_prepare(const cplx* __restrict__ u0, cplx* __restrict__ dst, const FreqDev* __
     if (tid == 0 && szeros) atomicAdd(reinterpret_cast<unsigned long long*>(ea.clamped + f), szeros);
 }
 
+// March prologue for an azimuth-independent starter on a periodic ring
+// (PE3D_FLAG_STARTER_COLUMN, the Gaussian starter of every drop-in march):
+// u0 is one depth column per frequency, so the boundary, the TL sample and
+// the first temp = [1 + cy_rhs Y] u are the same for every azimuth.  A CTA
+// computes PREPC_ROWS rows of one frequency once (k_prepare's arithmetic with
+// u_(m-1) = u_m = u_(m+1)) and streams them out: the temp as whole tiles
+// (n_theta contiguous 128-B lines per tile), TL / snapshot / final as
+// depth runs of every azimuth.  The prologue is pure write bandwidth
+// (cfg4: 134 MB TL + 268 MB temp); k_prepare staged 34 x 64 input points
+// per 32 x 64 outputs and ran at ~2 TB/s (199 us of the march at cfg4).
+constexpr int PREPC_ROWS = 64;
+__global__ void __launch_bounds__(256)
+k_prepare_column(const cplx* __restrict__ u0, cplx* __restrict__ dst, const FreqDev* __restrict__ fdev, int n_theta,
+                 int n_tiles, int n_depth, double r, double delta_theta, EpilogueArgs ea) {
+    __shared__ cplx su[PREPC_ROWS], st[PREPC_ROWS];
+    __shared__ double stl[PREPC_ROWS];
+    __shared__ unsigned long long szeros;
+    const int f = blockIdx.y, l0 = blockIdx.x * PREPC_ROWS, tid = threadIdx.x;
+    const int rows = min(PREPC_ROWS, n_tiles * 8 - l0);            // rows of this block inside the tiles
+    if (tid == 0) szeros = 0;
+    const FreqDev fd = fdev[f];
+    const double s = azimuth_scale(fd.k0, r, delta_theta);
+    const cplx b2 = crmul(s, fd.cy_rhs);                           // scale 1: b2 = alpha, b1 = 1 - 2 alpha
+    const cplx b1 = csub(cone(), cadd(b2, b2));
+    if (tid < PREPC_ROWS) {
+        const int l = l0 + tid;
+        const bool ok = tid < rows && l < n_depth && l + ea.row_offset != 0;
+        const cplx u = ok ? ldc(u0 + int64_t(f) * n_depth + l) : czero();
+        su[tid] = u;
+        st[tid] = cfma(b1, u, cmul(b2, cadd(u, u)));               // periodic: both neighbours are u
+        if (ea.tl && l < n_depth) {
+            const double mag = cabs(u) * ea.w_abs[f];
+            if (mag == 0.0) atomicAdd(&szeros, (unsigned long long)n_theta);
+            stl[tid] = (mag == 0.0) ? TL_FLOOR_DB : -20.0 * log10(mag);
+        }
+    }
+    __syncthreads();
+    // first temp: tiles [l0/8, l0/8 + rows/8), each n_theta lines of 8 rows
+    if (ea.write_temp) {
+        cplx* base = dst + ring_base(f, 0, n_tiles, n_theta, n_theta) + int64_t(l0 / 8) * n_theta * 8;
+        const int line_elems = n_theta * 8, n = (rows / 8) * line_elems;   // <= 2^18: 32-bit indices
+        for (int e = tid; e < n; e += blockDim.x) stc_stream(base + e, st[(e / line_elems) * 8 + (e & 7)]);
+    }
+    // TL / snapshot / final in the reference layout [.][m][l]: depth runs of every azimuth
+    const int dr = min(rows, n_depth - l0);
+    if (dr > 0 && (ea.tl || ea.snap || ea.final_out)) {
+        const int n = n_theta * dr;
+        const int64_t so = (int64_t(f) * ea.n_samples + ea.sample) * n_theta * n_depth + l0;
+        for (int e = tid; e < n; e += blockDim.x) {
+            const int m = e / dr, dl = e - m * dr;
+            const int64_t off = int64_t(m) * n_depth + dl;
+            if (ea.tl) ea.tl[so + off] = stl[dl];
+            if (ea.snap) stc(ea.snap + so + off, su[dl]);
+            if (ea.final_out) stc(ea.final_out + int64_t(f) * n_theta * n_depth + l0 + off, su[dl]);
+        }
+    }
+    __syncthreads();
+    if (tid == 0 && szeros) atomicAdd(reinterpret_cast<unsigned long long*>(ea.clamped + f), szeros);
+}
+
 // ------------------------------------------------------------ launchers
 
 static int round32(int x) { return (x + 31) / 32 * 32; }
@@ -1872,6 +1932,12 @@ cudaError_t launch_azimuth_scan(const LaunchCtx& c, const cplx* src, cplx* dst, 
 cudaError_t launch_finish(const LaunchCtx& c, const cplx* src, int src_tiled, cplx* dst, double r,
                           const EpilogueArgs& ea) {
     const bool standard = ea.chunk_gap == 0 && (ea.chunk_cols == 0 || ea.chunk_cols == c.n_theta) && !ea.peer[0];
+    if (!src_tiled && standard && ea.src_column && ea.periodic && !getenv("PE3D_PREPARE_STAGED")) {
+        dim3 grid((c.n_tiles * 8 + PREPC_ROWS - 1) / PREPC_ROWS, c.n_freq);
+        k_prepare_column<<<grid, 256, 0, c.stream>>>(src, dst, c.fdev, c.n_theta, c.n_tiles, c.n_depth, r,
+                                                     c.delta_theta, ea);
+        return cudaGetLastError();
+    }
     if (!src_tiled && standard && c.n_theta % PREP_MB == 0) {
         dim3 grid(c.n_theta / PREP_MB, (c.n_tiles * 8 + PREP_DB - 1) / PREP_DB, c.n_freq);
         k_prepare<<<grid, 256, 0, c.stream>>>(src, dst, c.fdev, c.n_theta, c.n_tiles, c.n_depth, r, c.delta_theta, ea);
