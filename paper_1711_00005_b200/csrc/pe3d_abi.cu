@@ -583,6 +583,7 @@ static int march_device_impl(void* handle, const pe3d_grid* g, const pe3d_coeffs
             e = cudaGraphInstantiate(&h->graph_exec, graph, 0);
             cudaGraphDestroy(graph);
             if (e != cudaSuccess) { h->graph_exec = nullptr; return cuda_fail(err, e, "instantiate"); }
+            CK(cudaGraphUpload(h->graph_exec, stream), "graph upload");      // device-side setup off the first launch
             h->graph_key = key;
         }
         CK(cudaGraphLaunch(h->graph_exec, stream), "graph launch");

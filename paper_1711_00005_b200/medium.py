@@ -193,9 +193,44 @@ class LayeredMedium:
             n2 = n2 + (d2 / (2.0 * rho) - 0.75 * (d1 / rho) ** 2) / (k0 * k0)
         return n2
 
+    def _column_parts(self, grid: Grid3D):
+        """Range-independent media: the k0-independent n^2 column and the
+        density term's numerator, computed once per depth grid (a batch of
+        frequencies shares them; index_squared's arithmetic, term by term)."""
+        key = (grid.n_depth, grid.delta_z)
+        cache = self.__dict__.setdefault("_parts_cache", {})
+        parts = cache.get(key)
+        if parts is None:
+            z = grid.depths()[None, :]
+            c_w = self.water.speed_at(grid.depths())[None, :]
+            n2_w = ((self.c0 / c_w) * (1.0 + 1j * ETA * self.water_alpha)) ** 2
+            b = self.bottom
+            n2_b = ((self.c0 / b.speed) * (1.0 + 1j * ETA * b.alpha)) ** 2
+            h = b.bathymetry.depth(0.0, np.zeros((1, 1)))
+            w = self.interface_width
+            t = np.tanh((z - h) / w)
+            step = 0.5 * (1.0 + t)
+            n2 = (1.0 - step) * n2_w + step * n2_b
+            n2 = n2 * (1.0 + 1j * ETA * self._sponge_alpha(grid)[None, :]) ** 2
+            dens = None
+            if self.has_density_contrast:
+                jump = b.density - self.water_density
+                sech2 = 1.0 - t * t
+                rho = self.water_density + jump * step
+                d1 = jump * sech2 / (2.0 * w)
+                d2 = -jump * sech2 * t / (w * w)
+                dens = d2 / (2.0 * rho) - 0.75 * (d1 / rho) ** 2
+            parts = cache[key] = (n2, dens)
+        return parts
+
     def index_grid(self, grid: Grid3D, r: float, k0: Optional[float]) -> np.ndarray:
         """Complex n (principal square root of n_eff^2), (n_azimuth, n_depth)."""
         if self.range_independent:
-            column = np.sqrt(self.index_squared(grid, r, [0.0], k0)[0])
+            if self.has_density_contrast and k0 is None:
+                raise DomainError("a medium with a density contrast needs k0")
+            n2, dens = self._column_parts(grid)
+            if dens is not None:
+                n2 = n2 + dens / (k0 * k0)
+            column = np.sqrt(n2[0])
             return np.broadcast_to(column, (grid.n_azimuth, grid.n_depth))
         return np.sqrt(self.index_squared(grid, r, grid.azimuths(), k0))
