@@ -28,7 +28,7 @@ roofline = both sweeps, 32 algorithmic bytes per grid point per launch
            K steps (first and last two launches of each sweep excluded; no TL,
            no final slab), against MEASURED_PEAKS.json hbm_gbs; `kernel` is the
            slower sweep.  `traffic` = ncu DRAM bytes per launch from
-           profiles/traffic_<workload>.json when its source hash matches csrc/.
+           profiles/traffic_<workload>.json when its hash of the sweep kernels' sources matches.
 cpu_baseline / --impl reference = the UNMODIFIED reference (baseline/_ref,
            the pip install of /root/reference) through its own frequency_farm
            on the host cores, bounded sample (oracle/ref_harness.py injects the
@@ -97,13 +97,17 @@ def peaks():
     return 6650.0, "fallback"
 
 
+SWEEP_SOURCES = ("pe3d_depth.cu", "pe3d_ring.cu", "pe3d_device.cuh", "pe3d_internal.h")
+
+
 def source_hash():
-    """Hash of the CUDA sources the library is built from (stamps traffic files)."""
+    """Hash of the sweep kernels' CUDA sources (stamps traffic files: a DRAM
+    traffic capture stays valid while the kernels it measured are unchanged)."""
     h = hashlib.sha256()
     csrc = ROOT / "paper_1711_00005_b200" / "csrc"
-    for p in sorted(csrc.glob("*.cu")) + sorted(csrc.glob("*.h")) + sorted(csrc.glob("*.cuh")):
-        h.update(p.name.encode())
-        h.update(p.read_bytes())
+    for name in SWEEP_SOURCES:
+        h.update(name.encode())
+        h.update((csrc / name).read_bytes())
     return h.hexdigest()[:16]
 
 
