@@ -39,6 +39,10 @@ def main():
         cnt[short] += 1
         if cnt[short] <= 3 or "prepare" in short or "factor" in short or "setup" in short:
             print(f"  +{e.time_range.start - t0:9.1f} us  {d:8.1f} us  {short}")
+    print("  ... last kernels:")
+    for e in evs[-5:]:
+        print(f"  +{e.time_range.start - t0:9.1f} us  {e.time_range.end - e.time_range.start:8.1f} us  "
+              f"{e.name.split('(')[0][:70]}")
     print(f"  last kernel ends at +{max(e.time_range.end for e in evs) - t0:.1f} us")
     for k, v in sorted(tot.items(), key=lambda kv: -kv[1]):
         print(f"  {v:9.1f} us  {cnt[k]:4d} x  {k}")
