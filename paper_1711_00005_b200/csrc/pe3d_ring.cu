@@ -1022,7 +1022,8 @@ __global__ void __launch_bounds__(ring_tma_threads<RT>(), MINB)
 k_azimuth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ CUtensorMap tm_dst,
               const cplx* __restrict__ table, int E, int tab_elems, int n_theta, int n_tiles, int n_depth,
               int64_t total_items, int n_units, EpilogueArgs ea, const cplx* __restrict__ sp_cd,
-              const cplx* __restrict__ sp_aq, const cplx* __restrict__ sp_pa, int split, int tile_perm) {
+              const cplx* __restrict__ sp_aq, const cplx* __restrict__ sp_pa, int split, int tile_perm,
+              const __grid_constant__ CUtensorMap tm_fin, int fin_tma) {
     namespace cg = cooperative_groups;
     constexpr int NW = 8 / RT;                      // consumer warps; warp NW is the TMA producer
     constexpr int NS = 32 * L;                      // segment length
@@ -1119,7 +1120,12 @@ k_azimuth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant_
             for (int n = 0; n < N; ++n) {
                 const int slot = n % S;
                 mbar_wait(&empty[slot], unsigned(n / S) & 1u);      // consumers wrote the temp (or are done)
-                if (ea.write_temp) {
+                if (fin_tma) {
+                    // last step: the slot holds the final slab's tile (reference layout via tm_fin)
+                    const int item = first + n * G, f = item / n_tiles;
+                    tma_store_5d(&tm_fin, 0, 0, 0, (item - f * n_tiles) * tile_perm % n_tiles, f, stage + slot * ITEM);
+                    bulk_commit();
+                } else if (ea.write_temp) {
                     const int item = first + n * G, f = item / n_tiles;
                     tma_store_5d(&tm_dst, 0, 0, 0, s, f * n_tiles + (item - f * n_tiles) * tile_perm % n_tiles,
                                  stage + slot * ITEM);
@@ -1312,6 +1318,7 @@ k_azimuth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant_
                     for (int k = 0; k < L; ++k) {
                         const int m = mseg + m0 + k;
                         const cplx uf = cmul(scale, v[h][k]);
+                        if (fin_tma) stg[tma_slot(q, k, warp * RT + h)] = uf;     // stored by the producer's TMA
                         const int64_t so = (int64_t(f) * ea.n_samples + ea.sample) * n_theta * n_depth +
                                            (int64_t(m) * n_depth + l);
                         if (ea.tl) {
@@ -1320,7 +1327,7 @@ k_azimuth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant_
                             ea.tl[so] = (mag == 0.0) ? TL_FLOOR_DB : -20.0 * log10(mag);
                         }
                         if (ea.snap) stc(ea.snap + so, uf);
-                        if (ea.final_out) stc(ea.final_out + (int64_t(f) * n_theta + m) * n_depth + l, uf);
+                        if (ea.final_out && !fin_tma) stc(ea.final_out + (int64_t(f) * n_theta + m) * n_depth + l, uf);
                     }
                     if (ea.tl && zeros)
                         atomicAdd(reinterpret_cast<unsigned long long*>(ea.clamped + f), (unsigned long long)zeros);
@@ -1713,9 +1720,22 @@ static cudaError_t launch_tma_ring(const LaunchCtx& c, const cplx* src, cplx* ds
         int per = int((items + ctas - 1) / ctas);
         if (items <= 2 * ctas) per = 1;               // few items: let the block scheduler balance the tail
         const int grid = int((items + per - 1) / per);
+        // last step: the final slab leaves through the stage with one TMA store per item
+        // (reference layout [f][m][l]: an item's 8 rows of azimuth m are one 128-B run)
+        // instead of 16-B stores strided by n_depth (cfg4 last azimuth sweep 166-189 -> 97-99 us,
+        // 20-step march 3945 -> 3841 us; bitwise the same slab)
+        CUtensorMap tm_fin = tm_dst;
+        int fin_tma = 0;
+        if (ea.final_out && !ea.write_temp && c.n_depth % 8 == 0 && !getenv("PE3D_FINAL_STORES")) {
+            const uint64_t NZb = uint64_t(c.n_depth) * 16;
+            const uint64_t dims[5] = {16, 32, uint64_t(L), uint64_t(c.n_tiles), uint64_t(c.n_freq)};
+            const uint64_t strides[4] = {uint64_t(L) * NZb, NZb, 128, uint64_t(c.n_theta) * NZb};
+            const uint32_t box[5] = {16, 32, uint32_t(L), 1, 1};
+            fin_tma = encode_swizzled_map(&tm_fin, ea.final_out, 5, dims, strides, box, 128) ? 1 : 0;
+        }
         return launch_pdl(c.pdl != 0, kern, dim3(grid), dim3(nthr), bytes, c.stream, tm_src, tm_dst, table_step, E,
                           tab_elems, c.n_theta, c.n_tiles, c.n_depth, items, grid, ea, (const cplx*)c.sp_cd,
-                          (const cplx*)c.sp_aq, (const cplx*)c.sp_pa, c.split, 1);
+                          (const cplx*)c.sp_aq, (const cplx*)c.sp_pa, c.split, 1, tm_fin, fin_tma);
     } else {
         if (CL > 8) {
             e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -1749,7 +1769,7 @@ static cudaError_t launch_tma_ring(const LaunchCtx& c, const cplx* src, cplx* ds
         }
         return cudaLaunchKernelEx(&cfg, kern, tm_src, tm_dst, table_step, E, tab_elems, c.n_theta, c.n_tiles,
                                   c.n_depth, items, per, ea, (const cplx*)c.sp_cd, (const cplx*)c.sp_aq,
-                                  (const cplx*)c.sp_pa, c.split, perm);
+                                  (const cplx*)c.sp_pa, c.split, perm, tm_dst, 0);
     }
 }
 
