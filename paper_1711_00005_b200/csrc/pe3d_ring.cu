@@ -1120,7 +1120,7 @@ k_azimuth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant_
             for (int n = 0; n < N; ++n) {
                 const int slot = n % S;
                 mbar_wait(&empty[slot], unsigned(n / S) & 1u);      // consumers wrote the temp (or are done)
-                if (fin_tma) {
+                if (!CLUSTER && fin_tma) {
                     // last step: the slot holds the final slab's tile (reference layout via tm_fin)
                     const int item = first + n * G, f = item / n_tiles;
                     tma_store_5d(&tm_fin, 0, 0, 0, (item - f * n_tiles) * tile_perm % n_tiles, f, stage + slot * ITEM);
@@ -1318,7 +1318,7 @@ k_azimuth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant_
                     for (int k = 0; k < L; ++k) {
                         const int m = mseg + m0 + k;
                         const cplx uf = cmul(scale, v[h][k]);
-                        if (fin_tma) stg[tma_slot(q, k, warp * RT + h)] = uf;     // stored by the producer's TMA
+                        if (!CLUSTER && fin_tma) stg[tma_slot(q, k, warp * RT + h)] = uf;   // stored by the producer's TMA
                         const int64_t so = (int64_t(f) * ea.n_samples + ea.sample) * n_theta * n_depth +
                                            (int64_t(m) * n_depth + l);
                         if (ea.tl) {
@@ -1327,7 +1327,7 @@ k_azimuth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant_
                             ea.tl[so] = (mag == 0.0) ? TL_FLOOR_DB : -20.0 * log10(mag);
                         }
                         if (ea.snap) stc(ea.snap + so, uf);
-                        if (ea.final_out && !fin_tma) stc(ea.final_out + (int64_t(f) * n_theta + m) * n_depth + l, uf);
+                        if (ea.final_out && (CLUSTER || !fin_tma)) stc(ea.final_out + (int64_t(f) * n_theta + m) * n_depth + l, uf);
                     }
                     if (ea.tl && zeros)
                         atomicAdd(reinterpret_cast<unsigned long long*>(ea.clamped + f), (unsigned long long)zeros);
