@@ -362,6 +362,7 @@ int pe3d_handle_destroy(void* handle) {
     cudaSetDevice(h->device);
     for (DevBuf* b : h->buffers()) b->release();
     if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
+    if (h->pre_exec) cudaGraphExecDestroy(h->pre_exec);
     for (int k = 0; k <= Handle::MAX_CHAINS; ++k)
         if (h->tl_side[k]) cudaStreamDestroy(h->tl_side[k]);
     for (cudaEvent_t e : h->tl_ev) cudaEventDestroy(e);
@@ -472,13 +473,18 @@ static int march_device_impl(void* handle, const pe3d_grid* g, const pe3d_coeffs
     const cplx* local = reinterpret_cast<const cplx*>(d_local);
     Prof prof{h, (g->flags & PE3D_FLAG_PROFILE) != 0, stream, {}};
     // setup: the depth factorisation (+ per-march sweep tables) and the ring tables
+    auto enqueue_depth_setup = [&](pe3d::LaunchCtx& cs) -> cudaError_t {
+        return p.serial ? cudaSuccess
+                        : prof.run(2, [&] { return pe3d::launch_factor_depth(cs, local, NZ, g->first_index + 1); });
+    };
+    auto enqueue_ring_setup = [&](pe3d::LaunchCtx& cs) -> cudaError_t {
+        return !ring_tables ? cudaSuccess
+                            : prof.run(2, [&] { return pe3d::launch_ring_setup(cs, h->ring_tab.as<cplx>(), g->n_steps,
+                                                                               g->first_index, g->r_start, g->delta_r); });
+    };
     auto enqueue_setup = [&](pe3d::LaunchCtx& cs) -> cudaError_t {
-        cudaError_t e = cudaSuccess;
-        if (!p.serial) e = prof.run(2, [&] { return pe3d::launch_factor_depth(cs, local, NZ, g->first_index + 1); });
-        if (e == cudaSuccess && ring_tables)
-            e = prof.run(2, [&] { return pe3d::launch_ring_setup(cs, h->ring_tab.as<cplx>(), g->n_steps,
-                                                                 g->first_index, g->r_start, g->delta_r); });
-        return e;
+        cudaError_t e = enqueue_depth_setup(cs);
+        return e == cudaSuccess ? enqueue_ring_setup(cs) : e;
     };
     // starter: boundary, TL sample 0, first temp (ref marching.py:159-172)
     pe3d::EpilogueArgs ea0{};
@@ -542,55 +548,84 @@ static int march_device_impl(void* handle, const pe3d_grid* g, const pe3d_coeffs
         // the A/B switches pick kernels and launch attributes baked into the graph
         for (const char* name : {"PE3D_NO_PDL", "PE3D_CLUSTER_L", "PE3D_DEPTH_NO_CLUSTER", "PE3D_RING_BLOCK",
                                  "PE3D_RING_CPASYNC", "PE3D_DEPTH_NO_SPLIT", "PE3D_FACTOR_SERIAL",
-                                 "PE3D_PREPARE_STAGED"}) {
+                                 "PE3D_PREPARE_STAGED", "PE3D_PARAMS_MEMCPY"}) {
             const char* v = getenv(name);
             const std::string val = v ? std::string("=") + v : std::string("-");
             add(val.data(), val.size() + 1);
         }
         const TlSink none{nullptr, 0, 0};
         add(sink ? sink : &none, sizeof(TlSink));
-        if (!(h->graph_exec && key == h->graph_key)) {
+        if (!(h->graph_exec && h->pre_exec && key == h->graph_key)) {
             if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
+            if (h->pre_exec) cudaGraphExecDestroy(h->pre_exec);
             h->graph_exec = nullptr;
+            h->pre_exec = nullptr;
             h->graph_key.clear();
-            cudaGraph_t graph = nullptr;
+            auto capture = [&](cudaGraphExec_t* out, auto&& body) -> cudaError_t {
+                cudaGraph_t graph = nullptr;
+                cudaError_t e = cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal);
+                if (e != cudaSuccess) return e;
+                e = body();
+                const cudaError_t e2 = cudaStreamEndCapture(stream, &graph);
+                if (e == cudaSuccess) e = e2;
+                if (e == cudaSuccess) e = cudaGraphInstantiate(out, graph, 0);
+                if (graph) cudaGraphDestroy(graph);
+                if (e == cudaSuccess) e = cudaGraphUpload(*out, stream);    // device-side setup off the first launch
+                return e;
+            };
             const int64_t before = prof.launches;
-            CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal), "capture");
-            cudaError_t e = cudaMemcpyAsync(h->fdev.ptr, pin, fd_b, cudaMemcpyHostToDevice, stream);
-            if (e == cudaSuccess) e = cudaMemcpyAsync(h->w_abs.ptr, pin + w_o, w_b, cudaMemcpyHostToDevice, stream);
-            if (e == cudaSuccess) e = cudaMemcpyAsync(h->err.ptr, pin + e_o, sizeof(de0), cudaMemcpyHostToDevice, stream);
-            if (e == cudaSuccess && d_clamped) e = cudaMemsetAsync(d_clamped, 0, F * sizeof(int64_t), stream);
-            // fork: setup kernels on the side branch, prologue on the main one, join before the steps
-            if (e == cudaSuccess) e = cudaEventRecord(h->pro_fork, stream);
-            if (e == cudaSuccess) e = cudaStreamWaitEvent(h->pro_side, h->pro_fork, 0);
-            if (e == cudaSuccess) {
-                // The graph submits the side branch only after the main branch's nodes (the
-                // step loop included), so the branch captured second starts late (+110 us at
-                // 20 steps, +390 us at 100; tools/timeline.py): the prologue, the longer
-                // kernel, is captured first on the main branch.  (All of it in stream order
-                // instead: 20-step march 3920 -> 3980 us.)
-                const cudaError_t ep = enqueue_prologue();
+            // Two graphs.  The prologue graph: the parameter uploads, then the prologue on
+            // the main branch and the setup kernels on a side branch.  A graph submits a
+            // second branch only after the main branch's nodes, so with the step loop in the
+            // same graph the setup branch started after the whole loop had been submitted
+            // (+110 us at 64 frequencies x 20 steps, +390 us at 100 steps, +350 us at 8
+            // frequencies x 20 steps on 8 chains; tools/timeline.py).
+            cudaError_t e = capture(&h->pre_exec, [&]() -> cudaError_t {
+                // the parameters travel by value in one small kernel node (they are part of the
+                // graph key); larger ones as copies from the page-locked staging
+                const void* srcs[3] = {fd.data(), wabs.data(), &de0};
+                const int sizes[3] = {int(fd_b), int(w_b), int(sizeof(de0))};
+                void* dsts[3] = {h->fdev.ptr, h->w_abs.ptr, h->err.ptr};
+                cudaError_t e = getenv("PE3D_PARAMS_MEMCPY")
+                                    ? cudaErrorNotSupported
+                                    : pe3d::launch_params(3, srcs, sizes, dsts, d_clamped, d_clamped ? F : 0, stream);
+                if (e == cudaErrorNotSupported) {
+                    e = cudaMemcpyAsync(h->fdev.ptr, pin, fd_b, cudaMemcpyHostToDevice, stream);
+                    if (e == cudaSuccess) e = cudaMemcpyAsync(h->w_abs.ptr, pin + w_o, w_b, cudaMemcpyHostToDevice, stream);
+                    if (e == cudaSuccess) e = cudaMemcpyAsync(h->err.ptr, pin + e_o, sizeof(de0), cudaMemcpyHostToDevice, stream);
+                    if (e == cudaSuccess && d_clamped) e = cudaMemsetAsync(d_clamped, 0, F * sizeof(int64_t), stream);
+                }
+                if (e == cudaSuccess) e = cudaEventRecord(h->pro_fork, stream);
+                if (e == cudaSuccess) e = cudaStreamWaitEvent(h->pro_side, h->pro_fork, 0);
+                if (e != cudaSuccess) return e;
+                // main: prologue, then the ring tables; side: the depth factorisation and the
+                // sweep tables (8 frequencies: setup branch 35 -> 22 us)
+                cudaError_t ep = enqueue_prologue();
+                if (ep == cudaSuccess) ep = enqueue_ring_setup(c);
                 pe3d::LaunchCtx cs = c;
                 cs.stream = h->pro_side;
-                const cudaError_t es = ep == cudaSuccess ? enqueue_setup(cs) : cudaSuccess;
+                const cudaError_t es = ep == cudaSuccess ? enqueue_depth_setup(cs) : cudaSuccess;
                 cudaError_t ej = cudaEventRecord(h->pro_join, h->pro_side);     // always joined: capture ends cleanly
                 if (ej == cudaSuccess) ej = cudaStreamWaitEvent(stream, h->pro_join, 0);
-                e = ep != cudaSuccess ? ep : (es != cudaSuccess ? es : ej);
-            }
+                return ep != cudaSuccess ? ep : (es != cudaSuccess ? es : ej);
+            });
             if (e == cudaSuccess)
-                e = enqueue_steps(h, g, p, local, d_tl, reinterpret_cast<cplx*>(d_snapshots),
-                                  reinterpret_cast<cplx*>(d_u_final), d_clamped, h->w_abs.as<double>(), prof, sink);
+                e = capture(&h->graph_exec, [&]() -> cudaError_t {
+                    return enqueue_steps(h, g, p, local, d_tl, reinterpret_cast<cplx*>(d_snapshots),
+                                         reinterpret_cast<cplx*>(d_u_final), d_clamped, h->w_abs.as<double>(), prof,
+                                         sink);
+                });
             h->graph_launches = prof.launches - before;
             prof.launches = before;
-            cudaError_t e2 = cudaStreamEndCapture(stream, &graph);
-            if (e != cudaSuccess) { if (graph) cudaGraphDestroy(graph); return cuda_fail(err, e, "enqueue"); }
-            if (e2 != cudaSuccess) return cuda_fail(err, e2, "end capture");
-            e = cudaGraphInstantiate(&h->graph_exec, graph, 0);
-            cudaGraphDestroy(graph);
-            if (e != cudaSuccess) { h->graph_exec = nullptr; return cuda_fail(err, e, "instantiate"); }
-            CK(cudaGraphUpload(h->graph_exec, stream), "graph upload");      // device-side setup off the first launch
+            if (e != cudaSuccess) {
+                if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
+                if (h->pre_exec) cudaGraphExecDestroy(h->pre_exec);
+                h->graph_exec = h->pre_exec = nullptr;
+                return cuda_fail(err, e, "march graph");
+            }
             h->graph_key = key;
         }
+        CK(cudaGraphLaunch(h->pre_exec, stream), "graph launch");
         CK(cudaGraphLaunch(h->graph_exec, stream), "graph launch");
         prof.launches += h->graph_launches;
     } else {
@@ -1023,7 +1058,8 @@ int pe3d_march_medium_host(void* handle, const pe3d_grid* g, const pe3d_coeffs* 
         add(&gen, sizeof(gen));
         if (!(h->graph_exec && key == h->graph_key)) {
             if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
-            h->graph_exec = nullptr;
+            if (h->pre_exec) cudaGraphExecDestroy(h->pre_exec);
+            h->graph_exec = h->pre_exec = nullptr;
             h->graph_key.clear();
             cudaGraph_t graph = nullptr;
             CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "capture");

@@ -96,6 +96,7 @@ struct Handle {
     // one cached step-loop graph (reused when a march repeats with identical arguments)
     std::vector<unsigned char> graph_key;
     cudaGraphExec_t graph_exec = nullptr;
+    cudaGraphExec_t pre_exec = nullptr;       // pe3d_march_device: the uploads, setup and prologue graph
     // PE3D_FLAG_PROFILE accounting
     double prof_ms[3] = {0, 0, 0};
     int32_t prof_n[3] = {0, 0, 0};

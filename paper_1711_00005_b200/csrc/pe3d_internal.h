@@ -201,6 +201,11 @@ cudaError_t launch_solve_batch(int n, int members, int cyclic, StridedC sub, Str
                                StridedC rhs, cplx* x, cplx* cp, cplx* inv, cplx* y, cplx* q, int* fail_row,
                                double* fail_mag, cudaStream_t stream);
 cudaError_t launch_zero(cplx* p, int64_t n, cudaStream_t stream);
+// copy up to 4 small host segments (<= 30 KB in total, carried in the kernel's
+// parameters) to their device destinations and zero n_zero int64 at `zero`;
+// cudaErrorNotSupported when they are too large
+cudaError_t launch_params(int n_seg, const void* const* src, const int* bytes, void* const* dst, int64_t* zero,
+                          int n_zero, cudaStream_t stream);
 cudaError_t launch_reduce_failures(const int* fail_row, const double* fail_mag, int n_freq, int members, int step,
                                    int sweep, int rank1_row, DevError* err, cudaStream_t stream);
 

@@ -10,6 +10,8 @@
 #include "pe3d_device.cuh"
 #include "pe3d_internal.h"
 
+#include <cstring>
+
 namespace pe3d {
 
 // ----------------------------------- thread-per-system kernels (reference order)
@@ -308,6 +310,63 @@ cudaError_t launch_reduce_failures(const int* fail_row, const double* fail_mag, 
 
 // Pad the host-given local term [F][n_depth] (any stride) into nothing: the
 // factorization kernel reads it directly.  Zero-fill helper for buffers.
+// March parameters carried by value in the kernel's parameter space (baked into
+// the march graph, which is rebuilt whenever they change): copies `bytes` of the
+// blob to `dst` and zeroes n_zero int64 (the clamped counters).  One kernel node
+// instead of H2D copies from page-locked staging plus a memset, whose copy-engine
+// to SM hand-off delayed the first kernel of the march by ~25 us.
+template <int CAP>
+struct ParamBlob {
+    unsigned char b[CAP];
+};
+struct ParamSegs {
+    unsigned char* dst[4];
+    int end[4];                 // prefix byte offsets of the segments in the blob (multiples of 4)
+    int n;
+};
+template <int CAP>
+__global__ void __launch_bounds__(256) k_params(const __grid_constant__ ParamBlob<CAP> blob, ParamSegs segs,
+                                               int64_t* __restrict__ zero, int n_zero) {
+    const uint32_t* s = reinterpret_cast<const uint32_t*>(blob.b);
+    int begin = 0;
+    for (int k = 0; k < segs.n; ++k) {
+        uint32_t* d = reinterpret_cast<uint32_t*>(segs.dst[k]);
+        for (int i = begin / 4 + int(threadIdx.x); i < segs.end[k] / 4; i += blockDim.x) d[i - begin / 4] = s[i];
+        begin = segs.end[k];
+    }
+    if (zero)
+        for (int i = threadIdx.x; i < n_zero; i += blockDim.x) zero[i] = 0;
+}
+
+cudaError_t launch_params(int n_seg, const void* const* src, const int* bytes, void* const* dst, int64_t* zero,
+                          int n_zero, cudaStream_t stream) {
+    if (n_seg < 0 || n_seg > 4) return cudaErrorInvalidValue;
+    ParamSegs segs{};
+    segs.n = n_seg;
+    int total = 0;
+    for (int k = 0; k < n_seg; ++k) {
+        if (bytes[k] % 4 != 0) return cudaErrorInvalidValue;
+        total += bytes[k];
+        segs.dst[k] = static_cast<unsigned char*>(dst[k]);
+        segs.end[k] = total;
+    }
+    auto go = [&](auto tag) -> cudaError_t {
+        using Blob = decltype(tag);
+        Blob blob;
+        int off = 0;
+        for (int k = 0; k < n_seg; ++k) {
+            std::memcpy(blob.b + off, src[k], size_t(bytes[k]));
+            off += bytes[k];
+        }
+        k_params<<<1, 256, 0, stream>>>(blob, segs, zero, n_zero);
+        return cudaGetLastError();
+    };
+    if (total <= 2048) return go(ParamBlob<2048>{});
+    if (total <= 8192) return go(ParamBlob<8192>{});
+    if (total <= 30720) return go(ParamBlob<30720>{});
+    return cudaErrorNotSupported;
+}
+
 __global__ void k_zero(cplx* p, int64_t n) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
         stc(p + i, czero());

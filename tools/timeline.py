@@ -3,7 +3,8 @@ graph the bench times) from CUPTI activity records via torch.profiler -- no
 replay, launches run as in the bench.  Prints every kernel of the last march
 with its start offset and duration, and totals per kernel name.
 
-    python tools/timeline.py [workload] [steps]
+    python tools/timeline.py [workload] [steps] [shard_of]
+(shard_of N: rank 0's frequency block of an N-way split, as bench.py --shard-of)
 """
 import collections
 import sys
@@ -19,8 +20,10 @@ def main():
     import bench
     name = sys.argv[1] if len(sys.argv) > 1 else "cfg4"
     steps = int(sys.argv[2]) if len(sys.argv) > 2 else 20
+    shard = int(sys.argv[3]) if len(sys.argv) > 3 else 1
     cfg = bench.workload(name, steps)
-    freqs = list(cfg.source.frequencies)
+    from paper_1711_00005_b200 import parallel
+    freqs = parallel.rank_frequencies(list(cfg.source.frequencies), 0, shard)
     m = bench.DeviceMarch(cfg, freqs, 0, steps, cfg.options.output_stride)
     for _ in range(3):
         m.timed(steps)
@@ -29,7 +32,7 @@ def main():
     evs = [e for e in prof.events() if e.device_type.name == "CUDA" and e.name not in ("Memset", "Memcpy")]
     evs.sort(key=lambda e: e.time_range.start)
     t0 = evs[0].time_range.start
-    print(f"{name}, {steps} steps: CUDA-event time of the march {ms * 1e3:.1f} us")
+    print(f"{name}, {len(freqs)} frequencies, {steps} steps: CUDA-event time of the march {ms * 1e3:.1f} us")
     tot = collections.defaultdict(float)
     cnt = collections.Counter()
     for e in evs:
