@@ -388,6 +388,35 @@ def test_concurrent_chains_bitwise_equal_to_one_chain(monkeypatch, chains):
         assert x.clamped_samples == y.clamped_samples
 
 
+@pytest.mark.parametrize("n_steps,stride", [(2, 5), (6, 3), (9, 4)])
+def test_march_graph_variants_bitwise_equal(monkeypatch, n_steps, stride):
+    """The march's round-2 launch forms against their plain counterparts, bitwise:
+    the final slab stored by TMA from the azimuth sweep's stage (reference layout,
+    PE3D_FINAL_STORES: per-element stores), the parameters carried by one kernel
+    node (PE3D_PARAMS_MEMCPY: copies from page-locked staging), and the write-only
+    prologue of a column starter (PE3D_PREPARE_STAGED: the staged prologue).  Final
+    step with and without a TL sample; two chains."""
+    freqs = (50.0, 170.0, 420.0)
+    cfg = configs.build("cfg4", n_range=max(n_steps, 3), frequencies=freqs, output_stride=stride)
+
+    def run():
+        res = march_frequencies(cfg, list(freqs), n_steps=n_steps)
+        return [(r.tl_field.tobytes(), r.final_slab.values.tobytes(), r.clamped_samples) for r in res]
+
+    monkeypatch.setenv("PE3D_CHAINS", "2")
+    ref = None
+    for switch in (None, "PE3D_FINAL_STORES", "PE3D_PARAMS_MEMCPY", "PE3D_PREPARE_STAGED"):
+        for name in ("PE3D_FINAL_STORES", "PE3D_PARAMS_MEMCPY", "PE3D_PREPARE_STAGED"):
+            monkeypatch.delenv(name, raising=False)
+        if switch:
+            monkeypatch.setenv(switch, "1")
+        got = run()
+        if ref is None:
+            ref = got
+        else:
+            assert got == ref, switch
+
+
 @pytest.mark.parametrize("shape", ["cfg4", "long"])
 def test_depth_setup_table_bitwise_equal_to_in_kernel_setup(monkeypatch, shape):
     """The per-march depth-sweep setup records (k_depth_setup /
