@@ -33,6 +33,9 @@ struct MarchPlan {
     bool serial;
     int64_t field_elems;
     int n_samples;
+    // column starter: the prologue leaves the first temp as one column per frequency
+    // ([F][n_tiles][8]) and the first depth sweep reads it (null: the full field)
+    pe3d::cplx* temp_col;
 };
 
 // Number of concurrent step-loop chains.  Frequencies are independent, so a
@@ -165,7 +168,9 @@ cudaError_t enqueue_group(Handle* h, const pe3d_grid* g, const MarchPlan& p, int
     for (int s = 0; s < g->n_steps; ++s) {
         const int j_new = g->first_index + s + 1;
         const double r_new = g->r_start + j_new * g->delta_r;      // Grid3D.range_at
-        cudaError_t e = prof.run(0, [&] { return pe3d::launch_depth_scan(ck1, A, B); });
+        pe3d::LaunchCtx ck = ck1;
+        if (s == 0 && p.temp_col) ck.src_col = p.temp_col + int64_t(f0) * c.n_tiles * 8;
+        cudaError_t e = prof.run(0, [&] { return pe3d::launch_depth_scan(ck, A, B); });
         if (e != cudaSuccess) return e;
         if (c.split) {                                      // exact sub-column carries for the azimuth sweep
             e = prof.run(2, [&] { return pe3d::launch_split_carry(cg); });
@@ -498,6 +503,13 @@ static int march_device_impl(void* handle, const pe3d_grid* g, const pe3d_coeffs
     ea0.periodic = g->topology == PE3D_PERIODIC;
     ea0.write_temp = g->n_steps > 0;
     ea0.src_column = (g->flags & PE3D_FLAG_STARTER_COLUMN) != 0;
+    // a column starter on a periodic ring stays one column through the prologue: the first
+    // depth sweep reads it directly (the azimuth-uniform first temp is never written)
+    if (ea0.src_column && ea0.periodic && !p.serial && g->n_steps > 0 && pe3d::depth_sweep_takes_column(c)) {
+        CK(h->col_tab.ensure(int64_t(F) * n_tiles * 8 * sizeof(cplx)), "alloc column");
+        p.temp_col = h->col_tab.as<cplx>();
+        ea0.temp_col = p.temp_col;
+    }
     if (sink) CK(tl_prepare(h, *sink), "tl streams");
     auto enqueue_prologue = [&]() -> cudaError_t {
         return prof.run(2, [&] { return pe3d::launch_finish(c, reinterpret_cast<const cplx*>(d_u0), 0,
@@ -536,7 +548,8 @@ static int march_device_impl(void* handle, const pe3d_grid* g, const pe3d_coeffs
         add(coeffs, sizeof(pe3d_coeffs) * F);
         add(ptrs, sizeof(ptrs));
         add(&stream, sizeof(stream));
-        const void* tabs[6] = {h->w_abs.ptr, h->fdev.ptr, h->loc_tab.ptr, h->err.ptr, h->ring_tab.ptr, p.ctx.k1_tab};
+        const void* tabs[7] = {h->w_abs.ptr, h->fdev.ptr, h->loc_tab.ptr, h->err.ptr, h->ring_tab.ptr, p.ctx.k1_tab,
+                               p.temp_col};
         add(tabs, sizeof(tabs));
         const int chains = step_chains(p.ctx, false);
         add(&chains, sizeof(chains));
@@ -548,7 +561,8 @@ static int march_device_impl(void* handle, const pe3d_grid* g, const pe3d_coeffs
         // the A/B switches pick kernels and launch attributes baked into the graph
         for (const char* name : {"PE3D_NO_PDL", "PE3D_CLUSTER_L", "PE3D_DEPTH_NO_CLUSTER", "PE3D_RING_BLOCK",
                                  "PE3D_RING_CPASYNC", "PE3D_DEPTH_NO_SPLIT", "PE3D_FACTOR_SERIAL",
-                                 "PE3D_PREPARE_STAGED", "PE3D_PARAMS_MEMCPY", "PE3D_FINAL_STORES"}) {
+                                 "PE3D_PREPARE_STAGED", "PE3D_PARAMS_MEMCPY", "PE3D_FINAL_STORES",
+                                 "PE3D_FIRST_STEP_FIELD"}) {
             const char* v = getenv(name);
             const std::string val = v ? std::string("=") + v : std::string("-");
             add(val.data(), val.size() + 1);

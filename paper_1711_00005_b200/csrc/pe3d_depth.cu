@@ -408,7 +408,7 @@ __global__ void __launch_bounds__(MAXT, MINB)
 k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ DepthDst tm_dst,
             const cplx* __restrict__ loc_tab, const cplx* __restrict__ mul_tab, const FreqDev* __restrict__ fdev,
             const cplx* __restrict__ k1_tab, int n_theta, int n_tiles, int64_t total_cols, int cols_per_cta,
-            int sector, const cplx* __restrict__ src_raw, int split, cplx* __restrict__ sp_tot) {
+            int sector, const cplx* __restrict__ src_raw, int split, cplx* __restrict__ sp_tot, int src_col) {
     constexpr int RPT = 8;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     const int nthreads = NTH ? NTH : int(blockDim.x);   // compile-time when NTH: constant table offsets
@@ -496,7 +496,7 @@ k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ 
         for (int p = 0; p < STAGES - 1; ++p) {
             if (p < n_cols) {
                 mbar_expect_tx(&bars[p], 32 * 128);
-                tma_load_4d(stage + p * 256, &tm_src, 0, pc, tile0, pf, &bars[p]);
+                tma_load_4d(stage + p * 256, &tm_src, 0, src_col ? 0 : pc, tile0, pf, &bars[p]);
                 if (++pc == n_theta) { pc = 0; ++pf; }
             }
         }
@@ -674,7 +674,7 @@ k_depth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ 
             if (it + STAGES - 1 < n_cols) {
                 const int ps = (slot + STAGES - 1) % STAGES;
                 mbar_expect_tx(&bars[ps], 32 * 128);
-                tma_load_4d(stage + ps * 256, &tm_src, 0, pc, tile0, pf, &bars[ps]);
+                tma_load_4d(stage + ps * 256, &tm_src, 0, src_col ? 0 : pc, tile0, pf, &bars[ps]);
                 if (++pc == n_theta) { pc = 0; ++pf; }
             }
         }
@@ -1179,6 +1179,20 @@ static bool field_tensor_map(CUtensorMap* tm, const void* base, const LaunchCtx&
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// The first step's input when it is one column per frequency (LaunchCtx::src_col):
+// [F][n_tiles][8] complex, one azimuth.
+static bool column_tensor_map(CUtensorMap* tm, const void* base, const LaunchCtx& c) {
+    auto enc = tensor_map_encoder();
+    if (!enc) return false;
+    const cuuint64_t dims[4] = {16, 1, cuuint64_t(c.n_tiles), cuuint64_t(c.n_freq)};
+    const cuuint64_t strides[3] = {128, 128, cuuint64_t(c.n_tiles) * 128};
+    const cuuint32_t box[4] = {16, 1, 32, 1};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<void*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // Output maps: the plain field, or one map per peer chunk (slab march).
 static bool depth_dst_maps(DepthDst* d, const void* dst, const LaunchCtx& c) {
     if (c.n_peers == 0) {
@@ -1198,7 +1212,12 @@ template <int STAGES, int MINB, int MAXT, bool SPLIT = false>
 static cudaError_t launch_depth_tma_cfg(const LaunchCtx& c, const cplx* src, cplx* dst) {
     CUtensorMap tm_src;
     DepthDst tm_dst;
-    if (!field_tensor_map(&tm_src, src, c) || !depth_dst_maps(&tm_dst, dst, c)) return cudaErrorNotSupported;
+    // c.src_col: the input is one column per frequency ([F][n_tiles][8]), the same for every
+    // azimuth (the first step after a column starter's prologue): a map with one azimuth,
+    // every column loads azimuth 0
+    if (c.src_col && (SPLIT || c.sector)) return cudaErrorNotSupported;
+    const bool ok = c.src_col ? column_tensor_map(&tm_src, c.src_col, c) : field_tensor_map(&tm_src, src, c);
+    if (!ok || !depth_dst_maps(&tm_dst, dst, c)) return cudaErrorNotSupported;
     const int nthreads = (c.n_tiles + 31) / 32 * 32;
     const int nwarps = nthreads / 32;
     const size_t bytes = 1024 + sizeof(cplx) * (size_t(nwarps) * STAGES * 256 + 10 * size_t(nthreads) + 5 * nwarps + 4) +
@@ -1223,7 +1242,8 @@ static cudaError_t launch_depth_tma_cfg(const LaunchCtx& c, const cplx* src, cpl
     const int per = int((total + ctas - 1) / ctas);
     const int grid = int((total + per - 1) / per);
     return launch_pdl(c.pdl != 0, kern, dim3(grid), dim3(nthreads), bytes, c.stream, tm_src, tm_dst, c.loc_tab,
-                      c.mul_tab, c.fdev, k1, c.n_theta, c.n_tiles, total, per, c.sector, src, c.split, c.sp_tot);
+                      c.mul_tab, c.fdev, k1, c.n_theta, c.n_tiles, total, per, c.sector, src, c.split, c.sp_tot,
+                      c.src_col ? 1 : 0);
 }
 
 static cudaError_t launch_depth_tma_cluster(const LaunchCtx& c, const cplx* src, cplx* dst, int CL) {
@@ -1392,7 +1412,12 @@ cudaError_t launch_split_carry(const LaunchCtx& c) {
                       c.sp_pa, c.sp_cd, c.n_freq, c.n_theta, c.split, ring_segment(c.n_theta) / 32);
 }
 
+bool depth_sweep_takes_column(const LaunchCtx& c) {
+    return c.split < 2 && !c.sector && c.n_peers == 0 && c.n_tiles <= 128 && !getenv("PE3D_FIRST_STEP_FIELD");
+}
+
 cudaError_t launch_depth_scan(const LaunchCtx& c, const cplx* src, cplx* dst) {
+    if (c.src_col) return c.n_tiles <= 128 ? launch_depth_tma_cfg<3, 3, 128>(c, src, dst) : cudaErrorNotSupported;
     if (c.split >= 2) {
         // every 1024-row sub-column as a column of its own virtual frequency
         LaunchCtx v = c;

@@ -50,6 +50,9 @@ struct EpilogueArgs {
     // march prologue only: the starter u0 is one column per frequency ([F][n_depth],
     // PE3D_FLAG_STARTER_COLUMN) instead of a [F][n_theta][n_depth] slab
     int src_column;
+    // march prologue only, with src_column: write the first temp as one column per
+    // frequency ([F][n_tiles][8]) here instead of the azimuth-uniform field
+    cplx* temp_col;
 };
 
 // Destination of the next temp of ring element (m, row r) of local tile t.
@@ -116,6 +119,10 @@ struct LaunchCtx {
     cplx* sp_aq;            // [F][n_tiles*8][2]
     cplx* sp_pa;            // [F*split][3]: P_s, A_s, (a_span, q_span) rows needing the correction
     cplx* sp_cd;            // [F][split][2][n_theta]
+    // First step after a column starter's prologue (depth_sweep_takes_column): the depth
+    // sweep reads its input from one column per frequency, [F][n_tiles][8], instead of the
+    // azimuth-uniform field the prologue would otherwise have to write
+    const cplx* src_col;
     int n_peers;
     int peer_tiles;
     cplx* peer_dst[MAX_PEERS];
@@ -176,6 +183,7 @@ int ring_table_elems(int n_theta);   // complex entries per (step, frequency) ri
 cudaError_t launch_factor_depth(const LaunchCtx& c, const cplx* local, int64_t local_fstride, int step_for_error);
 cudaError_t launch_factor_depth_scan(const LaunchCtx& c, const cplx* local, int64_t local_fstride, int step_for_error);
 cudaError_t launch_depth_scan(const LaunchCtx& c, const cplx* src, cplx* dst);
+bool depth_sweep_takes_column(const LaunchCtx& c);
 // Split-column plan for a march (0: no split) and the per-step carry kernel.
 int depth_split_plan(const LaunchCtx& c, int periodic);
 cudaError_t launch_split_carry(const LaunchCtx& c);

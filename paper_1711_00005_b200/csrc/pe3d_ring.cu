@@ -1548,8 +1548,11 @@ k_prepare_column(const cplx* __restrict__ u0, cplx* __restrict__ dst, const Freq
         }
     }
     __syncthreads();
-    // first temp: tiles [l0/8, l0/8 + rows/8), each n_theta lines of 8 rows
-    if (ea.write_temp) {
+    // first temp: one column per frequency for the first depth sweep (LaunchCtx::src_col) ...
+    if (ea.write_temp && ea.temp_col) {
+        if (tid < rows) ea.temp_col[(int64_t(f) * n_tiles * 8) + l0 + tid] = st[tid];
+    } else if (ea.write_temp) {
+        // ... or tiles [l0/8, l0/8 + rows/8), each n_theta lines of 8 rows
         cplx* base = dst + ring_base(f, 0, n_tiles, n_theta, n_theta) + int64_t(l0 / 8) * n_theta * 8;
         const int line_elems = n_theta * 8, n = (rows / 8) * line_elems;   // <= 2^18: 32-bit indices
         for (int e = tid; e < n; e += blockDim.x) stc_stream(base + e, st[(e / line_elems) * 8 + (e & 7)]);
@@ -1952,12 +1955,13 @@ cudaError_t launch_azimuth_scan(const LaunchCtx& c, const cplx* src, cplx* dst, 
 cudaError_t launch_finish(const LaunchCtx& c, const cplx* src, int src_tiled, cplx* dst, double r,
                           const EpilogueArgs& ea) {
     const bool standard = ea.chunk_gap == 0 && (ea.chunk_cols == 0 || ea.chunk_cols == c.n_theta) && !ea.peer[0];
-    if (!src_tiled && standard && ea.src_column && ea.periodic && !getenv("PE3D_PREPARE_STAGED")) {
+    if (!src_tiled && standard && ea.src_column && ea.periodic && (ea.temp_col || !getenv("PE3D_PREPARE_STAGED"))) {
         dim3 grid((c.n_tiles * 8 + PREPC_ROWS - 1) / PREPC_ROWS, c.n_freq);
         k_prepare_column<<<grid, 256, 0, c.stream>>>(src, dst, c.fdev, c.n_theta, c.n_tiles, c.n_depth, r,
                                                      c.delta_theta, ea);
         return cudaGetLastError();
     }
+    if (ea.temp_col) return cudaErrorInvalidValue;         // only the column prologue writes a temp column
     if (!src_tiled && standard && c.n_theta % PREP_MB == 0) {
         dim3 grid(c.n_theta / PREP_MB, (c.n_tiles * 8 + PREP_DB - 1) / PREP_DB, c.n_freq);
         k_prepare<<<grid, 256, 0, c.stream>>>(src, dst, c.fdev, c.n_theta, c.n_tiles, c.n_depth, r, c.delta_theta, ea);

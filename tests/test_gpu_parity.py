@@ -393,9 +393,10 @@ def test_march_graph_variants_bitwise_equal(monkeypatch, n_steps, stride):
     """The march's round-2 launch forms against their plain counterparts, bitwise:
     the final slab stored by TMA from the azimuth sweep's stage (reference layout,
     PE3D_FINAL_STORES: per-element stores), the parameters carried by one kernel
-    node (PE3D_PARAMS_MEMCPY: copies from page-locked staging), and the write-only
-    prologue of a column starter (PE3D_PREPARE_STAGED: the staged prologue).  Final
-    step with and without a TL sample; two chains."""
+    node (PE3D_PARAMS_MEMCPY: copies from page-locked staging), the write-only
+    prologue of a column starter (PE3D_PREPARE_STAGED: the staged prologue) and the
+    first depth sweep reading the starter's temp column (PE3D_FIRST_STEP_FIELD: the
+    azimuth-uniform temp field).  Final step with and without a TL sample; two chains."""
     freqs = (50.0, 170.0, 420.0)
     cfg = configs.build("cfg4", n_range=max(n_steps, 3), frequencies=freqs, output_stride=stride)
 
@@ -405,8 +406,9 @@ def test_march_graph_variants_bitwise_equal(monkeypatch, n_steps, stride):
 
     monkeypatch.setenv("PE3D_CHAINS", "2")
     ref = None
-    for switch in (None, "PE3D_FINAL_STORES", "PE3D_PARAMS_MEMCPY", "PE3D_PREPARE_STAGED"):
-        for name in ("PE3D_FINAL_STORES", "PE3D_PARAMS_MEMCPY", "PE3D_PREPARE_STAGED"):
+    switches = ("PE3D_FINAL_STORES", "PE3D_PARAMS_MEMCPY", "PE3D_PREPARE_STAGED", "PE3D_FIRST_STEP_FIELD")
+    for switch in (None,) + switches:
+        for name in switches:
             monkeypatch.delenv(name, raising=False)
         if switch:
             monkeypatch.setenv(switch, "1")
