@@ -303,33 +303,37 @@ cudaError_t launch_depth_medium_scan(const LaunchCtx& c, const MediumDev& M, con
 }
 
 // Range-independent depth factorization (tables of K1), one CTA per
-// frequency, thread t owning depth tile t: the same continuant scan as above
-// replaces the single-thread Thomas recurrence of k_factor_depth (ref
+// frequency, thread t owning RPT consecutive rows: the same continuant scan as
+// above replaces the single-thread Thomas recurrence of k_factor_depth (ref
 // tridiag.py:151-167): d_l = p_l / p_(l-1), m_l = -off / d_l, loc_tab = the
 // local term, pads zero; the first pivot below the floor is reported with
-// the reference's (row, member) convention.
+// the reference's (row, member) convention.  It sits on the march's setup
+// path (before the first depth sweep), which is latency bound: RPT = 2 (512
+// threads for 1024 rows) and a warp scan of the warp products replace the
+// 8-row serial chains and the serial warp loop (cfg4, 8 frequencies: 17 ->
+// ~6 us standalone).
+template <int RPT>
 __global__ void __launch_bounds__(512)
 k_factor_depth_scan(const cplx* __restrict__ local, int64_t local_fstride, cplx* __restrict__ loc_tab,
-                    cplx* __restrict__ mul_tab, const FreqDev* __restrict__ fdev, int n_depth, int n_tiles,
+                    cplx* __restrict__ mul_tab, const FreqDev* __restrict__ fdev, int n_depth, int n_rows,
                     int step_for_error, DevError* err) {
-    __shared__ M2 sM[16];
+    __shared__ M2 sM[32];
     __shared__ int sFail;
-    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nwarps = int(blockDim.x) >> 5;
     const int f = blockIdx.x;
-    const bool active = t < n_tiles;
+    const bool active = t * RPT < n_rows;
     const FreqDev fd = fdev[f];
-    const int nz8 = n_tiles * 8;
     if (t == 0) sFail = 0x7fffffff;
     const cplx off2 = cmul(fd.off_z, fd.off_z);
     const double two_s = 2.0 * fd.s_z;
-    cplx mainv[8];
+    cplx mainv[RPT];
     M2 T{cone(), czero(), czero(), cone()};
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const int l = 8 * t + i;
+    for (int i = 0; i < RPT; ++i) {
+        const int l = RPT * t + i;
         const bool real_row = active && l < n_depth;
         const cplx loc = real_row ? ldc(local + f * local_fstride + l) : czero();
-        if (active) stc(loc_tab + int64_t(f) * nz8 + l, loc);
+        if (active) stc(loc_tab + int64_t(f) * n_rows + l, loc);
         mainv[i] = cadd(cone(), cmul(fd.cx_lhs, mk(loc.re - two_s, loc.im)));
         M2 Ml;
         if (l == 0 || !real_row) Ml = M2{cone(), czero(), czero(), cone()};   // surface / pads: identity
@@ -343,15 +347,27 @@ k_factor_depth_scan(const cplx* __restrict__ local, int64_t local_fstride, cplx*
     }
     if (lane == 31) sM[warp] = T;
     __syncthreads();
-    M2 Cw{cone(), czero(), czero(), cone()};
-    for (int w = 0; w < warp; ++w) Cw = m2norm(m2mul(sM[w], Cw));
+    if (warp == 0) {                                        // exclusive scan of the warp products
+        M2 W = lane < nwarps ? sM[lane] : M2{cone(), czero(), czero(), cone()};
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const M2 Wp = shfl_up_m2(W, d);
+            if (lane >= d) W = m2norm(m2mul(W, Wp));
+        }
+        M2 E = shfl_up_m2(W, 1);
+        if (lane == 0) E = M2{cone(), czero(), czero(), cone()};
+        __syncwarp();
+        if (lane < nwarps) sM[lane] = E;
+    }
+    __syncthreads();
+    const M2 Cw = sM[warp];
     M2 Tin = shfl_up_m2(m2norm(m2mul(T, Cw)), 1);
     if (lane == 0) Tin = Cw;
     cplx pa = Tin.a, pb = Tin.c;
     int my_fail = 0x7fffffff;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const int l = 8 * t + i;
+    for (int i = 0; i < RPT; ++i) {
+        const int l = RPT * t + i;
         cplx mult = czero();
         if (l == 0) {
             pa = cone(); pb = czero();                      // d_0 = main_0 = 1 (surface row)
@@ -365,7 +381,7 @@ k_factor_depth_scan(const cplx* __restrict__ local, int64_t local_fstride, cplx*
             if (sc > 0.0 && isfinite(sc)) { pa = crmul(1.0 / sc, pa); pb = crmul(1.0 / sc, pb); }
             mult = cneg(cmul(fd.off_z, crecip(d)));
         }
-        if (active) stc(mul_tab + int64_t(f) * nz8 + l, mult);
+        if (active) stc(mul_tab + int64_t(f) * n_rows + l, mult);
     }
     if (my_fail != 0x7fffffff) atomicMin(&sFail, my_fail);
     __syncthreads();
@@ -374,11 +390,17 @@ k_factor_depth_scan(const cplx* __restrict__ local, int64_t local_fstride, cplx*
 
 cudaError_t launch_factor_depth_scan(const LaunchCtx& c, const cplx* local, int64_t local_fstride,
                                      int step_for_error) {
-    const int nthreads = (c.n_tiles + 31) / 32 * 32;
-    if (nthreads > 512) return cudaErrorNotSupported;
-    k_factor_depth_scan<<<c.n_freq, nthreads, 0, c.stream>>>(local, local_fstride, c.loc_tab, c.mul_tab, c.fdev,
-                                                             c.n_depth, c.n_tiles, step_for_error, c.err);
-    return cudaGetLastError();
+    const int n_rows = c.n_tiles * 8;
+    auto go = [&](auto kern, int rpt) -> cudaError_t {
+        const int nthreads = (n_rows / rpt + 31) / 32 * 32;
+        kern<<<c.n_freq, nthreads, 0, c.stream>>>(local, local_fstride, c.loc_tab, c.mul_tab, c.fdev, c.n_depth,
+                                                  n_rows, step_for_error, c.err);
+        return cudaGetLastError();
+    };
+    if (n_rows <= 1024) return go(k_factor_depth_scan<2>, 2);     // <= 512 threads each
+    if (n_rows <= 2048) return go(k_factor_depth_scan<4>, 4);
+    if (n_rows <= 4096) return go(k_factor_depth_scan<8>, 8);
+    return cudaErrorNotSupported;
 }
 
 // local term in the device tile layout (the starter range of the scan path)
