@@ -517,11 +517,11 @@ static int march_device_impl(void* handle, const pe3d_grid* g, const pe3d_coeffs
     };
 
     if (use_graph) {
-        // ONE graph for the whole march: the parameter uploads (memcpy nodes from
-        // page-locked staging), the setup kernels on a side branch running under
-        // the prologue, the prologue, then the step loop.  Launched as is, the
-        // march used to spend ~85 us in host-issued uploads and serial setup
-        // kernels before the prologue (cfg4, tools/timeline.py).
+        // The whole march as two cached graphs (prologue graph, step graph; see the
+        // capture below).  Issued from the host, the uploads and the serial setup
+        // kernels before the prologue used to cost ~85 us of the march (cfg4,
+        // tools/timeline.py).  The page-locked staging feeds the copy fallback for
+        // parameter sets too large for one kernel node.
         const size_t fd_b = F * sizeof(pe3d::FreqDev), w_b = wabs.size() * sizeof(double);
         const size_t w_o = (fd_b + 15) & ~size_t(15), e_o = (w_o + w_b + 15) & ~size_t(15);
         CK(h->params_pin.ensure(e_o + sizeof(de0)), "alloc pinned params");
