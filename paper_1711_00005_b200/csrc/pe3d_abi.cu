@@ -16,6 +16,7 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "../../include/pe3d_b200.h"
@@ -367,7 +368,12 @@ int pe3d_handle_destroy(void* handle) {
     cudaSetDevice(h->device);
     for (DevBuf* b : h->buffers()) b->release();
     if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
-    if (h->pre_exec) cudaGraphExecDestroy(h->pre_exec);
+    for (auto& mg : h->march_graphs) {
+        if (mg.pre) cudaGraphExecDestroy(mg.pre);
+        if (mg.steps) cudaGraphExecDestroy(mg.steps);
+    }
+    if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
+    if (h->copy_ev) cudaEventDestroy(h->copy_ev);
     for (int k = 0; k <= Handle::MAX_CHAINS; ++k)
         if (h->tl_side[k]) cudaStreamDestroy(h->tl_side[k]);
     for (cudaEvent_t e : h->tl_ev) cudaEventDestroy(e);
@@ -569,12 +575,21 @@ static int march_device_impl(void* handle, const pe3d_grid* g, const pe3d_coeffs
         }
         const TlSink none{nullptr, 0, 0};
         add(sink ? sink : &none, sizeof(TlSink));
-        if (!(h->graph_exec && h->pre_exec && key == h->graph_key)) {
-            if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
-            if (h->pre_exec) cudaGraphExecDestroy(h->pre_exec);
-            h->graph_exec = nullptr;
-            h->pre_exec = nullptr;
-            h->graph_key.clear();
+        int hit = -1;
+        for (int i = 0; i < int(h->march_graphs.size()); ++i)
+            if (h->march_graphs[i].key == key) hit = i;
+        if (hit >= 0) {                                     // most recently used goes last
+            Handle::MarchGraph mg = h->march_graphs[hit];
+            h->march_graphs.erase(h->march_graphs.begin() + hit);
+            h->march_graphs.push_back(mg);
+        } else {
+            if (int(h->march_graphs.size()) >= Handle::MAX_MARCH_GRAPHS) {
+                Handle::MarchGraph& old = h->march_graphs.front();
+                if (old.pre) cudaGraphExecDestroy(old.pre);
+                if (old.steps) cudaGraphExecDestroy(old.steps);
+                h->march_graphs.erase(h->march_graphs.begin());
+            }
+            Handle::MarchGraph mg;
             auto capture = [&](cudaGraphExec_t* out, auto&& body) -> cudaError_t {
                 cudaGraph_t graph = nullptr;
                 cudaError_t e = cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal);
@@ -594,7 +609,7 @@ static int march_device_impl(void* handle, const pe3d_grid* g, const pe3d_coeffs
             // same graph the setup branch started after the whole loop had been submitted
             // (+110 us at 64 frequencies x 20 steps, +390 us at 100 steps, +350 us at 8
             // frequencies x 20 steps on 8 chains; tools/timeline.py).
-            cudaError_t e = capture(&h->pre_exec, [&]() -> cudaError_t {
+            cudaError_t e = capture(&mg.pre, [&]() -> cudaError_t {
                 // the parameters travel by value in one small kernel node (they are part of the
                 // graph key); larger ones as copies from the page-locked staging
                 const void* srcs[3] = {fd.data(), wabs.data(), &de0};
@@ -624,24 +639,25 @@ static int march_device_impl(void* handle, const pe3d_grid* g, const pe3d_coeffs
                 return ep != cudaSuccess ? ep : (es != cudaSuccess ? es : ej);
             });
             if (e == cudaSuccess)
-                e = capture(&h->graph_exec, [&]() -> cudaError_t {
+                e = capture(&mg.steps, [&]() -> cudaError_t {
                     return enqueue_steps(h, g, p, local, d_tl, reinterpret_cast<cplx*>(d_snapshots),
                                          reinterpret_cast<cplx*>(d_u_final), d_clamped, h->w_abs.as<double>(), prof,
                                          sink);
                 });
-            h->graph_launches = prof.launches - before;
+            mg.launches = prof.launches - before;
             prof.launches = before;
             if (e != cudaSuccess) {
-                if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
-                if (h->pre_exec) cudaGraphExecDestroy(h->pre_exec);
-                h->graph_exec = h->pre_exec = nullptr;
+                if (mg.pre) cudaGraphExecDestroy(mg.pre);
+                if (mg.steps) cudaGraphExecDestroy(mg.steps);
                 return cuda_fail(err, e, "march graph");
             }
-            h->graph_key = key;
+            mg.key = std::move(key);
+            h->march_graphs.push_back(mg);
         }
-        CK(cudaGraphLaunch(h->pre_exec, stream), "graph launch");
-        CK(cudaGraphLaunch(h->graph_exec, stream), "graph launch");
-        prof.launches += h->graph_launches;
+        const Handle::MarchGraph& mg = h->march_graphs.back();
+        CK(cudaGraphLaunch(mg.pre, stream), "graph launch");
+        CK(cudaGraphLaunch(mg.steps, stream), "graph launch");
+        prof.launches += mg.launches;
     } else {
         CK(cudaMemcpyAsync(h->fdev.ptr, fd.data(), F * sizeof(pe3d::FreqDev), cudaMemcpyHostToDevice, stream), "H2D");
         CK(cudaMemcpyAsync(h->w_abs.ptr, wabs.data(), wabs.size() * sizeof(double), cudaMemcpyHostToDevice, stream),
@@ -661,6 +677,35 @@ static int march_device_impl(void* handle, const pe3d_grid* g, const pe3d_coeffs
     if (!p.serial && g->topology == PE3D_PERIODIC) hf = azimuth_failures(g, coeffs);   // the ring sweep has no pivots
     return decode_error(h, stream, err, &hf);
 }
+
+}  // extern "C"
+
+// Frequency groups of a pe3d_march_host call (see there): >1 only when the final
+// slab's copy to the host (PCIe, modelled at 57 GB/s) would take longer than half
+// the march (modelled at 5.5 TB/s of HBM for the 64 B per grid point and step);
+// PE3D_HOST_GROUPS=n forces n.
+static int host_groups(const pe3d_grid* g, bool has_final, bool has_snapshots) {
+    const int F = g->n_freq;
+    int G = 1;
+    if (const char* env = getenv("PE3D_HOST_GROUPS")) {
+        G = atoi(env);
+    } else if (has_final && !has_snapshots && g->topology == PE3D_PERIODIC && g->n_steps >= 2) {
+        const double points = double(F) * g->n_theta * g->n_depth;
+        const double t_copy = points * 16 / 57e9, t_march = points * 64 * g->n_steps / 5.5e12;
+        if (t_copy > 0.5 * t_march) G = 4;
+    }
+    if (has_snapshots) G = 1;                   // snapshots leave after the march
+    G = std::min(G, F / 2);                     // at least two frequencies per group
+    return G < 1 ? 1 : G;
+}
+
+// Propagate a non-singular failure of one group unchanged.
+static int cuda_or(pe3d_error* err, int st, const pe3d_error& e) {
+    if (err) *err = e;
+    return st;
+}
+
+extern "C" {
 
 int pe3d_march_host(void* handle, const pe3d_grid* g, const pe3d_coeffs* coeffs, const pe3d_c128* local,
                     const pe3d_c128* u0, pe3d_c128* u_final, double* tl, pe3d_c128* snapshots, int64_t* clamped,
@@ -692,12 +737,57 @@ int pe3d_march_host(void* handle, const pe3d_grid* g, const pe3d_coeffs* coeffs,
     if (snapshots) CK(h->h_snap.ensure(F * S * slab * sizeof(cplx)), "alloc");
     CK(cudaMemcpyAsync(h->h_local.ptr, local, F * g->n_depth * sizeof(cplx), cudaMemcpyHostToDevice, s), "H2D");
     CK(cudaMemcpyAsync(h->h_u0.ptr, u0, u0_elems * sizeof(cplx), cudaMemcpyHostToDevice, s), "H2D");
-    st = march_device_impl(handle, g, coeffs, h->h_local.as<pe3d_c128>(), h->h_u0.as<pe3d_c128>(),
-                           u_final ? h->h_final.as<pe3d_c128>() : nullptr, tl ? h->h_tl.as<double>() : nullptr,
-                           snapshots ? h->h_snap.as<pe3d_c128>() : nullptr, h->h_clamped.as<int64_t>(), s, err,
-                           sink.host ? &sink : nullptr);
-    if (st != PE3D_OK) return st;
-    if (u_final) CK(cudaMemcpyAsync(u_final, h->h_final.ptr, F * slab * sizeof(cplx), cudaMemcpyDeviceToHost, s), "D2H");
+    // Short marches with a final slab are bound by its device-to-host copy (PCIe,
+    // ~57 GB/s: 4.7 ms for cfg4's 268 MB against a 3.8 ms 20-step march).  Then the
+    // frequencies are marched in groups, one after another, and each group's final
+    // slab leaves on a copy stream while the next group marches.
+    const int G = host_groups(g, u_final != nullptr, snapshots != nullptr);
+    if (G > 1) {
+        if (!h->copy_stream) CK(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking), "stream");
+        if (!h->copy_ev) CK(cudaEventCreateWithFlags(&h->copy_ev, cudaEventDisableTiming), "event");
+    }
+    const int64_t u0_per = (g->flags & PE3D_FLAG_STARTER_COLUMN) ? g->n_depth : slab;
+    const int64_t tl_per = (sink.host ? sink.R : S) * slab;
+    pe3d_error best{};
+    int best_st = PE3D_OK;
+    for (int gi = 0; gi < G; ++gi) {
+        const int f0 = int(F * gi / G), f1 = int(F * (gi + 1) / G);
+        pe3d_grid gg = *g;
+        gg.n_freq = f1 - f0;
+        TlSink sk = sink;
+        if (sk.host) sk.host = tl + int64_t(f0) * S * slab;
+        pe3d_error e_g{};
+        const int st_g =
+            march_device_impl(handle, &gg, coeffs + f0, h->h_local.as<pe3d_c128>() + int64_t(f0) * g->n_depth,
+                              h->h_u0.as<pe3d_c128>() + f0 * u0_per,
+                              u_final ? h->h_final.as<pe3d_c128>() + f0 * slab : nullptr,
+                              tl ? h->h_tl.as<double>() + f0 * tl_per : nullptr,
+                              snapshots ? h->h_snap.as<pe3d_c128>() : nullptr, h->h_clamped.as<int64_t>() + f0, s,
+                              &e_g, sk.host ? &sk : nullptr);
+        if (st_g != PE3D_OK) {
+            // the batch reports the lowest (step, sweep, frequency, member), as one march would
+            if (st_g != PE3D_SINGULAR) return cuda_or(err, st_g, e_g);
+            e_g.frequency += f0;
+            const bool lower = best_st == PE3D_OK ||
+                               std::make_tuple(e_g.range_index, e_g.sweep, e_g.frequency, e_g.member) <
+                                   std::make_tuple(best.range_index, best.sweep, best.frequency, best.member);
+            if (lower) { best = e_g; best_st = st_g; }
+            continue;
+        }
+        if (G > 1 && u_final) {                             // this group's slab leaves while the next marches
+            CK(cudaEventRecord(h->copy_ev, s), "event");
+            CK(cudaStreamWaitEvent(h->copy_stream, h->copy_ev, 0), "event");
+            CK(cudaMemcpyAsync(u_final + f0 * slab, h->h_final.as<cplx>() + f0 * slab, (f1 - f0) * slab * sizeof(cplx),
+                               cudaMemcpyDeviceToHost, h->copy_stream), "D2H");
+        }
+    }
+    if (G > 1) CK(cudaStreamSynchronize(h->copy_stream), "sync");
+    if (best_st != PE3D_OK) {
+        if (err) *err = best;
+        return best_st;
+    }
+    if (u_final && G == 1)
+        CK(cudaMemcpyAsync(u_final, h->h_final.ptr, F * slab * sizeof(cplx), cudaMemcpyDeviceToHost, s), "D2H");
     if (tl && !sink.host)
         CK(cudaMemcpyAsync(tl, h->h_tl.ptr, F * S * slab * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
     if (snapshots)
@@ -1072,8 +1162,7 @@ int pe3d_march_medium_host(void* handle, const pe3d_grid* g, const pe3d_coeffs* 
         add(&gen, sizeof(gen));
         if (!(h->graph_exec && key == h->graph_key)) {
             if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
-            if (h->pre_exec) cudaGraphExecDestroy(h->pre_exec);
-            h->graph_exec = h->pre_exec = nullptr;
+            h->graph_exec = nullptr;
             h->graph_key.clear();
             cudaGraph_t graph = nullptr;
             CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "capture");

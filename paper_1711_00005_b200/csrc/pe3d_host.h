@@ -98,7 +98,6 @@ struct Handle {
     // one cached step-loop graph (reused when a march repeats with identical arguments)
     std::vector<unsigned char> graph_key;
     cudaGraphExec_t graph_exec = nullptr;
-    cudaGraphExec_t pre_exec = nullptr;       // pe3d_march_device: the uploads, setup and prologue graph
     // PE3D_FLAG_PROFILE accounting
     double prof_ms[3] = {0, 0, 0};
     int32_t prof_n[3] = {0, 0, 0};
@@ -118,6 +117,18 @@ struct Handle {
     PinBuf params_pin;
     cudaStream_t pro_side = nullptr;
     cudaEvent_t pro_fork = nullptr, pro_join = nullptr;
+    // cached march graphs of pe3d_march_device, most recently used last (a grouped
+    // pe3d_march_host marches several frequency groups per call, one graph pair each)
+    struct MarchGraph {
+        std::vector<unsigned char> key;
+        cudaGraphExec_t pre = nullptr, steps = nullptr;
+        int64_t launches = 0;
+    };
+    static constexpr int MAX_MARCH_GRAPHS = 8;
+    std::vector<MarchGraph> march_graphs;
+    // pe3d_march_host: copy stream for the per-group results and its event
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t copy_ev = nullptr;
 };
 
 // Launch wrapper: in profile mode, bracket each launch with events.

@@ -419,6 +419,25 @@ def test_march_graph_variants_bitwise_equal(monkeypatch, n_steps, stride):
             assert got == ref, switch
 
 
+@pytest.mark.parametrize("groups", ["2", "3", "4"])
+def test_grouped_host_march_bitwise_equal(monkeypatch, groups):
+    """pe3d_march_host marching its frequencies in groups (each group's final slab
+    copied out while the next marches; PE3D_HOST_GROUPS) against one march of all
+    of them: bitwise equal TL, final slabs and clamped counts, with uneven groups
+    (7 frequencies) and TL streamed to page-locked memory."""
+    freqs = (50.0, 80.0, 130.0, 170.0, 260.0, 340.0, 500.0)
+    cfg = configs.build("cfg4", n_range=6, frequencies=freqs, output_stride=2)
+
+    def run():
+        res = march_frequencies(cfg, list(freqs))
+        return [(r.tl_field.tobytes(), r.final_slab.values.tobytes(), r.clamped_samples) for r in res]
+
+    monkeypatch.setenv("PE3D_HOST_GROUPS", "1")
+    ref = run()
+    monkeypatch.setenv("PE3D_HOST_GROUPS", groups)
+    assert run() == ref
+
+
 @pytest.mark.parametrize("shape", ["cfg4", "long"])
 def test_depth_setup_table_bitwise_equal_to_in_kernel_setup(monkeypatch, shape):
     """The per-march depth-sweep setup records (k_depth_setup /
