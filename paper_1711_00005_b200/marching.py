@@ -119,14 +119,36 @@ def _local_column(env, grid: Grid3D, r: float, k0: float) -> np.ndarray:
     return np.ascontiguousarray(n ** 2 - 1.0)
 
 
+def _local_columns(env, grid: Grid3D, r: float, k0s) -> np.ndarray:
+    """_local_column of every frequency, [F][n_depth].  A range-independent
+    LayeredMedium evaluates its k0-independent column once and adds the density
+    term per frequency in one array expression (elementwise the same
+    arithmetic as index_grid, so the same bits)."""
+    from .medium import LayeredMedium
+    medium = getattr(env, "medium", None)
+    if isinstance(medium, LayeredMedium) and medium.range_independent and len(k0s) > 1:
+        n2, dens = medium._column_parts(grid)
+        n2 = np.broadcast_to(n2[0], (len(k0s), grid.n_depth))
+        if dens is not None:
+            k0 = np.asarray(k0s, dtype=np.float64)[:, None]
+            n2 = n2 + dens[0][None, :] / (k0 * k0)
+        return np.ascontiguousarray(np.sqrt(n2) ** 2 - 1.0)
+    return np.ascontiguousarray(np.stack([_local_column(env, grid, r, k0) for k0 in k0s]))
+
+
 def _starter_columns(grid: Grid3D, source, k0s) -> np.ndarray:
     """The Gaussian starter of every frequency as one depth column each
     (azimuth independent, surface zero; ref environment.py:270-284) -- the
-    march reads them with PE3D_FLAG_STARTER_COLUMN."""
-    cols = np.empty((len(k0s), grid.n_depth), dtype=np.complex128)
-    for i, k0 in enumerate(k0s):
-        cols[i] = gaussian_starter_column(grid, source, k0)
-    return cols
+    march reads them with PE3D_FLAG_STARTER_COLUMN.  One array expression
+    for all frequencies: elementwise the arithmetic of gaussian_starter_column."""
+    if len(k0s) == 0:
+        return np.empty((0, grid.n_depth), dtype=np.complex128)
+    gaussian_starter_column(grid, source, k0s[0])              # validates the source depth
+    z = grid.depths()
+    k0 = np.asarray(k0s, dtype=np.float64)[:, None]
+    cols = (np.sqrt(k0) * np.exp(-0.5 * k0 * k0 * (z - source.depth) ** 2)).astype(np.complex128)
+    cols[:, 0] = 0.0
+    return np.ascontiguousarray(cols)
 
 
 def range_step(state: MarchState, device: int = 0) -> MarchState:
@@ -211,8 +233,7 @@ def march_frequencies(config, frequencies: Sequence[float], n_steps: Optional[in
         chunk = max(1, min(F, BATCH_BYTES // max(per_freq, 1)))
         for lo in range(0, F, chunk):
             hi = min(F, lo + chunk)
-            local = np.ascontiguousarray(np.stack([_local_column(env, grid, grid.r_start, k0)
-                                                   for k0 in k0s[lo:hi]]))
+            local = _local_columns(env, grid, grid.r_start, k0s[lo:hi])
             g = _grid_params(grid, hi - lo, steps, stride, 0, grid.r_start, flags | _native.FLAG_STARTER_COLUMN)
             cf = _native.make_coeffs(k0s[lo:hi], coeffs[lo:hi])
             _native.call("pe3d_march_host", h, g, cf, _native.ptr(local), _native.ptr(cols[lo:hi]),
