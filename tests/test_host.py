@@ -178,3 +178,23 @@ class TestErrorMapping:
 
     def test_ok(self):
         errors.raise_from_record(0, self.Rec())
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg4", "cfg5"])
+def test_batched_host_columns_bitwise_equal_to_per_frequency(name):
+    """The drop-in's host inputs for a batch of frequencies (starter columns and
+    medium columns as one array expression each) equal, bit for bit, the
+    per-frequency functions they replace (gaussian_starter_column, ref
+    environment.py:270-284; the local term n^2 - 1 of the medium column)."""
+    from paper_1711_00005_b200.environment import gaussian_starter_column, wavenumber
+    from paper_1711_00005_b200.marching import _local_column, _local_columns, _starter_columns
+    cfg = configs.build(name, n_range=5)
+    grid, env, source, _ = cfg
+    freqs = list(source.frequencies)[:7] + [f * 1.37 for f in source.frequencies[:2]]
+    k0s = [wavenumber(f, env.c0) for f in freqs]
+    got = _starter_columns(grid, source, k0s)
+    want = np.stack([gaussian_starter_column(grid, source, k0) for k0 in k0s])
+    assert got.tobytes() == want.tobytes()
+    got = _local_columns(env, grid, grid.r_start, k0s)
+    want = np.stack([_local_column(env, grid, grid.r_start, k0) for k0 in k0s])
+    assert got.tobytes() == want.tobytes()
