@@ -267,9 +267,10 @@ PE3D_API int pe3d_last_launches(void* handle, int64_t* launches);
 
 /*
  * pe3d_profile_launches -- the individual CUDA-event times (ms, launch order)
- * of kernel class `cls` in the last PE3D_FLAG_PROFILE march on this handle;
- * writes min(count, capacity) entries and the full count to *count
- * (measurement only: steady-state launches for the bench's roofline).
+ * of kernel class `cls` (0 depth sweep, 1 azimuth sweep, 2 other, 3 the carry
+ * and edge fix of a split-ring azimuth sweep) in the last PE3D_FLAG_PROFILE
+ * march on this handle; writes min(count, capacity) entries and the full count
+ * to *count (measurement only: steady-state launches for the bench's roofline).
  */
 PE3D_API int pe3d_profile_launches(void* handle, int32_t cls, double* ms, int32_t capacity, int32_t* count);
 

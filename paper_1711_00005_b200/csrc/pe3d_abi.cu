@@ -37,7 +37,40 @@ struct MarchPlan {
     // column starter: the prologue leaves the first temp as one column per frequency
     // ([F][n_tiles][8]) and the first depth sweep reads it (null: the full field)
     pe3d::cplx* temp_col;
+    // split rings (pe3d_ring.cu k_sring_*): tables [step][F][sring_table_elems], segment
+    // totals, and per step the corrected span (0: that step runs the cluster kernel)
+    pe3d::cplx *sr_coef, *sr_tot;
+    const int* sr_span;
 };
+
+// Split-ring plan of a march: per step, the number of points from each segment
+// edge whose next temp needs the carry correction (k_sring_fix), from the largest
+// |rho| of the step's frequencies: the dropped terms are below 1e-22 of the
+// carries.  0 (the exact cluster kernel) where the span exceeds 0.17 of the
+// segment: the segmented sweep + carry + fix beat the cluster kernel (cfg5:
+// ~105 + ~4 + fix vs 142 us) only while the fix rewrites at most ~1/3 of the field.
+static std::vector<int> sring_spans(const pe3d_grid* g, const std::vector<pe3d::FreqDev>& fd, int ns) {
+    std::vector<int> span(g->n_steps, 0);
+    for (int s = 0; s < g->n_steps; ++s) {
+        const double r_new = g->r_start + double(g->first_index + s + 1) * g->delta_r;
+        double rmax = 0.0;
+        for (const auto& d : fd) {
+            const double sc = pe3d::azimuth_scale(d.k0, r_new, g->delta_theta);
+            const cplx diag = pe3d::csub(pe3d::cone(), pe3d::crmul(sc, pe3d::crmul(2.0, d.cy_lhs)));
+            const cplx off = pe3d::crmul(sc, d.cy_lhs);
+            if (off.re == 0.0 && off.im == 0.0) continue;          // rho = 0
+            const cplx tq = pe3d::crmul(0.5, pe3d::cneg(pe3d::cdiv(diag, off)));
+            cplx sq = pe3d::csqrt(pe3d::csub(pe3d::cmul(tq, tq), pe3d::cone()));
+            if (tq.re * sq.re + tq.im * sq.im < 0.0) sq = pe3d::cneg(sq);
+            rmax = std::max(rmax, pe3d::cabs(pe3d::crecip(pe3d::cadd(tq, sq))));
+        }
+        if (rmax == 0.0) { span[s] = 1; continue; }
+        if (!(rmax < 1.0 - 1e-9)) continue;
+        const double need = (std::log(1e-22) + std::log(1.0 - rmax * rmax)) / std::log(rmax) + 2.0;
+        if (need <= 0.17 * ns) span[s] = std::max(1, int(std::ceil(need)));
+    }
+    return span;
+}
 
 // Number of concurrent step-loop chains.  Frequencies are independent, so a
 // march runs disjoint frequency groups as parallel graph branches: each
@@ -200,7 +233,20 @@ cudaError_t enqueue_group(Handle* h, const pe3d_grid* g, const MarchPlan& p, int
             ea.sample = k % sink->R;
         }
         const cplx* tab = h->ring_tab.as<cplx>() + (int64_t(s) * c.n_freq + f0) * E;
-        e = prof.run(1, [&] { return pe3d::launch_azimuth_scan(cg, B, A, tab, r_new, ea); });
+        const bool split_ring = p.sr_span && p.sr_span[s] > 0 && !ea.tl && !ea.snap && !ea.final_out;
+        if (split_ring) {
+            // segments with zero carries, then the exact carries and the edge fix of the next temp
+            const int nseg = c.n_theta / pe3d::sring_segment(c.n_theta);
+            const int64_t rows = int64_t(c.n_tiles) * 8;
+            pe3d::LaunchCtx cs = cg;
+            cs.sring_tot = p.sr_tot + int64_t(f0) * nseg * 2 * rows;
+            const cplx* coef = p.sr_coef + (int64_t(s) * c.n_freq + f0) * pe3d::sring_table_elems(c.n_theta);
+            e = prof.run(1, [&] { return pe3d::launch_azimuth_seg(cs, B, A, tab, ea); });
+            if (e == cudaSuccess)
+                e = prof.run(3, [&] { return pe3d::launch_sring_fix(cs, A, cs.sring_tot, coef, p.sr_span[s]); });
+        } else {
+            e = prof.run(1, [&] { return pe3d::launch_azimuth_scan(cg, B, A, tab, r_new, ea); });
+        }
         if (e != cudaSuccess) return e;
         if (stream_tl) {
             e = tl_after(h, *sink, chain, k, f0, nf, oe, d_tl, st);
@@ -480,6 +526,19 @@ static int march_device_impl(void* handle, const pe3d_grid* g, const pe3d_coeffs
     const bool ring_tables = !p.serial && g->topology == PE3D_PERIODIC && g->n_steps > 0;
     if (ring_tables) CK(h->ring_tab.ensure(int64_t(g->n_steps) * F * pe3d::ring_table_elems(NT) * sizeof(cplx)),
                         "alloc ring table");
+    // split rings for cluster-sized rings (cfg5): steps whose carries only reach the
+    // segment edges run the segmented sweep + carry + edge fix instead of the cluster kernel
+    std::vector<int> sr_span;
+    const int sr_ns = ring_tables && !getenv("PE3D_NO_SPLIT_RING") ? pe3d::sring_segment(NT) : 0;
+    if (sr_ns) {
+        sr_span = sring_spans(g, fd, sr_ns);
+        const int nseg = NT / sr_ns;
+        CK(h->sr_coef.ensure(int64_t(g->n_steps) * F * pe3d::sring_table_elems(NT) * sizeof(cplx)), "alloc split ring");
+        CK(h->sr_tot.ensure(int64_t(F) * nseg * 2 * n_tiles * 8 * sizeof(cplx)), "alloc split ring");
+        p.sr_coef = h->sr_coef.as<cplx>();
+        p.sr_tot = h->sr_tot.as<cplx>();
+        p.sr_span = sr_span.data();
+    }
 
     const cplx* local = reinterpret_cast<const cplx*>(d_local);
     Prof prof{h, (g->flags & PE3D_FLAG_PROFILE) != 0, stream, {}};
@@ -489,9 +548,12 @@ static int march_device_impl(void* handle, const pe3d_grid* g, const pe3d_coeffs
                         : prof.run(2, [&] { return pe3d::launch_factor_depth(cs, local, NZ, g->first_index + 1); });
     };
     auto enqueue_ring_setup = [&](pe3d::LaunchCtx& cs) -> cudaError_t {
-        return !ring_tables ? cudaSuccess
-                            : prof.run(2, [&] { return pe3d::launch_ring_setup(cs, h->ring_tab.as<cplx>(), g->n_steps,
-                                                                               g->first_index, g->r_start, g->delta_r); });
+        if (!ring_tables) return cudaSuccess;
+        cudaError_t e = prof.run(2, [&] { return pe3d::launch_ring_setup(cs, h->ring_tab.as<cplx>(), g->n_steps,
+                                                                        g->first_index, g->r_start, g->delta_r); });
+        if (e == cudaSuccess && p.sr_coef)
+            e = prof.run(2, [&] { return pe3d::launch_sring_setup(cs, p.sr_coef, h->ring_tab.as<cplx>(), g->n_steps); });
+        return e;
     };
     auto enqueue_setup = [&](pe3d::LaunchCtx& cs) -> cudaError_t {
         cudaError_t e = enqueue_depth_setup(cs);
@@ -554,9 +616,10 @@ static int march_device_impl(void* handle, const pe3d_grid* g, const pe3d_coeffs
         add(coeffs, sizeof(pe3d_coeffs) * F);
         add(ptrs, sizeof(ptrs));
         add(&stream, sizeof(stream));
-        const void* tabs[7] = {h->w_abs.ptr, h->fdev.ptr, h->loc_tab.ptr, h->err.ptr, h->ring_tab.ptr, p.ctx.k1_tab,
-                               p.temp_col};
+        const void* tabs[10] = {h->w_abs.ptr, h->fdev.ptr, h->loc_tab.ptr, h->err.ptr, h->ring_tab.ptr, p.ctx.k1_tab,
+                                p.temp_col, p.sr_coef, p.sr_tot, nullptr};
         add(tabs, sizeof(tabs));
+        if (!sr_span.empty()) add(sr_span.data(), sr_span.size() * sizeof(int));
         const int chains = step_chains(p.ctx, false);
         add(&chains, sizeof(chains));
         // any workspace reallocation (also by other entry points on this handle)
@@ -568,7 +631,7 @@ static int march_device_impl(void* handle, const pe3d_grid* g, const pe3d_coeffs
         for (const char* name : {"PE3D_NO_PDL", "PE3D_CLUSTER_L", "PE3D_DEPTH_NO_CLUSTER", "PE3D_RING_BLOCK",
                                  "PE3D_RING_CPASYNC", "PE3D_DEPTH_NO_SPLIT", "PE3D_FACTOR_SERIAL",
                                  "PE3D_PREPARE_STAGED", "PE3D_PARAMS_MEMCPY", "PE3D_FINAL_STORES",
-                                 "PE3D_FIRST_STEP_FIELD"}) {
+                                 "PE3D_FIRST_STEP_FIELD", "PE3D_NO_SPLIT_RING"}) {
             const char* v = getenv(name);
             const std::string val = v ? std::string("=") + v : std::string("-");
             add(val.data(), val.size() + 1);
@@ -1204,7 +1267,7 @@ int pe3d_last_launches(void* handle, int64_t* launches) {
 
 int pe3d_profile_launches(void* handle, int32_t cls, double* ms, int32_t capacity, int32_t* count) {
     Handle* h = static_cast<Handle*>(handle);
-    if (!h || cls < 0 || cls > 2 || capacity < 0) return PE3D_BAD_ARGUMENT;
+    if (!h || cls < 0 || cls > 3 || capacity < 0) return PE3D_BAD_ARGUMENT;
     const std::vector<double>& v = h->prof_list[cls];
     if (count) *count = int32_t(v.size());
     for (int32_t i = 0; ms && i < capacity && i < int32_t(v.size()); ++i) ms[i] = v[i];

@@ -82,12 +82,14 @@ struct Handle {
     DevBuf sp_tot, sp_aq, sp_pa, sp_cd;
     // column starter: the first temp as one column per frequency (MarchPlan::temp_col)
     DevBuf col_tab;
+    // split rings: per-(step, frequency) tables, segment totals
+    DevBuf sr_coef, sr_tot;
     // every workspace buffer (release, allocation generation)
     std::vector<DevBuf*> buffers() {
         return {&field_a, &field_b, &field_c, &loc_tab, &mul_tab, &fdev, &w_abs, &err, &k1_tab, &az_cp, &az_inv,
                 &az_q, &az_ring, &fail_row, &fail_mag, &ring_tab, &h_local, &h_local2, &h_u0, &h_final, &h_tl,
                 &h_snap, &h_clamped, &sb_in, &sb_x, &sb_cp, &sb_inv, &sb_y, &sb_q, &med_prof, &med_lat, &med_local,
-                &slab_flags, &sp_tot, &sp_aq, &sp_pa, &sp_cd, &col_tab};
+                &slab_flags, &sp_tot, &sp_aq, &sp_pa, &sp_cd, &col_tab, &sr_coef, &sr_tot};
     }
     // changes whenever any workspace buffer was reallocated since the last call
     uint64_t alloc_generation() {
@@ -99,9 +101,11 @@ struct Handle {
     std::vector<unsigned char> graph_key;
     cudaGraphExec_t graph_exec = nullptr;
     // PE3D_FLAG_PROFILE accounting
-    double prof_ms[3] = {0, 0, 0};
-    int32_t prof_n[3] = {0, 0, 0};
-    std::vector<double> prof_list[3];     // per launch, in launch order
+    // classes: 0 depth sweep, 1 azimuth sweep, 2 other, 3 the split-ring carry and
+    // edge fix (part of the azimuth sweep of a split-ring step)
+    double prof_ms[4] = {0, 0, 0, 0};
+    int32_t prof_n[4] = {0, 0, 0, 0};
+    std::vector<double> prof_list[4];     // per launch, in launch order
     // kernels launched by the last march (graph replays included)
     int64_t graph_launches = 0, last_launches = 0;
     // concurrent step-loop chains over disjoint frequency groups
@@ -152,7 +156,7 @@ struct Prof {
     }
     void collect() {
         if (!on) return;
-        for (int k = 0; k < 3; ++k) { h->prof_ms[k] = 0; h->prof_n[k] = 0; h->prof_list[k].clear(); }
+        for (int k = 0; k < 4; ++k) { h->prof_ms[k] = 0; h->prof_n[k] = 0; h->prof_list[k].clear(); }
         for (auto& p : ev) {
             float ms = 0;
             cudaEventSynchronize(p.second.second);

@@ -114,6 +114,145 @@ __global__ void k_ring_setup(cplx* __restrict__ table, const FreqDev* __restrict
     T[5] = b2;
 }
 
+// ------------------------------------------------------------ split rings
+// A ring of nseg segments of NS points solved segment by segment with zero
+// carries (k_azimuth_tma SEG: all SMs, no cluster) and chained exactly
+// afterwards.  With w = w0 + rho^(o+1) c inside segment s (c: w at the point
+// before it) and x = z + A_o c + B_o d (d: x at the point after it),
+//   A_o = rho^(o+1) S_(NS-o),  B_o = rho^(NS-o),  S_n = sum_(t<n) rho^(2t),
+// the carries follow from the segments' zero-carry totals W_s (w0 at the last
+// point) and X0_s (z at the first point): X_s = X0_s + gamma c_s with
+// gamma = rho S_NS, and the cyclic chains of the cluster kernel.  The next
+// temp b1 x + b2 (x+ + x-) of segment s then differs from the one the segment
+// wrote (zero neighbours outside it) by alpha_o c_s + beta_o d_s, plus b2 times
+// the true left neighbour at o = 0 (alpha, beta below; B_NS = 1 carries the
+// right neighbour d_s).  |rho| < 1, so alpha and beta decay away from the
+// segment edges: only the points within `span` of an edge are corrected
+// (k_sring_fix, which also chains the carries; the host picks per step either
+// this or the cluster kernel).
+//
+// Per (step, frequency) table (SRING_HDR + 2 NS entries):
+//   [0] rho, [1] 1/(1 - rho^N), [2] gamma, [3] A_0, [4] B_0, [5] b2,
+//   [6 + j] Rs^j (Rs = rho^NS, j < 16), then alpha[NS], beta[NS].
+constexpr int SRING_HDR = 22;
+__host__ __device__ constexpr int sring_elems(int ns) { return SRING_HDR + 2 * ns; }
+
+__global__ void k_sring_setup(cplx* __restrict__ coef, const cplx* __restrict__ ring_tab, int E, int n_items,
+                              int ns) {
+    const int gid = blockIdx.x * blockDim.x + threadIdx.x;     // (step, frequency)
+    if (gid >= n_items) return;
+    const cplx* T = ring_tab + int64_t(gid) * E;
+    cplx* C = coef + int64_t(gid) * sring_elems(ns);
+    const cplx rho = T[0], b1 = T[4], b2 = T[5];
+    cplx* al = C + SRING_HDR;
+    cplx* be = al + ns;
+    const cplx r2 = cmul(rho, rho);
+    // pass 1, o = ns-1 .. 0 (n = ns - o = 1 .. ns): S_n into al[o], B_o = rho^n into be[o]
+    cplx S = czero(), r2p = cone(), bp = cone();
+    for (int o = ns - 1; o >= 0; --o) {
+        S = cadd(S, r2p);
+        r2p = cmul(r2p, r2);
+        bp = cmul(bp, rho);
+        al[o] = S;
+        be[o] = bp;
+    }
+    const cplx S_ns = S, Rs = be[0];                           // S_NS, rho^NS
+    // pass 2: A_o = rho^(o+1) S_(ns-o)
+    cplx ap = rho;
+    for (int o = 0; o < ns; ++o) {
+        al[o] = cmul(ap, al[o]);
+        ap = cmul(ap, rho);
+    }
+    C[0] = rho;
+    C[1] = T[2];
+    C[2] = cmul(rho, S_ns);
+    C[3] = al[0];
+    C[4] = be[0];
+    C[5] = b2;
+    cplx rj = cone();
+    for (int j = 0; j < 16; ++j) { C[6 + j] = rj; rj = cmul(rj, Rs); }
+    // pass 3: alpha_o = b1 A_o + b2 (A_(o+1) + A_(o-1)), beta likewise with B_ns = 1
+    cplx a_prev = czero(), b_prev = czero();
+    for (int o = 0; o < ns; ++o) {
+        const cplx a = al[o], b = be[o];
+        const cplx a_next = o + 1 < ns ? al[o + 1] : czero();
+        const cplx b_next = o + 1 < ns ? be[o + 1] : cone();
+        al[o] = cfma(b1, a, cmul(b2, cadd(a_next, a_prev)));
+        be[o] = cfma(b1, b, cmul(b2, cadd(b_next, b_prev)));
+        a_prev = a;
+        b_prev = b;
+    }
+}
+
+// The edge fix of a split-ring step, one CTA of 128 threads per (frequency,
+// tile, segment s):
+//  1. the exact carries of the tile's 8 rows, a half-warp per row with lane j
+//     holding segment j's zero-carry totals (tot [F][nseg][2][n_rows]: W, X0);
+//     the segment chains are 4-level scans:
+//       c_j = sum_(j'<j) Rs^(j-1-j') W_j' + Rs^j wend,  X_j = X0_j + gamma c_j,
+//       d_j = sum_(j'>j) Rs^(j'-j-1) X_j' + Rs^(nseg-1-j) xstart
+//     (wend, xstart: the cyclic closures), and e_j = c_j + rho x_first(j);
+//  2. temp += alpha_o c_s + beta_o d_s (+ b2 e_s at o = 0) on the 2 span lines
+//     of the segment's edges, read-modify-write.
+// Every CTA of a tile recomputes its rows' chains (128 threads, a few hundred
+// FMAs) instead of a separate carry kernel and its global round trip (8.4 us).
+__global__ void __launch_bounds__(128) k_sring_fix(cplx* __restrict__ temp, const cplx* __restrict__ tot,
+                                                   const cplx* __restrict__ coef_step, int n_tiles, int n_theta,
+                                                   int nseg, int ns, int span) {
+    __shared__ cplx sc[3][8];
+    const int b = blockIdx.x;
+    const int s = b % nseg, ft = b / nseg;
+    const int tile = ft % n_tiles, f = ft / n_tiles;
+    const int n_rows = n_tiles * 8;
+    const int lane = threadIdx.x & 31, j = lane & 15, row = threadIdx.x >> 4;
+    const cplx* C = coef_step + int64_t(f) * sring_elems(ns);
+    {
+        const cplx rho = C[0], inv_wrap = C[1], gamma = C[2], B0 = C[4], b2 = C[5];
+        const bool seg = j < nseg;
+        const int l = tile * 8 + row;
+        const cplx* T = tot + (int64_t(f) * nseg + j) * 2 * n_rows + l;
+        const cplx W = seg ? ldc(T) : czero();
+        const cplx X0 = seg ? ldc(T + n_rows) : czero();
+        cplx I = W;                                            // sum_(j'<=j) Rs^(j-j') W_j'
+#pragma unroll
+        for (int d = 1; d < 16; d <<= 1) {
+            const cplx t = shfl_up(I, d);
+            if (j >= d) I = cfma(C[6 + d], t, I);
+        }
+        const cplx wend = cmul(shfl_idx(I, (lane & 16) + nseg - 1), inv_wrap);
+        cplx ip = shfl_up(I, 1);
+        if (j == 0) ip = czero();
+        const cplx c = seg ? cfma(C[6 + (seg ? j : 0)], wend, ip) : czero();
+        const cplx X = cfma(gamma, c, X0);
+        cplx J = X;                                            // sum_(j'>=j) Rs^(j'-j) X_j'
+#pragma unroll
+        for (int d = 1; d < 16; d <<= 1) {
+            const cplx t = shfl_down(J, d);
+            if (j + d < nseg) J = cfma(C[6 + d], t, J);
+        }
+        const cplx xstart = cmul(shfl_idx(J, lane & 16), inv_wrap);
+        cplx jn = shfl_down(J, 1);
+        if (j + 1 >= nseg) jn = czero();
+        const cplx dv = seg ? cfma(C[6 + (seg ? nseg - 1 - j : 0)], xstart, jn) : czero();
+        if (j == s) {
+            sc[0][row] = c;
+            sc[1][row] = dv;
+            sc[2][row] = cmul(b2, cfma(rho, cfma(B0, dv, X), c));   // b2 (c + rho x_first)
+        }
+    }
+    __syncthreads();
+    const cplx* A = C + SRING_HDR;
+    cplx* base = temp + ((int64_t(f) * n_tiles + tile) * n_theta + int64_t(s) * ns) * 8;
+    for (int e = threadIdx.x; e < 16 * span; e += blockDim.x) {
+        const int jj = e >> 3, r = e & 7;
+        const int o = jj < span ? jj : ns - 2 * span + jj;     // [0, span) then [ns - span, ns)
+        cplx dt = cfma(ldc(A + o), sc[0][r], cmul(ldc(A + ns + o), sc[1][r]));
+        if (o == 0) dt = cadd(dt, sc[2][r]);
+        cplx* p = base + o * 8 + r;
+        *p = cadd(*p, dt);
+    }
+}
+
 // Given u on this thread's azimuth chunk of RT depth rows, write the TL
 // sample / snapshot / final slab if requested and the next step's
 // temp = u + cy_rhs * s_theta * d2_theta(u)  (ref operators.py:105-122,
@@ -1017,13 +1156,14 @@ __device__ __forceinline__ int tma_slot(int q, int k, int r) { return ((k * 32 +
 template <int RT>
 __host__ __device__ constexpr int ring_tma_threads() { return 32 * (8 / RT + 1); }
 
-template <int L, int RT, int S, bool CLUSTER, int MINB, bool CORR = false>
+template <int L, int RT, int S, bool CLUSTER, int MINB, bool CORR = false, bool SEG = false>
 __global__ void __launch_bounds__(ring_tma_threads<RT>(), MINB)
 k_azimuth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ CUtensorMap tm_dst,
               const cplx* __restrict__ table, int E, int tab_elems, int n_theta, int n_tiles, int n_depth,
               int64_t total_items, int n_units, EpilogueArgs ea, const cplx* __restrict__ sp_cd,
               const cplx* __restrict__ sp_aq, const cplx* __restrict__ sp_pa, int split, int tile_perm,
-              const __grid_constant__ CUtensorMap tm_fin, int fin_tma) {
+              const __grid_constant__ CUtensorMap tm_fin, int fin_tma, cplx* __restrict__ seg_tot) {
+    static_assert(!SEG || (!CLUSTER && RT == 1), "segmented rings: plain kernel, one row per warp");
     namespace cg = cooperative_groups;
     constexpr int NW = 8 / RT;                      // consumer warps; warp NW is the TMA producer
     constexpr int NS = 32 * L;                      // segment length
@@ -1082,8 +1222,9 @@ k_azimuth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant_
             griddep_wait();                         // the field belongs to the previous sweep until here
             const unsigned tab_bytes = unsigned(tab_elems) * unsigned(sizeof(cplx));
             int span_fs = -1, a_span = 0, q_span = 0;
+            const int nseg = SEG ? n_theta / NS : 1;
             auto load = [&](int n, int slot) {
-                const int item = first + n * G;
+                const int item = (first + n * G) / nseg, seg = SEG ? (first + n * G) % nseg : s;
                 const int f = item / n_tiles;
                 const int titem = f * n_tiles + (item - f * n_tiles) * tile_perm % n_tiles;   // permuted tile
                 bool corr_item = false;
@@ -1103,12 +1244,12 @@ k_azimuth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant_
                 }
                 const unsigned corr_bytes = corr_item ? CORRE * unsigned(sizeof(cplx)) : 0u;
                 mbar_expect_tx(&full[slot], ITEM_BYTES + tab_bytes + corr_bytes);
-                tma_load_5d(stage + slot * ITEM, &tm_src, 0, 0, 0, s, titem, &full[slot]);
+                tma_load_5d(stage + slot * ITEM, &tm_src, 0, 0, 0, seg, titem, &full[slot]);
                 bulk_load(tabs + slot * tab_pad, table + int64_t(f) * E, tab_bytes, &full[slot]);
                 if (CORR && corr_item) {
                     const int tile = titem - f * n_tiles;
                     const int sub = tile / (n_tiles / split);
-                    const cplx* cd = sp_cd + (int64_t(f) * split + sub) * 2 * n_theta + s * NS;
+                    const cplx* cd = sp_cd + (int64_t(f) * split + sub) * 2 * n_theta + seg * NS;
                     cplx* dstc = corr + slot * CORRE;
                     bulk_load(dstc, cd, NS * unsigned(sizeof(cplx)), &full[slot]);
                     bulk_load(dstc + NS, cd + n_theta, NS * unsigned(sizeof(cplx)), &full[slot]);
@@ -1126,8 +1267,9 @@ k_azimuth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant_
                     tma_store_5d(&tm_fin, 0, 0, 0, (item - f * n_tiles) * tile_perm % n_tiles, f, stage + slot * ITEM);
                     bulk_commit();
                 } else if (ea.write_temp) {
-                    const int item = first + n * G, f = item / n_tiles;
-                    tma_store_5d(&tm_dst, 0, 0, 0, s, f * n_tiles + (item - f * n_tiles) * tile_perm % n_tiles,
+                    const int item = (first + n * G) / nseg, seg = SEG ? (first + n * G) % nseg : s;
+                    const int f = item / n_tiles;
+                    tma_store_5d(&tm_dst, 0, 0, 0, seg, f * n_tiles + (item - f * n_tiles) * tile_perm % n_tiles,
                                  stage + slot * ITEM);
                     bulk_commit();
                 }
@@ -1149,8 +1291,9 @@ k_azimuth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant_
             if (lane < CL) st_async_cplx(mapa_shared(smem_addr(table_ + s * 8 + row), lane), val,
                                          mapa_shared(smem_addr(bar), lane));
         };
+        const int nseg = SEG ? n_theta / NS : 1;
         for (int n = 0; n < N; ++n) {
-            const int item = first + n * G;
+            const int item = (first + n * G) / nseg, seg = SEG ? (first + n * G) % nseg : 0;
             const int f = item / n_tiles, tile = (item - f * n_tiles) * tile_perm % n_tiles;
             const int slot = n % S;
             const int buf = n & 1;
@@ -1165,7 +1308,7 @@ k_azimuth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant_
             const cplx* pw = T + RING_HDR;          // rho^k, k = 0..L
             const cplx* qp = pw + L + 1;            // R^j, j = 0..32 (cluster: R^(32k) = qp[32k])
             const cplx rho = T[0], scale = T[1], inv_wrap = T[2], b1 = T[4], b2 = T[5];
-            const bool diagonal = T[3].re != 0.0;
+            const bool diagonal = !SEG && T[3].re != 0.0;   // SEG: rho = 0 runs the general recurrences
             cplx* stg = stage + slot * ITEM;
             cplx v[RT][L];
 #pragma unroll
@@ -1219,6 +1362,17 @@ k_azimuth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant_
                     const cplx cw = cfma(qp[32 * s], cmul(wend, inv_wrap), cin);   // w_(mseg-1), cyclic
 #pragma unroll
                     for (int h = 0; h < RT; ++h) carry_w[h] = shfl_idx(cw, 16 * h);
+                } else if constexpr (SEG) {
+                    // a segment of a longer ring with zero carries: its total W leaves for
+                    // k_sring_fix, which chains the segments exactly
+#pragma unroll
+                    for (int h = 0; h < RT; ++h) carry_w[h] = czero();
+                    const cplx W = shfl_idx(Y[0], 31);
+                    if (lane == 0) {
+                        const int l = tile * 8 + warp;
+                        const bool live = l + ea.row_offset != 0 && l < n_depth;
+                        stc(seg_tot + ((int64_t(f) * nseg + seg) * 2) * (n_tiles * 8) + l, live ? W : czero());
+                    }
                 } else {
 #pragma unroll
                     for (int h = 0; h < RT; ++h) carry_w[h] = cmul(shfl_idx(Y[h], 31), inv_wrap);   // cyclic closure
@@ -1265,6 +1419,15 @@ k_azimuth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant_
                     const cplx cx = cfma(qp[32 * (CL - 1 - s)], cmul(x0, inv_wrap), dn);   // x_(mseg+NS), cyclic
 #pragma unroll
                     for (int h = 0; h < RT; ++h) carry_x[h] = shfl_idx(cx, 16 * h);
+                } else if constexpr (SEG) {
+#pragma unroll
+                    for (int h = 0; h < RT; ++h) carry_x[h] = czero();
+                    const cplx X0 = shfl_idx(X[0], 0);     // zero-carry solution at the segment's first point
+                    if (lane == 0) {
+                        const int l = tile * 8 + warp;
+                        const bool live = l + ea.row_offset != 0 && l < n_depth;
+                        stc(seg_tot + ((int64_t(f) * nseg + seg) * 2 + 1) * (n_tiles * 8) + l, live ? X0 : czero());
+                    }
                 } else {
 #pragma unroll
                     for (int h = 0; h < RT; ++h) carry_x[h] = cmul(shfl_idx(X[h], 0), inv_wrap);    // cyclic closure
@@ -1337,6 +1500,10 @@ k_azimuth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant_
                     if constexpr (CLUSTER) {
                         if (lane == 0) prev = prev_edge[h];
                         if (lane == 31) next = next_edge[h];
+                    } else if constexpr (SEG) {
+                        // neighbours outside the segment enter later (k_sring_fix)
+                        if (lane == 0) prev = czero();
+                        if (lane == 31) next = czero();
                     } else {
                         const cplx wrap_prev = shfl_idx(v[h][L - 1], 31), wrap_next = shfl_idx(v[h][0], 0);
                         if (lane == 0) prev = wrap_prev;
@@ -1686,14 +1853,16 @@ int cached_occupancy(const void* kern, size_t bytes, int cluster, int nthr, cuda
     return v;
 }
 
-template <int L, int RT, int S, bool CLUSTER, int MINB = 1, bool CORR = false>
+template <int L, int RT, int S, bool CLUSTER, int MINB = 1, bool CORR = false, bool SEG = false>
 static cudaError_t launch_tma_ring(const LaunchCtx& c, const cplx* src, cplx* dst, const cplx* table_step, int E,
                                    const EpilogueArgs& ea) {
     constexpr int NS = 32 * L, NW = 8 / RT;
     const int CL = c.n_theta / NS;
-    if (c.n_theta % NS != 0 || (CLUSTER ? (CL < 2 || CL > 16) : CL != 1)) return cudaErrorNotSupported;
+    if (c.n_theta % NS != 0 || (CLUSTER ? (CL < 2 || CL > 16) : (SEG ? (CL < 2 || CL > 16) : CL != 1)))
+        return cudaErrorNotSupported;
+    if (SEG && (!c.sring_tot || ea.tl || ea.snap || ea.final_out)) return cudaErrorNotSupported;
     const int64_t tiles = int64_t(c.n_freq) * c.n_tiles;
-    const int64_t items = tiles;
+    const int64_t items = SEG ? tiles * CL : tiles;
     if (items > 0x7fffffff) return cudaErrorNotSupported;
     CUtensorMap tm_src, tm_dst;
     if (!ring_tensor_map(&tm_src, src, c.n_theta, L, tiles) || !ring_tensor_map(&tm_dst, dst, c.n_theta, L, tiles))
@@ -1707,7 +1876,7 @@ static cudaError_t launch_tma_ring(const LaunchCtx& c, const cplx* src, cplx* ds
                          sizeof(uint64_t) * (2 * S + (CLUSTER ? 4 * NW : 0)) + sizeof(int) * S;
     if (bytes > 227 * 1024) return cudaErrorNotSupported;
     if (CORR && (c.split < 2 || c.n_tiles % c.split != 0 || !c.sp_cd || !c.sp_aq)) return cudaErrorNotSupported;
-    auto kern = k_azimuth_tma<L, RT, S, CLUSTER, MINB, CORR>;
+    auto kern = k_azimuth_tma<L, RT, S, CLUSTER, MINB, CORR, SEG>;
     cudaError_t e = set_smem(kern, bytes);
     if (e != cudaSuccess) return e;
     const int nthr = ring_tma_threads<RT>();
@@ -1738,7 +1907,7 @@ static cudaError_t launch_tma_ring(const LaunchCtx& c, const cplx* src, cplx* ds
         }
         return launch_pdl(c.pdl != 0, kern, dim3(grid), dim3(nthr), bytes, c.stream, tm_src, tm_dst, table_step, E,
                           tab_elems, c.n_theta, c.n_tiles, c.n_depth, items, grid, ea, (const cplx*)c.sp_cd,
-                          (const cplx*)c.sp_aq, (const cplx*)c.sp_pa, c.split, 1, tm_fin, fin_tma);
+                          (const cplx*)c.sp_aq, (const cplx*)c.sp_pa, c.split, 1, tm_fin, fin_tma, c.sring_tot);
     } else {
         if (CL > 8) {
             e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -1772,7 +1941,7 @@ static cudaError_t launch_tma_ring(const LaunchCtx& c, const cplx* src, cplx* ds
         }
         return cudaLaunchKernelEx(&cfg, kern, tm_src, tm_dst, table_step, E, tab_elems, c.n_theta, c.n_tiles,
                                   c.n_depth, items, per, ea, (const cplx*)c.sp_cd, (const cplx*)c.sp_aq,
-                                  (const cplx*)c.sp_pa, c.split, perm, tm_dst, 0);
+                                  (const cplx*)c.sp_pa, c.split, perm, tm_dst, 0, (cplx*)nullptr);
     }
 }
 
@@ -1843,6 +2012,19 @@ static cudaError_t launch_cluster_ring(const LaunchCtx& c, const cplx* src, cplx
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kern, src, dst, table_step, E, c.fdev, c.n_theta, c.n_tiles, c.n_depth, items, per,
                               r_new, c.delta_theta, ea);
+}
+
+// Split-ring azimuth sweep of a cluster-sized ring (see k_sring_setup): every
+// segment solved with zero carries; c.sring_tot receives the segment totals.
+cudaError_t launch_azimuth_seg(const LaunchCtx& c, const cplx* src, cplx* dst, const cplx* table_step,
+                               const EpilogueArgs& ea) {
+    const RingPlan plan = ring_plan(c.n_theta);
+    if (plan.kind != 2 || plan.L != 16 || !ea.periodic || ea.chunk_gap != 0 || ea.peer[0] || ea.row_offset != 0 ||
+        (ea.chunk_cols != 0 && ea.chunk_cols != c.n_theta))
+        return cudaErrorNotSupported;
+    const int E = plan.lay.E;
+    if (c.split >= 2) return launch_tma_ring<16, 1, 2, false, 1, true, true>(c, src, dst, table_step, E, ea);
+    return launch_tma_ring<16, 1, 2, false, 1, false, true>(c, src, dst, table_step, E, ea);
 }
 
 cudaError_t launch_azimuth_scan(const LaunchCtx& c, const cplx* src, cplx* dst, const cplx* table_step, double r_new,
@@ -1950,6 +2132,30 @@ cudaError_t launch_azimuth_scan(const LaunchCtx& c, const cplx* src, cplx* dst, 
     if (L == 16 && RW == 4) return direct(k_azimuth_direct<16, 4>, 16, 4);
     if (L == 16 && RW == 2) return direct(k_azimuth_direct<16, 2>, 16, 2);
     return cudaErrorInvalidConfiguration;
+}
+
+int sring_segment(int n_theta) {
+    const RingPlan p = ring_plan(n_theta);
+    return (p.kind == 2 && p.L == 16) ? 32 * p.L : 0;
+}
+
+int64_t sring_table_elems(int n_theta) { return sring_elems(sring_segment(n_theta)); }
+
+cudaError_t launch_sring_setup(const LaunchCtx& c, cplx* coef, const cplx* ring_tab, int n_steps) {
+    const int ns = sring_segment(c.n_theta);
+    if (!ns) return cudaErrorNotSupported;
+    const int n_items = n_steps * c.n_freq;
+    if (n_items == 0) return cudaSuccess;
+    k_sring_setup<<<(n_items + 63) / 64, 64, 0, c.stream>>>(coef, ring_tab, ring_plan(c.n_theta).lay.E, n_items, ns);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sring_fix(const LaunchCtx& c, cplx* temp, const cplx* tot, const cplx* coef_step, int span) {
+    const int ns = sring_segment(c.n_theta), nseg = c.n_theta / ns;
+    const int64_t blocks = int64_t(c.n_freq) * c.n_tiles * nseg;
+    if (nseg > 16 || blocks > 0x7fffffff) return cudaErrorNotSupported;
+    k_sring_fix<<<int(blocks), 128, 0, c.stream>>>(temp, tot, coef_step, c.n_tiles, c.n_theta, nseg, ns, span);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_finish(const LaunchCtx& c, const cplx* src, int src_tiled, cplx* dst, double r,
