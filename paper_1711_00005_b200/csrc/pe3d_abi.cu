@@ -38,8 +38,8 @@ struct MarchPlan {
     // ([F][n_tiles][8]) and the first depth sweep reads it (null: the full field)
     pe3d::cplx* temp_col;
     // split rings (pe3d_ring.cu k_sring_*): tables [step][F][sring_table_elems], segment
-    // totals, and per step the corrected span (0: that step runs the cluster kernel)
-    pe3d::cplx *sr_coef, *sr_tot;
+    // totals, carries, and per step the corrected span (0: that step runs the cluster kernel)
+    pe3d::cplx *sr_coef, *sr_tot, *sr_cd;
     const int* sr_span;
 };
 
@@ -242,8 +242,10 @@ cudaError_t enqueue_group(Handle* h, const pe3d_grid* g, const MarchPlan& p, int
             cs.sring_tot = p.sr_tot + int64_t(f0) * nseg * 2 * rows;
             const cplx* coef = p.sr_coef + (int64_t(s) * c.n_freq + f0) * pe3d::sring_table_elems(c.n_theta);
             e = prof.run(1, [&] { return pe3d::launch_azimuth_seg(cs, B, A, tab, ea); });
+            cplx* cd = p.sr_cd + int64_t(f0) * nseg * 3 * rows;
+            if (e == cudaSuccess) e = prof.run(3, [&] { return pe3d::launch_sring_carry(cs, cs.sring_tot, coef, cd); });
             if (e == cudaSuccess)
-                e = prof.run(3, [&] { return pe3d::launch_sring_fix(cs, A, cs.sring_tot, coef, p.sr_span[s]); });
+                e = prof.run(3, [&] { return pe3d::launch_sring_fix(cs, A, cd, coef, p.sr_span[s]); });
         } else {
             e = prof.run(1, [&] { return pe3d::launch_azimuth_scan(cg, B, A, tab, r_new, ea); });
         }
@@ -535,8 +537,10 @@ static int march_device_impl(void* handle, const pe3d_grid* g, const pe3d_coeffs
         const int nseg = NT / sr_ns;
         CK(h->sr_coef.ensure(int64_t(g->n_steps) * F * pe3d::sring_table_elems(NT) * sizeof(cplx)), "alloc split ring");
         CK(h->sr_tot.ensure(int64_t(F) * nseg * 2 * n_tiles * 8 * sizeof(cplx)), "alloc split ring");
+        CK(h->sr_cd.ensure(int64_t(F) * nseg * 3 * n_tiles * 8 * sizeof(cplx)), "alloc split ring");
         p.sr_coef = h->sr_coef.as<cplx>();
         p.sr_tot = h->sr_tot.as<cplx>();
+        p.sr_cd = h->sr_cd.as<cplx>();
         p.sr_span = sr_span.data();
     }
 
@@ -617,7 +621,7 @@ static int march_device_impl(void* handle, const pe3d_grid* g, const pe3d_coeffs
         add(ptrs, sizeof(ptrs));
         add(&stream, sizeof(stream));
         const void* tabs[10] = {h->w_abs.ptr, h->fdev.ptr, h->loc_tab.ptr, h->err.ptr, h->ring_tab.ptr, p.ctx.k1_tab,
-                                p.temp_col, p.sr_coef, p.sr_tot, nullptr};
+                                p.temp_col, p.sr_coef, p.sr_tot, p.sr_cd};
         add(tabs, sizeof(tabs));
         if (!sr_span.empty()) add(sr_span.data(), sr_span.size() * sizeof(int));
         const int chains = step_chains(p.ctx, false);

@@ -128,8 +128,8 @@ __global__ void k_ring_setup(cplx* __restrict__ table, const FreqDev* __restrict
 // the true left neighbour at o = 0 (alpha, beta below; B_NS = 1 carries the
 // right neighbour d_s).  |rho| < 1, so alpha and beta decay away from the
 // segment edges: only the points within `span` of an edge are corrected
-// (k_sring_fix, which also chains the carries; the host picks per step either
-// this or the cluster kernel).
+// (k_sring_carry chains the carries, k_sring_fix applies them; the host picks per
+// step either this or the cluster kernel).
 //
 // Per (step, frequency) table (SRING_HDR + 2 NS entries):
 //   [0] rho, [1] 1/(1 - rho^N), [2] gamma, [3] A_0, [4] B_0, [5] b2,
@@ -184,19 +184,63 @@ __global__ void k_sring_setup(cplx* __restrict__ coef, const cplx* __restrict__ 
     }
 }
 
-// The edge fix of a split-ring step, one CTA of 128 threads per (frequency,
-// tile, segment s):
-//  1. the exact carries of the tile's 8 rows, a half-warp per row with lane j
-//     holding segment j's zero-carry totals (tot [F][nseg][2][n_rows]: W, X0);
-//     the segment chains are 4-level scans:
-//       c_j = sum_(j'<j) Rs^(j-1-j') W_j' + Rs^j wend,  X_j = X0_j + gamma c_j,
-//       d_j = sum_(j'>j) Rs^(j'-j-1) X_j' + Rs^(nseg-1-j) xstart
-//     (wend, xstart: the cyclic closures), and e_j = c_j + rho x_first(j);
-//  2. temp += alpha_o c_s + beta_o d_s (+ b2 e_s at o = 0) on the 2 span lines
-//     of the segment's edges, read-modify-write.
-// Every CTA of a tile recomputes its rows' chains (128 threads, a few hundred
-// FMAs) instead of a separate carry kernel and its global round trip (8.4 us).
-__global__ void __launch_bounds__(128) k_sring_fix(cplx* __restrict__ temp, const cplx* __restrict__ tot,
+// Exact carries of every segment from the zero-carry totals (tot
+// [F][nseg][2][n_rows]: W, X0), written as cd [F][nseg][3][n_rows]: c_s, d_s,
+// b2 * (true x at the point before s).  A half-warp per (frequency, row), lane j
+// holding segment j; the segment chains are 4-level scans:
+//   c_j = sum_(j'<j) Rs^(j-1-j') W_j' + Rs^j wend,  X_j = X0_j + gamma c_j,
+//   d_j = sum_(j'>j) Rs^(j'-j-1) X_j' + Rs^(nseg-1-j) xstart
+// (wend, xstart: the cyclic closures).  (Measured and not kept: the chains
+// recomputed inside the fix kernel, per (tile, segment) CTA 24.5 us or per tile
+// CTA 26.8 us, against 8.4 + 16.5 us for the two kernels, and 3 us slower per step.)
+__global__ void __launch_bounds__(128) k_sring_carry(const cplx* __restrict__ tot, const cplx* __restrict__ coef_step,
+                                                     cplx* __restrict__ cd, int n_freq, int nseg, int n_rows, int ns) {
+    const int lane = threadIdx.x & 31, j = lane & 15;
+    const int64_t pair = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 4;   // (frequency, row)
+    const bool live = pair < int64_t(n_freq) * n_rows;
+    const int f = live ? int(pair / n_rows) : 0, l = live ? int(pair - int64_t(f) * n_rows) : 0;
+    const cplx* C = coef_step + int64_t(f) * sring_elems(ns);
+    const cplx rho = C[0], inv_wrap = C[1], gamma = C[2], B0 = C[4], b2 = C[5];
+    const bool seg = live && j < nseg;
+    griddep_wait();                                            // the totals come from the segmented sweep
+    griddep_launch();
+    const cplx* T = tot + (int64_t(f) * nseg + j) * 2 * n_rows + l;
+    const cplx W = seg ? ldc(T) : czero();
+    const cplx X0 = seg ? ldc(T + n_rows) : czero();
+    cplx I = W;                                                // sum_(j'<=j) Rs^(j-j') W_j'
+#pragma unroll
+    for (int d = 1; d < 16; d <<= 1) {
+        const cplx t = shfl_up(I, d);
+        if (j >= d) I = cfma(C[6 + d], t, I);
+    }
+    const cplx wend = cmul(shfl_idx(I, (lane & 16) + nseg - 1), inv_wrap);
+    cplx ip = shfl_up(I, 1);
+    if (j == 0) ip = czero();
+    const cplx c = seg ? cfma(C[6 + (j < 16 ? j : 0)], wend, ip) : czero();
+    const cplx X = cfma(gamma, c, X0);
+    cplx J = X;                                                // sum_(j'>=j) Rs^(j'-j) X_j'
+#pragma unroll
+    for (int d = 1; d < 16; d <<= 1) {
+        const cplx t = shfl_down(J, d);
+        if (j + d < nseg) J = cfma(C[6 + d], t, J);
+    }
+    const cplx xstart = cmul(shfl_idx(J, lane & 16), inv_wrap);
+    cplx jn = shfl_down(J, 1);
+    if (j + 1 >= nseg) jn = czero();
+    const int up = nseg - 1 - j;
+    const cplx dv = seg ? cfma(C[6 + (up >= 0 && up < 16 ? up : 0)], xstart, jn) : czero();
+    if (seg) {
+        cplx* out = cd + (int64_t(f) * nseg + j) * 3 * n_rows + l;
+        stc(out, c);
+        stc(out + n_rows, dv);
+        stc(out + 2 * n_rows, cmul(b2, cfma(rho, cfma(B0, dv, X), c)));      // b2 (c + rho x_first)
+    }
+}
+
+// temp += alpha_o c_s + beta_o d_s (+ b2 x_before at o = 0) at the points within
+// `span` of a segment edge.  One CTA per (frequency, tile, segment): the rows'
+// carries in shared memory, then the 2 span lines of 8 rows, read-modify-write.
+__global__ void __launch_bounds__(128) k_sring_fix(cplx* __restrict__ temp, const cplx* __restrict__ cd,
                                                    const cplx* __restrict__ coef_step, int n_tiles, int n_theta,
                                                    int nseg, int ns, int span) {
     __shared__ cplx sc[3][8];
@@ -204,44 +248,14 @@ __global__ void __launch_bounds__(128) k_sring_fix(cplx* __restrict__ temp, cons
     const int s = b % nseg, ft = b / nseg;
     const int tile = ft % n_tiles, f = ft / n_tiles;
     const int n_rows = n_tiles * 8;
-    const int lane = threadIdx.x & 31, j = lane & 15, row = threadIdx.x >> 4;
-    const cplx* C = coef_step + int64_t(f) * sring_elems(ns);
-    {
-        const cplx rho = C[0], inv_wrap = C[1], gamma = C[2], B0 = C[4], b2 = C[5];
-        const bool seg = j < nseg;
-        const int l = tile * 8 + row;
-        const cplx* T = tot + (int64_t(f) * nseg + j) * 2 * n_rows + l;
-        const cplx W = seg ? ldc(T) : czero();
-        const cplx X0 = seg ? ldc(T + n_rows) : czero();
-        cplx I = W;                                            // sum_(j'<=j) Rs^(j-j') W_j'
-#pragma unroll
-        for (int d = 1; d < 16; d <<= 1) {
-            const cplx t = shfl_up(I, d);
-            if (j >= d) I = cfma(C[6 + d], t, I);
-        }
-        const cplx wend = cmul(shfl_idx(I, (lane & 16) + nseg - 1), inv_wrap);
-        cplx ip = shfl_up(I, 1);
-        if (j == 0) ip = czero();
-        const cplx c = seg ? cfma(C[6 + (seg ? j : 0)], wend, ip) : czero();
-        const cplx X = cfma(gamma, c, X0);
-        cplx J = X;                                            // sum_(j'>=j) Rs^(j'-j) X_j'
-#pragma unroll
-        for (int d = 1; d < 16; d <<= 1) {
-            const cplx t = shfl_down(J, d);
-            if (j + d < nseg) J = cfma(C[6 + d], t, J);
-        }
-        const cplx xstart = cmul(shfl_idx(J, lane & 16), inv_wrap);
-        cplx jn = shfl_down(J, 1);
-        if (j + 1 >= nseg) jn = czero();
-        const cplx dv = seg ? cfma(C[6 + (seg ? nseg - 1 - j : 0)], xstart, jn) : czero();
-        if (j == s) {
-            sc[0][row] = c;
-            sc[1][row] = dv;
-            sc[2][row] = cmul(b2, cfma(rho, cfma(B0, dv, X), c));   // b2 (c + rho x_first)
-        }
+    griddep_wait();                                            // carries and temp of the previous kernels
+    griddep_launch();
+    if (threadIdx.x < 24) {
+        const int k = threadIdx.x >> 3, r = threadIdx.x & 7;
+        sc[k][r] = ldc(cd + ((int64_t(f) * nseg + s) * 3 + k) * n_rows + tile * 8 + r);
     }
     __syncthreads();
-    const cplx* A = C + SRING_HDR;
+    const cplx* A = coef_step + int64_t(f) * sring_elems(ns) + SRING_HDR;
     cplx* base = temp + ((int64_t(f) * n_tiles + tile) * n_theta + int64_t(s) * ns) * 8;
     for (int e = threadIdx.x; e < 16 * span; e += blockDim.x) {
         const int jj = e >> 3, r = e & 7;
@@ -1364,7 +1378,7 @@ k_azimuth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant_
                     for (int h = 0; h < RT; ++h) carry_w[h] = shfl_idx(cw, 16 * h);
                 } else if constexpr (SEG) {
                     // a segment of a longer ring with zero carries: its total W leaves for
-                    // k_sring_fix, which chains the segments exactly
+                    // k_sring_carry, which chains the segments exactly
 #pragma unroll
                     for (int h = 0; h < RT; ++h) carry_w[h] = czero();
                     const cplx W = shfl_idx(Y[0], 31);
@@ -1888,7 +1902,7 @@ static cudaError_t launch_tma_ring(const LaunchCtx& c, const cplx* src, cplx* ds
         // round-1 cp.async kernel's lighter CTAs share the SMs with the other chains'
         // sweeps better (8 frequencies, 8 chains: 30.9 -> 27.0 us per step; with more
         // items per CTA the TMA pipeline wins: 64 frequencies 101 -> 96 us per sweep)
-        if (!CORR && items <= 2 * ctas) return cudaErrorNotSupported;
+        if (!CORR && !SEG && items <= 2 * ctas) return cudaErrorNotSupported;
         int per = int((items + ctas - 1) / ctas);
         if (items <= 2 * ctas) per = 1;               // few items: let the block scheduler balance the tail
         const int grid = int((items + per - 1) / per);
@@ -2150,12 +2164,20 @@ cudaError_t launch_sring_setup(const LaunchCtx& c, cplx* coef, const cplx* ring_
     return cudaGetLastError();
 }
 
-cudaError_t launch_sring_fix(const LaunchCtx& c, cplx* temp, const cplx* tot, const cplx* coef_step, int span) {
+cudaError_t launch_sring_carry(const LaunchCtx& c, const cplx* tot, const cplx* coef_step, cplx* cd) {
+    const int ns = sring_segment(c.n_theta), nseg = c.n_theta / ns, n_rows = c.n_tiles * 8;
+    if (nseg > 16) return cudaErrorNotSupported;
+    const int64_t threads = int64_t(c.n_freq) * n_rows * 16;   // a half-warp per (frequency, row)
+    return launch_pdl(c.pdl != 0, k_sring_carry, dim3(unsigned((threads + 127) / 128)), dim3(128), 0, c.stream, tot,
+                      coef_step, cd, c.n_freq, nseg, n_rows, ns);
+}
+
+cudaError_t launch_sring_fix(const LaunchCtx& c, cplx* temp, const cplx* cd, const cplx* coef_step, int span) {
     const int ns = sring_segment(c.n_theta), nseg = c.n_theta / ns;
     const int64_t blocks = int64_t(c.n_freq) * c.n_tiles * nseg;
-    if (nseg > 16 || blocks > 0x7fffffff) return cudaErrorNotSupported;
-    k_sring_fix<<<int(blocks), 128, 0, c.stream>>>(temp, tot, coef_step, c.n_tiles, c.n_theta, nseg, ns, span);
-    return cudaGetLastError();
+    if (blocks > 0x7fffffff) return cudaErrorNotSupported;
+    return launch_pdl(c.pdl != 0, k_sring_fix, dim3(unsigned(blocks)), dim3(128), 0, c.stream, temp, cd, coef_step,
+                      c.n_tiles, c.n_theta, nseg, ns, span);
 }
 
 cudaError_t launch_finish(const LaunchCtx& c, const cplx* src, int src_tiled, cplx* dst, double r,

@@ -419,6 +419,29 @@ def test_march_graph_variants_bitwise_equal(monkeypatch, n_steps, stride):
             assert got == ref, switch
 
 
+@pytest.mark.parametrize("n_theta,n_depth", [(1024, 1024), (2048, 2048), (4096, 1024)])
+def test_split_rings_match_cluster_sweep(monkeypatch, n_theta, n_depth):
+    """Split-ring steps (every 512-point ring segment solved with zero carries on
+    all SMs, the exact segment carries chained afterwards and applied within the
+    span of each segment edge) against the cluster kernel on every step: the
+    cfg5 medium at 400-450 m (where the carries only reach the segment edges),
+    2 to 8 segments, with and without split depth columns; TL every 4 steps (those
+    steps run the cluster kernel)."""
+    import dataclasses
+    cfg = configs.build("cfg5", n_range=12, output_stride=4)
+    grid, env, source, options = cfg
+    grid = dataclasses.replace(grid, n_azimuth=n_theta, n_depth=n_depth, delta_theta=2 * math.pi / n_theta,
+                               r_start=400.0)
+    cfg = Config(grid, env, dataclasses.replace(source, depth=min(source.depth, 0.4 * grid.depth_extent)), options)
+    f = cfg.source.frequencies[0]
+    monkeypatch.setenv("PE3D_NO_SPLIT_RING", "1")
+    ref = march_frequencies(cfg, [f])[0]
+    monkeypatch.delenv("PE3D_NO_SPLIT_RING")
+    got = march_frequencies(cfg, [f])[0]
+    assert rel_l2(got.final_slab.values, ref.final_slab.values) <= 1e-12
+    assert tl_err(got.tl_field, ref.tl_field) <= 1e-9
+
+
 @pytest.mark.parametrize("groups", ["2", "3", "4"])
 def test_grouped_host_march_bitwise_equal(monkeypatch, groups):
     """pe3d_march_host marching its frequencies in groups (each group's final slab
