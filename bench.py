@@ -465,7 +465,8 @@ def run_gpu_arm(a, rank, world, local):
         secondary = {"cfg2": secondary_line("cfg2", 400, local, peak, peak_kind),
                      "cfg5": secondary_line("cfg5", configs_n_range("cfg5"), local, peak, peak_kind)}
         secondary["cfg2"]["note"] = "BASELINE configs[1]"
-        secondary["cfg5"]["note"] = "BASELINE configs[4] on one GPU (split long columns, cluster azimuth sweep)"
+        secondary["cfg5"]["note"] = ("BASELINE configs[4] on one GPU over its 1000 steps (split long columns; split rings "
+                                     "where the azimuth carries only reach the segment edges, cluster sweep elsewhere)")
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:
