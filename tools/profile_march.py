@@ -1,6 +1,7 @@
 """Small driver for ncu captures: one cfg4 march of a few steps with the
 per-launch profile flag (no graph), so each sweep kernel is a separate,
-identifiable launch.  Usage: python tools/profile_march.py [workload] [steps]"""
+identifiable launch.  Usage: python tools/profile_march.py [workload] [steps] [r_start]
+(r_start: start the march at this range, e.g. 500 for cfg5's split-ring steps)."""
 
 import ctypes as C
 import sys
@@ -23,6 +24,9 @@ def main():
     steps = int(sys.argv[2]) if len(sys.argv) > 2 else 4
     cfg = configs.build(name, n_range=max(steps, 3))
     grid, env, source, _ = cfg
+    if len(sys.argv) > 3:
+        import dataclasses
+        grid = dataclasses.replace(grid, r_start=float(sys.argv[3]))
     freqs = list(source.frequencies)
     k0s = [wavenumber(f, env.c0) for f in freqs]
     F, NT, NZ = len(freqs), grid.n_azimuth, grid.n_depth
