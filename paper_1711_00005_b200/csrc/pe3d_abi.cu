@@ -635,7 +635,7 @@ static int march_device_impl(void* handle, const pe3d_grid* g, const pe3d_coeffs
         for (const char* name : {"PE3D_NO_PDL", "PE3D_CLUSTER_L", "PE3D_DEPTH_NO_CLUSTER", "PE3D_RING_BLOCK",
                                  "PE3D_RING_CPASYNC", "PE3D_DEPTH_NO_SPLIT", "PE3D_FACTOR_SERIAL",
                                  "PE3D_PREPARE_STAGED", "PE3D_PARAMS_MEMCPY", "PE3D_FINAL_STORES",
-                                 "PE3D_FIRST_STEP_FIELD", "PE3D_NO_SPLIT_RING"}) {
+                                 "PE3D_FIRST_STEP_FIELD", "PE3D_NO_SPLIT_RING", "PE3D_DEPTH_SMALL_CTA_OFF"}) {
             const char* v = getenv(name);
             const std::string val = v ? std::string("=") + v : std::string("-");
             add(val.data(), val.size() + 1);

@@ -1228,6 +1228,10 @@ static cudaError_t launch_depth_tma_cfg(const LaunchCtx& c, const cplx* src, cpl
     auto kern = SPLIT ? k_depth_tma<STAGES, MINB, MAXT, 128, true, true>
                       : (MAXT == 128 && nthreads == 128)
                             ? (k1 ? k_depth_tma<STAGES, MINB, MAXT, 128, true> : k_depth_tma<STAGES, MINB, MAXT, 128>)
+                      : (MAXT == 64 && nthreads == 64)
+                            ? (k1 ? k_depth_tma<STAGES, MINB, MAXT, 64, true> : k_depth_tma<STAGES, MINB, MAXT, 64>)
+                      : (MAXT == 32 && nthreads == 32)
+                            ? (k1 ? k_depth_tma<STAGES, MINB, MAXT, 32, true> : k_depth_tma<STAGES, MINB, MAXT, 32>)
                             : (k1 ? k_depth_tma<STAGES, MINB, MAXT, 0, true> : k_depth_tma<STAGES, MINB, MAXT>);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
     if (e != cudaSuccess) return e;
@@ -1295,6 +1299,13 @@ static cudaError_t launch_depth_tma_cluster(const LaunchCtx& c, const cplx* src,
 // per CTA of a cluster (cfg5: 4096 rows, CL = 4); otherwise one 512-thread
 // CTA per SM.
 static cudaError_t launch_depth_tma(const LaunchCtx& c, const cplx* src, cplx* dst) {
+    // the SM runs 12 column warps whatever the column length (168 registers, ~70 KB of
+    // shared memory per 4-warp CTA): shorter columns get more, smaller CTAs (512-row
+    // columns: 3 x 2 warps 152 us -> 6 x 2 warps 109.5 us per 16.8 M points, tools/ring_probe.py)
+    if (!getenv("PE3D_DEPTH_SMALL_CTA_OFF")) {
+        if (c.n_tiles <= 32) return launch_depth_tma_cfg<3, 12, 32>(c, src, dst);
+        if (c.n_tiles <= 64) return launch_depth_tma_cfg<3, 6, 64>(c, src, dst);
+    }
     if (c.n_tiles <= 128) return launch_depth_tma_cfg<3, 3, 128>(c, src, dst);
     if (c.n_tiles % 128 == 0 && c.n_tiles / 128 <= 8 && !getenv("PE3D_DEPTH_NO_CLUSTER"))
         return launch_depth_tma_cluster(c, src, dst, c.n_tiles / 128);
@@ -1417,7 +1428,7 @@ bool depth_sweep_takes_column(const LaunchCtx& c) {
 }
 
 cudaError_t launch_depth_scan(const LaunchCtx& c, const cplx* src, cplx* dst) {
-    if (c.src_col) return c.n_tiles <= 128 ? launch_depth_tma_cfg<3, 3, 128>(c, src, dst) : cudaErrorNotSupported;
+    if (c.src_col) return c.n_tiles <= 128 ? launch_depth_tma(c, src, dst) : cudaErrorNotSupported;
     if (c.split >= 2) {
         // every 1024-row sub-column as a column of its own virtual frequency
         LaunchCtx v = c;
