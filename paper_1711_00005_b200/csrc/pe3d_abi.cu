@@ -41,6 +41,9 @@ struct MarchPlan {
     // totals, carries, and per step the corrected span (0: that step runs the cluster kernel)
     pe3d::cplx *sr_coef, *sr_tot, *sr_cd;
     const int* sr_span;
+    // halo form of the split rings (k_azimuth_tma HALO): the segmented sweep takes its
+    // carries from sr_span[s] neighbouring points per side; no totals, carry or fix kernels
+    bool sr_halo;
 };
 
 // Split-ring plan of a march: per step, the number of points from each segment
@@ -49,7 +52,8 @@ struct MarchPlan {
 // carries.  0 (the exact cluster kernel) where the span exceeds 0.17 of the
 // segment: the segmented sweep + carry + fix beat the cluster kernel (cfg5:
 // ~105 + ~4 + fix vs 142 us) only while the fix rewrites at most ~1/3 of the field.
-static std::vector<int> sring_spans(const pe3d_grid* g, const std::vector<pe3d::FreqDev>& fd, int ns) {
+// With max_span > 0 (the halo form) the bound is max_span points instead.
+static std::vector<int> sring_spans(const pe3d_grid* g, const std::vector<pe3d::FreqDev>& fd, int ns, int max_span) {
     std::vector<int> span(g->n_steps, 0);
     for (int s = 0; s < g->n_steps; ++s) {
         const double r_new = g->r_start + double(g->first_index + s + 1) * g->delta_r;
@@ -67,7 +71,7 @@ static std::vector<int> sring_spans(const pe3d_grid* g, const std::vector<pe3d::
         if (rmax == 0.0) { span[s] = 1; continue; }
         if (!(rmax < 1.0 - 1e-9)) continue;
         const double need = (std::log(1e-22) + std::log(1.0 - rmax * rmax)) / std::log(rmax) + 2.0;
-        if (need <= 0.17 * ns) span[s] = std::max(1, int(std::ceil(need)));
+        if (need <= (max_span > 0 ? double(max_span) : 0.17 * ns)) span[s] = std::max(1, int(std::ceil(need)));
     }
     return span;
 }
@@ -233,8 +237,11 @@ cudaError_t enqueue_group(Handle* h, const pe3d_grid* g, const MarchPlan& p, int
             ea.sample = k % sink->R;
         }
         const cplx* tab = h->ring_tab.as<cplx>() + (int64_t(s) * c.n_freq + f0) * E;
-        const bool split_ring = p.sr_span && p.sr_span[s] > 0 && !ea.tl && !ea.snap && !ea.final_out;
-        if (split_ring) {
+        const bool split_ring = p.sr_span && p.sr_span[s] > 0 && !ea.final_out && (p.sr_halo || (!ea.tl && !ea.snap));
+        if (split_ring && p.sr_halo) {
+            // segments on all SMs, carries from the neighbours' halo points, TL in the same kernel
+            e = prof.run(1, [&] { return pe3d::launch_azimuth_halo(cg, B, A, tab, ea, p.sr_span[s]); });
+        } else if (split_ring) {
             // segments with zero carries, then the exact carries and the edge fix of the next temp
             const int nseg = c.n_theta / pe3d::sring_segment(c.n_theta);
             const int64_t rows = int64_t(c.n_tiles) * 8;
@@ -532,8 +539,12 @@ static int march_device_impl(void* handle, const pe3d_grid* g, const pe3d_coeffs
     // segment edges run the segmented sweep + carry + edge fix instead of the cluster kernel
     std::vector<int> sr_span;
     const int sr_ns = ring_tables && !getenv("PE3D_NO_SPLIT_RING") ? pe3d::sring_segment(NT) : 0;
-    if (sr_ns) {
-        sr_span = sring_spans(g, fd, sr_ns);
+    p.sr_halo = sr_ns && !getenv("PE3D_SRING_FIX");     // A/B: the carry + edge-fix kernels of the first split rings
+    if (sr_ns && p.sr_halo) {
+        sr_span = sring_spans(g, fd, sr_ns, pe3d::sring_halo_max_span());
+        p.sr_span = sr_span.data();
+    } else if (sr_ns) {
+        sr_span = sring_spans(g, fd, sr_ns, 0);
         const int nseg = NT / sr_ns;
         CK(h->sr_coef.ensure(int64_t(g->n_steps) * F * pe3d::sring_table_elems(NT) * sizeof(cplx)), "alloc split ring");
         CK(h->sr_tot.ensure(int64_t(F) * nseg * 2 * n_tiles * 8 * sizeof(cplx)), "alloc split ring");
@@ -635,7 +646,7 @@ static int march_device_impl(void* handle, const pe3d_grid* g, const pe3d_coeffs
         for (const char* name : {"PE3D_NO_PDL", "PE3D_CLUSTER_L", "PE3D_DEPTH_NO_CLUSTER", "PE3D_RING_BLOCK",
                                  "PE3D_RING_CPASYNC", "PE3D_DEPTH_NO_SPLIT", "PE3D_FACTOR_SERIAL",
                                  "PE3D_PREPARE_STAGED", "PE3D_PARAMS_MEMCPY", "PE3D_FINAL_STORES",
-                                 "PE3D_FIRST_STEP_FIELD", "PE3D_NO_SPLIT_RING", "PE3D_DEPTH_SMALL_CTA_OFF"}) {
+                                 "PE3D_FIRST_STEP_FIELD", "PE3D_NO_SPLIT_RING", "PE3D_SRING_FIX", "PE3D_DEPTH_SMALL_CTA_OFF"}) {
             const char* v = getenv(name);
             const std::string val = v ? std::string("=") + v : std::string("-");
             add(val.data(), val.size() + 1);

@@ -256,6 +256,14 @@ __device__ __forceinline__ void tma_store_4d(const void* tmap, int c0, int c1, i
         "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_addr(smem_src))
         : "memory");
 }
+// 3-D tiled TMA load (the halo granules of a ring segment, k_azimuth_tma HALO).
+__device__ __forceinline__ void tma_load_3d(void* smem_dst, const void* tmap, int c0, int c1, int c2, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];\n" ::"r"(smem_addr(smem_dst)),
+        "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(smem_addr(bar))
+        : "memory");
+}
 // 5-D tiled TMA load / store (the azimuth sweep's ring segments, see k_azimuth_tma).
 __device__ __forceinline__ void tma_load_5d(void* smem_dst, const void* tmap, int c0, int c1, int c2, int c3, int c4,
                                             uint64_t* bar) {

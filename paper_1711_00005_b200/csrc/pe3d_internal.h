@@ -204,6 +204,10 @@ int64_t sring_table_elems(int n_theta);
 cudaError_t launch_sring_setup(const LaunchCtx& c, cplx* coef, const cplx* ring_tab, int n_steps);
 cudaError_t launch_azimuth_seg(const LaunchCtx& c, const cplx* src, cplx* dst, const cplx* table_step,
                                const EpilogueArgs& ea);
+// Halo form (k_azimuth_tma HALO): one kernel, carries from `span` neighbouring points per side.
+int sring_halo_max_span();
+cudaError_t launch_azimuth_halo(const LaunchCtx& c, const cplx* src, cplx* dst, const cplx* table_step,
+                                const EpilogueArgs& ea, int span);
 cudaError_t launch_sring_carry(const LaunchCtx& c, const cplx* tot, const cplx* coef_step, cplx* cd);
 cudaError_t launch_sring_fix(const LaunchCtx& c, cplx* temp, const cplx* cd, const cplx* coef_step, int span);
 cudaError_t launch_depth_serial(const LaunchCtx& c, const cplx* src, cplx* dst, cplx* scratch, const cplx* local_now,

@@ -62,9 +62,10 @@ __device__ __forceinline__ cplx cpow_int(cplx z, int n) {
 
 // Ring table of one (step, frequency): [0] rho, [1] scale = -rho/off,
 // [2] 1/(1 - rho^N), [3] (diagonal flag, 0), [4] b1, [5] b2 (the epilogue's
-// next-temp weights, see ring_epilogue), then pw[k] = rho^k (k = 0..L), then
+// next-temp weights, see ring_epilogue), [6] 1/(1 - rho^2), [7] rho/(1 - rho^2)
+// (the halo closure of k_azimuth_tma HALO), then pw[k] = rho^k (k = 0..L), then
 // qp[j] = rho^(jL) (j = 0..n_qp-1).
-constexpr int RING_HDR = 6;
+constexpr int RING_HDR = 8;
 struct RingLayout {
     int L, G, n_chunks, n_qp, E;
 };
@@ -112,6 +113,9 @@ __global__ void k_ring_setup(cplx* __restrict__ table, const FreqDev* __restrict
     const cplx b2 = cmul(rf.scale, alpha);
     T[4] = csub(rf.scale, cadd(b2, b2));
     T[5] = b2;
+    const cplx s_inf = crecip(csub(cone(), cmul(rf.rho, rf.rho)));
+    T[6] = s_inf;
+    T[7] = cmul(rf.rho, s_inf);
 }
 
 // ------------------------------------------------------------ split rings
@@ -1170,14 +1174,30 @@ __device__ __forceinline__ int tma_slot(int q, int k, int r) { return ((k * 32 +
 template <int RT>
 __host__ __device__ constexpr int ring_tma_threads() { return 32 * (8 / RT + 1); }
 
-template <int L, int RT, int S, bool CLUSTER, int MINB, bool CORR = false, bool SEG = false>
+//
+// HALO (with SEG): a segment of a longer ring whose carries only reach `span`
+// points across its edges (|rho|^span below 1e-22 of them; the host picks the
+// steps).  With the segment the producer loads halo_g 32-line granules of the
+// neighbouring segments on either side (3-D map {16 doubles, azimuth, tile},
+// box {16, 32, 1}, the same 128-B swizzle), and each consumer warp sums its row of
+// them into the carries that the cluster kernel gets from its peers:
+//   w at the point before the segment   = sum_(t>=0) rho^t v_(a-1-t),
+//   x at the point after the segment    = [sum_(s>=0) rho^s v_(b+s) + rho w_(b-1)] / (1 - rho^2),
+// so the segment is solved, its TL recorded and its next temp written in this one
+// kernel on all SMs: no cluster, no carry kernel and no edge fix.
+constexpr int RING_HALO_G = 3;                      // granules per side a slot can hold (span <= 96)
+
+template <int L, int RT, int S, bool CLUSTER, int MINB, bool CORR = false, bool SEG = false, bool HALO = false>
 __global__ void __launch_bounds__(ring_tma_threads<RT>(), MINB)
 k_azimuth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ CUtensorMap tm_dst,
               const cplx* __restrict__ table, int E, int tab_elems, int n_theta, int n_tiles, int n_depth,
               int64_t total_items, int n_units, EpilogueArgs ea, const cplx* __restrict__ sp_cd,
               const cplx* __restrict__ sp_aq, const cplx* __restrict__ sp_pa, int split, int tile_perm,
-              const __grid_constant__ CUtensorMap tm_fin, int fin_tma, cplx* __restrict__ seg_tot) {
+              const __grid_constant__ CUtensorMap tm_fin, int fin_tma, cplx* __restrict__ seg_tot,
+              const __grid_constant__ CUtensorMap tm_halo, int halo_g) {
     static_assert(!SEG || (!CLUSTER && RT == 1), "segmented rings: plain kernel, one row per warp");
+    static_assert(!HALO || SEG, "halo carries: segmented rings only");
+    constexpr int HALO_SLOT = HALO ? 2 * RING_HALO_G * 256 : 0;   // cplx per slot: [side][granule][32 lines x 8 rows]
     namespace cg = cooperative_groups;
     constexpr int NW = 8 / RT;                      // consumer warps; warp NW is the TMA producer
     constexpr int NS = 32 * L;                      // segment length
@@ -1186,7 +1206,8 @@ k_azimuth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant_
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     cplx* stage = reinterpret_cast<cplx*>(smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u));
     const int tab_pad = (tab_elems + 7) & ~7;
-    cplx* tabs = stage + S * ITEM;                  // [S][tab_pad]
+    cplx* halo = stage + S * ITEM;                  // HALO: [S][2][RING_HALO_G][256], 1024-B aligned granules
+    cplx* tabs = halo + S * HALO_SLOT;              // [S][tab_pad]
     // CORR: per slot the carries cin[NS], din[NS] of the item's (f, sub-column,
     // segment) and the (a_l, q_l) of its 8 rows, copied with every item (measured
     // faster than keeping one copy per run of items of a sub-column: 149 vs 158 us
@@ -1257,8 +1278,19 @@ k_azimuth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant_
                     need[slot] = corr_item ? 1 : 0;    // published by the arrive below (release)
                 }
                 const unsigned corr_bytes = corr_item ? CORRE * unsigned(sizeof(cplx)) : 0u;
-                mbar_expect_tx(&full[slot], ITEM_BYTES + tab_bytes + corr_bytes);
+                const unsigned halo_bytes = HALO ? 2u * unsigned(halo_g) * 4096u : 0u;
+                mbar_expect_tx(&full[slot], ITEM_BYTES + tab_bytes + corr_bytes + halo_bytes);
                 tma_load_5d(stage + slot * ITEM, &tm_src, 0, 0, 0, seg, titem, &full[slot]);
+                if constexpr (HALO) {
+                    cplx* hs = halo + slot * HALO_SLOT;
+                    for (int g = 0; g < halo_g; ++g) {
+                        int lo = seg * NS - 32 * (g + 1), hi = (seg + 1) * NS + 32 * g;   // cyclic
+                        if (lo < 0) lo += n_theta;
+                        if (hi >= n_theta) hi -= n_theta;
+                        tma_load_3d(hs + g * 256, &tm_halo, 0, lo, titem, &full[slot]);
+                        tma_load_3d(hs + (RING_HALO_G + g) * 256, &tm_halo, 0, hi, titem, &full[slot]);
+                    }
+                }
                 bulk_load(tabs + slot * tab_pad, table + int64_t(f) * E, tab_bytes, &full[slot]);
                 if (CORR && corr_item) {
                     const int tile = titem - f * n_tiles;
@@ -1341,6 +1373,45 @@ k_azimuth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant_
             }
 
             cplx prev_edge[RT], next_edge[RT];     // cluster: x at mseg-1 and mseg+NS (cyclic)
+            cplx halo_w = czero(), halo_x = czero();
+            if constexpr (HALO) {
+                // lane q reads line q of every granule (row `warp`): point t = 32 g + 31 - q before the
+                // segment, s = 32 g + q after it; Horner over the granules, the lane's own power, lane sum
+                const cplx* hs = halo + slot * HALO_SLOT;
+                const int pos = (q << 3) + (warp ^ (q & 7));
+                const cplx R32 = cmul(qp[32 / L], pw[32 % L]);
+                const bool fix = CORR && need[slot];
+                cplx a_l = czero(), q_l = czero();
+                const cplx* cdb = sp_cd;
+                if (fix) {
+                    const cplx* aq = corr + slot * CORRE + 2 * NS;
+                    a_l = aq[2 * warp];
+                    q_l = aq[2 * warp + 1];
+                    cdb = sp_cd + (int64_t(f) * split + tile / (n_tiles / split)) * 2 * n_theta;
+                }
+                for (int g = halo_g - 1; g >= 0; --g) {
+                    cplx a = hs[g * 256 + pos], b = hs[(RING_HALO_G + g) * 256 + pos];
+                    if (fix) {                      // the neighbours' raw points need the split-column carries too
+                        int ma = seg * NS - 32 * (g + 1) + q, mb = (seg + 1) * NS + 32 * g + q;
+                        if (ma < 0) ma += n_theta;
+                        if (mb >= n_theta) mb -= n_theta;
+                        const int ia = ma / NS * NS + (ma % L) * 32 + (ma % NS) / L;   // lane order within its segment
+                        const int ib = mb / NS * NS + (mb % L) * 32 + (mb % NS) / L;
+                        a = cfma(a_l, ldc(cdb + ia), cfma(q_l, ldc(cdb + n_theta + ia), a));
+                        b = cfma(a_l, ldc(cdb + ib), cfma(q_l, ldc(cdb + n_theta + ib), b));
+                    }
+                    halo_w = cfma(R32, halo_w, a);
+                    halo_x = cfma(R32, halo_x, b);
+                }
+                const int tl = 31 - q;
+                halo_w = cmul(cmul(qp[tl / L], pw[tl % L]), halo_w);
+                halo_x = cmul(cmul(qp[q / L], pw[q % L]), halo_x);
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    halo_w = cadd(halo_w, shfl_xor(halo_w, o));
+                    halo_x = cadd(halo_x, shfl_xor(halo_x, o));
+                }
+            }
             if (!diagonal) {
                 // ---- forward cyclic recurrence w_m = v_m + rho w_{m-1}
                 cplx Y[RT];
@@ -1376,6 +1447,8 @@ k_azimuth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant_
                     const cplx cw = cfma(qp[32 * s], cmul(wend, inv_wrap), cin);   // w_(mseg-1), cyclic
 #pragma unroll
                     for (int h = 0; h < RT; ++h) carry_w[h] = shfl_idx(cw, 16 * h);
+                } else if constexpr (HALO) {
+                    carry_w[0] = halo_w;                    // w at the point before the segment
                 } else if constexpr (SEG) {
                     // a segment of a longer ring with zero carries: its total W leaves for
                     // k_sring_carry, which chains the segments exactly
@@ -1433,6 +1506,10 @@ k_azimuth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant_
                     const cplx cx = cfma(qp[32 * (CL - 1 - s)], cmul(x0, inv_wrap), dn);   // x_(mseg+NS), cyclic
 #pragma unroll
                     for (int h = 0; h < RT; ++h) carry_x[h] = shfl_idx(cx, 16 * h);
+                } else if constexpr (HALO) {
+                    // x at the point after the segment: the halo's own forward sums closed by
+                    // 1/(1 - rho^2), plus the segment's last w (carry applied above) carried through
+                    carry_x[0] = cfma(T[7], shfl_idx(v[0][L - 1], 31), cmul(T[6], halo_x));
                 } else if constexpr (SEG) {
 #pragma unroll
                     for (int h = 0; h < RT; ++h) carry_x[h] = czero();
@@ -1454,7 +1531,7 @@ k_azimuth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant_
                     const cplx c_up = cfma(qup, carry_x[h], nx);
 #pragma unroll
                     for (int k = 0; k < L; ++k) v[h][k] = cfma(pw[L - k], c_up, v[h][k]);
-                    if constexpr (CLUSTER) {
+                    if constexpr (CLUSTER || HALO) {
                         next_edge[h] = carry_x[h];
                         prev_edge[h] = cfma(rho, shfl_idx(v[h][0], 0), carry_w[h]);   // x_(mseg-1) = w + rho x_mseg
                     }
@@ -1484,7 +1561,7 @@ k_azimuth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant_
                 if (l + ea.row_offset == 0 || l >= n_depth) {
 #pragma unroll
                     for (int k = 0; k < L; ++k) v[h][k] = czero();
-                    if constexpr (CLUSTER) {
+                    if constexpr (CLUSTER || HALO) {
                         prev_edge[h] = czero();
                         next_edge[h] = czero();
                     }
@@ -1493,7 +1570,7 @@ k_azimuth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant_
                     long long zeros = 0;
 #pragma unroll
                     for (int k = 0; k < L; ++k) {
-                        const int m = mseg + m0 + k;
+                        const int m = (SEG ? seg * NS : mseg) + m0 + k;
                         const cplx uf = cmul(scale, v[h][k]);
                         if (!CLUSTER && fin_tma) stg[tma_slot(q, k, warp * RT + h)] = uf;   // stored by the producer's TMA
                         const int64_t so = (int64_t(f) * ea.n_samples + ea.sample) * n_theta * n_depth +
@@ -1511,7 +1588,7 @@ k_azimuth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant_
                 }
                 if (ea.write_temp) {
                     cplx prev = shfl_up(v[h][L - 1], 1), next = shfl_down(v[h][0], 1);
-                    if constexpr (CLUSTER) {
+                    if constexpr (CLUSTER || HALO) {
                         if (lane == 0) prev = prev_edge[h];
                         if (lane == 31) next = next_edge[h];
                     } else if constexpr (SEG) {
@@ -1867,30 +1944,40 @@ int cached_occupancy(const void* kern, size_t bytes, int cluster, int nthr, cuda
     return v;
 }
 
-template <int L, int RT, int S, bool CLUSTER, int MINB = 1, bool CORR = false, bool SEG = false>
+template <int L, int RT, int S, bool CLUSTER, int MINB = 1, bool CORR = false, bool SEG = false, bool HALO = false>
 static cudaError_t launch_tma_ring(const LaunchCtx& c, const cplx* src, cplx* dst, const cplx* table_step, int E,
-                                   const EpilogueArgs& ea) {
+                                   const EpilogueArgs& ea, int span = 0) {
     constexpr int NS = 32 * L, NW = 8 / RT;
     const int CL = c.n_theta / NS;
     if (c.n_theta % NS != 0 || (CLUSTER ? (CL < 2 || CL > 16) : (SEG ? (CL < 2 || CL > 16) : CL != 1)))
         return cudaErrorNotSupported;
-    if (SEG && (!c.sring_tot || ea.tl || ea.snap || ea.final_out)) return cudaErrorNotSupported;
+    if (SEG && !HALO && (!c.sring_tot || ea.tl || ea.snap || ea.final_out)) return cudaErrorNotSupported;
+    const int halo_g = HALO ? (span + 31) / 32 : 0;
+    if (HALO && (ea.final_out || halo_g < 1 || halo_g > RING_HALO_G)) return cudaErrorNotSupported;
     const int64_t tiles = int64_t(c.n_freq) * c.n_tiles;
     const int64_t items = SEG ? tiles * CL : tiles;
     if (items > 0x7fffffff) return cudaErrorNotSupported;
     CUtensorMap tm_src, tm_dst;
     if (!ring_tensor_map(&tm_src, src, c.n_theta, L, tiles) || !ring_tensor_map(&tm_dst, dst, c.n_theta, L, tiles))
         return cudaErrorNotSupported;
+    CUtensorMap tm_halo = tm_dst;
+    if (HALO) {                                     // 32-line granules of a tile's ring, same swizzle as the segments
+        const uint64_t dims[3] = {16, uint64_t(c.n_theta), uint64_t(tiles)};
+        const uint64_t strides[2] = {128, uint64_t(c.n_theta) * 128};
+        const uint32_t box[3] = {16, 32, 1};
+        if (!encode_swizzled_map(&tm_halo, src, 3, dims, strides, box, 128)) return cudaErrorNotSupported;
+    }
     const int tab_elems = RING_HDR + L + 1 + (CLUSTER ? std::max(32, 32 * (CL - 1) + 1) : 32);
     if (tab_elems > E) return cudaErrorNotSupported;
     const int tab_pad = (tab_elems + 7) & ~7;
     const size_t corre = CORR ? 2 * NS + 16 : 0;    // per slot: the carries and the rows' (a_l, q_l)
     const size_t bytes = 1024 +
-                         sizeof(cplx) * (size_t(S) * NS * 8 + size_t(S) * tab_pad + S * corre + (CLUSTER ? 512 : 0)) +
+                         sizeof(cplx) * (size_t(S) * NS * 8 + size_t(S) * tab_pad + S * corre + (CLUSTER ? 512 : 0) +
+                                         (HALO ? size_t(S) * 2 * RING_HALO_G * 256 : 0)) +
                          sizeof(uint64_t) * (2 * S + (CLUSTER ? 4 * NW : 0)) + sizeof(int) * S;
     if (bytes > 227 * 1024) return cudaErrorNotSupported;
     if (CORR && (c.split < 2 || c.n_tiles % c.split != 0 || !c.sp_cd || !c.sp_aq)) return cudaErrorNotSupported;
-    auto kern = k_azimuth_tma<L, RT, S, CLUSTER, MINB, CORR, SEG>;
+    auto kern = k_azimuth_tma<L, RT, S, CLUSTER, MINB, CORR, SEG, HALO>;
     cudaError_t e = set_smem(kern, bytes);
     if (e != cudaSuccess) return e;
     const int nthr = ring_tma_threads<RT>();
@@ -1921,7 +2008,8 @@ static cudaError_t launch_tma_ring(const LaunchCtx& c, const cplx* src, cplx* ds
         }
         return launch_pdl(c.pdl != 0, kern, dim3(grid), dim3(nthr), bytes, c.stream, tm_src, tm_dst, table_step, E,
                           tab_elems, c.n_theta, c.n_tiles, c.n_depth, items, grid, ea, (const cplx*)c.sp_cd,
-                          (const cplx*)c.sp_aq, (const cplx*)c.sp_pa, c.split, 1, tm_fin, fin_tma, c.sring_tot);
+                          (const cplx*)c.sp_aq, (const cplx*)c.sp_pa, c.split, 1, tm_fin, fin_tma, c.sring_tot,
+                          tm_halo, halo_g);
     } else {
         if (CL > 8) {
             e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -1955,7 +2043,7 @@ static cudaError_t launch_tma_ring(const LaunchCtx& c, const cplx* src, cplx* ds
         }
         return cudaLaunchKernelEx(&cfg, kern, tm_src, tm_dst, table_step, E, tab_elems, c.n_theta, c.n_tiles,
                                   c.n_depth, items, per, ea, (const cplx*)c.sp_cd, (const cplx*)c.sp_aq,
-                                  (const cplx*)c.sp_pa, c.split, perm, tm_dst, 0, (cplx*)nullptr);
+                                  (const cplx*)c.sp_pa, c.split, perm, tm_dst, 0, (cplx*)nullptr, tm_dst, 0);
     }
 }
 
@@ -2039,6 +2127,21 @@ cudaError_t launch_azimuth_seg(const LaunchCtx& c, const cplx* src, cplx* dst, c
     const int E = plan.lay.E;
     if (c.split >= 2) return launch_tma_ring<16, 1, 2, false, 1, true, true>(c, src, dst, table_step, E, ea);
     return launch_tma_ring<16, 1, 2, false, 1, false, true>(c, src, dst, table_step, E, ea);
+}
+
+// Halo form of the split-ring sweep: the carries come from `span` (<= 32 RING_HALO_G)
+// points of the neighbouring segments loaded with every segment; TL and snapshots
+// are recorded in the same kernel (not the final slab).
+int sring_halo_max_span() { return 32 * RING_HALO_G; }
+cudaError_t launch_azimuth_halo(const LaunchCtx& c, const cplx* src, cplx* dst, const cplx* table_step,
+                                const EpilogueArgs& ea, int span) {
+    const RingPlan plan = ring_plan(c.n_theta);
+    if (plan.kind != 2 || plan.L != 16 || !ea.periodic || ea.chunk_gap != 0 || ea.peer[0] || ea.row_offset != 0 ||
+        (ea.chunk_cols != 0 && ea.chunk_cols != c.n_theta))
+        return cudaErrorNotSupported;
+    const int E = plan.lay.E;
+    if (c.split >= 2) return launch_tma_ring<16, 1, 2, false, 1, true, true, true>(c, src, dst, table_step, E, ea, span);
+    return launch_tma_ring<16, 1, 2, false, 1, false, true, true>(c, src, dst, table_step, E, ea, span);
 }
 
 cudaError_t launch_azimuth_scan(const LaunchCtx& c, const cplx* src, cplx* dst, const cplx* table_step, double r_new,

@@ -419,27 +419,34 @@ def test_march_graph_variants_bitwise_equal(monkeypatch, n_steps, stride):
             assert got == ref, switch
 
 
-@pytest.mark.parametrize("n_theta,n_depth", [(1024, 1024), (2048, 2048), (4096, 1024)])
-def test_split_rings_match_cluster_sweep(monkeypatch, n_theta, n_depth):
-    """Split-ring steps (every 512-point ring segment solved with zero carries on
-    all SMs, the exact segment carries chained afterwards and applied within the
-    span of each segment edge) against the cluster kernel on every step: the
-    cfg5 medium at 400-450 m (where the carries only reach the segment edges),
-    2 to 8 segments, with and without split depth columns; TL every 4 steps (those
-    steps run the cluster kernel)."""
+@pytest.mark.parametrize("mode", ["halo", "fix"])
+@pytest.mark.parametrize("n_theta,n_depth,r_start", [(1024, 1024, 400.0), (2048, 2048, 400.0), (4096, 1024, 400.0),
+                                                     (4096, 2048, 190.0), (1024, 512, 700.0)])
+def test_split_rings_match_cluster_sweep(monkeypatch, n_theta, n_depth, r_start, mode):
+    """Split-ring steps (every 512-point ring segment solved on all SMs) against the
+    cluster kernel on every step: the cfg5 medium where the carries only reach the
+    segment edges (spans of 86-20 points: three, two and one halo granules), 2 to 8
+    segments, with and without split depth columns, TL every 4 steps.
+    halo: the carries come from the neighbouring segments' points loaded with each
+    segment, TL steps included (the shipped path).  fix (PE3D_SRING_FIX): zero-carry
+    segments, the exact carries chained afterwards and applied within the span of
+    each segment edge; TL steps run the cluster kernel."""
     import dataclasses
     cfg = configs.build("cfg5", n_range=12, output_stride=4)
     grid, env, source, options = cfg
     grid = dataclasses.replace(grid, n_azimuth=n_theta, n_depth=n_depth, delta_theta=2 * math.pi / n_theta,
-                               r_start=400.0)
+                               r_start=r_start)
     cfg = Config(grid, env, dataclasses.replace(source, depth=min(source.depth, 0.4 * grid.depth_extent)), options)
     f = cfg.source.frequencies[0]
     monkeypatch.setenv("PE3D_NO_SPLIT_RING", "1")
     ref = march_frequencies(cfg, [f])[0]
     monkeypatch.delenv("PE3D_NO_SPLIT_RING")
+    if mode == "fix":
+        monkeypatch.setenv("PE3D_SRING_FIX", "1")
     got = march_frequencies(cfg, [f])[0]
     assert rel_l2(got.final_slab.values, ref.final_slab.values) <= 1e-12
     assert tl_err(got.tl_field, ref.tl_field) <= 1e-9
+    assert got.clamped_samples == ref.clamped_samples
 
 
 @pytest.mark.parametrize("groups", ["2", "3", "4"])
