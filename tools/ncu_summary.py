@@ -31,12 +31,14 @@ def main():
     rows = list(csv.reader(io.StringIO(ncu("-i", rep, "--page", "details", "--csv"))))
     h = rows[0]
     ik, im, iv, iu = (h.index(x) for x in ("Kernel Name", "Metric Name", "Metric Value", "Metric Unit"))
-    kernels = []
+    kernels, first_id = [], {}
+    iid = h.index("ID")
     for r in rows[1:]:
         name = r[ik].split("(")[0]
         if name not in out:
             out[name] = {}
             kernels.append(name)
+            first_id[name] = int(r[iid])            # launch index in the report (instantiations share a base name)
         if r[im] in DETAILS:
             out[name][r[im]] = f"{r[iv]} {r[iu]}".strip()
     raw = list(csv.reader(io.StringIO(ncu("-i", rep, "--page", "raw", "--csv", "--metrics", ",".join(RAW)))))
@@ -46,9 +48,8 @@ def main():
         for m in RAW:
             out[name][m] = r[hr.index(m)] + " " + raw[1][hr.index(m)]
     for name in kernels:
-        base = re.search(r"(k_\w+)", name).group(1)
         src = list(csv.reader(io.StringIO(ncu("-i", rep, "--page", "source", "--csv", "--print-source", "sass",
-                                              "--kernel-name", "regex:" + base + "(<|$)"))))
+                                              "--launch-skip", str(first_id[name]), "--launch-count", "1"))))
         hdr = src[1]
         iE0 = hdr.index("Instructions Executed")
         data = [r for r in src[2:] if len(r) == len(hdr) and r[iE0].isdigit()]   # one kernel's rows
