@@ -16,8 +16,12 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <thread>
 #include <tuple>
 #include <vector>
+#if defined(__x86_64__)
+#include <emmintrin.h>
+#endif
 
 #include "../../include/pe3d_b200.h"
 #include "pe3d_host.h"
@@ -105,6 +109,9 @@ struct TlSink {
     double* host;       // [F][S][n_theta][n_depth], page-locked
     int S;              // samples of the host stack
     int R;              // device ring slots per frequency
+    int col0;           // sample 0 is the same for every azimuth (column starter on a periodic ring):
+                        // only its first azimuth row leaves the device, the caller replicates it
+    int pad_;           // (the struct's bytes are part of the graph key: no padding)
 };
 
 // events: per copy stream c (0..MAX_CHAINS): R "copied" slots + 1 "written"
@@ -139,14 +146,15 @@ static cudaError_t tl_before(Handle* h, const TlSink& sk, int c, int k, cudaStre
 
 // after the kernel writing sample k of frequencies [f0, f0 + nf) on st
 static cudaError_t tl_after(Handle* h, const TlSink& sk, int c, int k, int f0, int nf, int64_t oe,
-                            const double* ring, cudaStream_t st) {
+                            const double* ring, cudaStream_t st, int64_t width = 0) {
     cudaStream_t side = h->tl_side[c];
     cudaError_t e = cudaEventRecord(tl_event(h, c, sk.R, sk), st);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(side, tl_event(h, c, sk.R, sk), 0);
     const size_t w = size_t(oe) * sizeof(double);
+    const size_t wcopy = width ? size_t(width) * sizeof(double) : w;     // the sample's leading doubles only
     if (e == cudaSuccess)
         e = cudaMemcpy2DAsync(sk.host + (int64_t(f0) * sk.S + k) * oe, sk.S * w, ring + (int64_t(f0) * sk.R + k % sk.R) * oe,
-                              sk.R * w, w, nf, cudaMemcpyDeviceToHost, side);
+                              sk.R * w, wcopy, nf, cudaMemcpyDeviceToHost, side);
     if (e == cudaSuccess) e = cudaEventRecord(tl_event(h, c, k % sk.R, sk), side);
     return e;
 }
@@ -278,7 +286,8 @@ cudaError_t enqueue_steps(Handle* h, const pe3d_grid* g, const MarchPlan& p, con
     const pe3d::LaunchCtx& c = p.ctx;
     if (sink && d_tl) {
         const int64_t oe = int64_t(c.n_theta) * g->n_depth;
-        cudaError_t e = tl_after(h, *sink, Handle::MAX_CHAINS, 0, 0, c.n_freq, oe, d_tl, c.stream);
+        cudaError_t e = tl_after(h, *sink, Handle::MAX_CHAINS, 0, 0, c.n_freq, oe, d_tl, c.stream,
+                                 sink->col0 ? g->n_depth : oe);
         if (e != cudaSuccess) return e;
     }
     int n_copy = 0;
@@ -651,7 +660,7 @@ static int march_device_impl(void* handle, const pe3d_grid* g, const pe3d_coeffs
             const std::string val = v ? std::string("=") + v : std::string("-");
             add(val.data(), val.size() + 1);
         }
-        const TlSink none{nullptr, 0, 0};
+        const TlSink none{nullptr, 0, 0, 0, 0};
         add(sink ? sink : &none, sizeof(TlSink));
         int hit = -1;
         for (int i = 0; i < int(h->march_graphs.size()); ++i)
@@ -758,6 +767,47 @@ static int march_device_impl(void* handle, const pe3d_grid* g, const pe3d_coeffs
 
 }  // extern "C"
 
+// Host threads that replicate the first azimuth row of TL sample 0 over the other
+// azimuths of frequencies [f0, f1) of a [F][S][n_theta][n_depth] stack (streaming
+// stores: the rows are written once and read by the caller much later).  Joined by
+// join() or the destructor, so every return path of the caller leaves no thread behind.
+struct RowReplicator {
+    std::vector<std::thread> threads;
+    static void fill(double* tl, int f0, int f1, int64_t S, int n_theta, int n_depth, int part, int parts) {
+        const int64_t rows = int64_t(f1 - f0) * (n_theta - 1);
+        const int64_t r0 = rows * part / parts, r1 = rows * (part + 1) / parts;
+        for (int64_t r = r0; r < r1; ++r) {
+            const int f = f0 + int(r / (n_theta - 1)), m = 1 + int(r % (n_theta - 1));
+            const double* src = tl + int64_t(f) * S * n_theta * n_depth;
+            double* dst = tl + (int64_t(f) * S * n_theta + m) * n_depth;
+#if defined(__x86_64__)
+            int l = 0;
+            if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)
+                for (; l + 2 <= n_depth; l += 2) _mm_stream_pd(dst + l, _mm_loadu_pd(src + l));
+            for (; l < n_depth; ++l) dst[l] = src[l];
+#else
+            std::memcpy(dst, src, size_t(n_depth) * sizeof(double));
+#endif
+        }
+#if defined(__x86_64__)
+        _mm_sfence();
+#endif
+    }
+    void start(double* tl, int f0, int f1, int64_t S, int n_theta, int n_depth) {
+        // two threads per group: measured best at cfg4's 20-step march (1-2 threads 6.6-6.9 ms,
+        // 4 threads 6.8-7.6 ms, full copy 7.9-8.1 ms; profiles/r02_ab_tl0_row.txt)
+        int parts = std::thread::hardware_concurrency() >= 4 ? 2 : 1;
+        if (const char* env = getenv("PE3D_TL0_THREADS")) parts = std::max(1, atoi(env));
+        for (int k = 0; k < parts; ++k) threads.emplace_back(fill, tl, f0, f1, S, n_theta, n_depth, k, parts);
+    }
+    void join() {
+        for (std::thread& t : threads)
+            if (t.joinable()) t.join();
+        threads.clear();
+    }
+    ~RowReplicator() { join(); }
+};
+
 // Frequency groups of a pe3d_march_host call (see there): >1 only when the final
 // slab's copy to the host (PCIe, modelled at 57 GB/s) would take longer than half
 // the march (modelled at 5.5 TB/s of HBM for the 64 B per grid point and step);
@@ -804,11 +854,11 @@ int pe3d_march_host(void* handle, const pe3d_grid* g, const pe3d_coeffs* coeffs,
     if (u_final) CK(h->h_final.ensure(F * slab * sizeof(cplx)), "alloc");
     // A page-locked TL stack (and no snapshots): stream the samples out while
     // the march runs, through a device ring of a few samples per frequency.
-    TlSink sink{nullptr, 0, 0};
+    TlSink sink{nullptr, 0, 0, 0, 0};
     if (tl && !snapshots && !getenv("PE3D_NO_TL_STREAM")) {
         cudaPointerAttributes pa{};
         if (cudaPointerGetAttributes(&pa, tl) == cudaSuccess && pa.type == cudaMemoryTypeHost)
-            sink = TlSink{tl, int(S), int(S < 4 ? S : 4)};
+            sink = TlSink{tl, int(S), int(S < 4 ? S : 4), 0, 0};
         cudaGetLastError();                                  // pageable memory: not an error
     }
     if (tl) CK(h->h_tl.ensure(F * (sink.host ? sink.R : S) * slab * sizeof(double)), "alloc");
@@ -826,6 +876,14 @@ int pe3d_march_host(void* handle, const pe3d_grid* g, const pe3d_coeffs* coeffs,
     }
     const int64_t u0_per = (g->flags & PE3D_FLAG_STARTER_COLUMN) ? g->n_depth : slab;
     const int64_t tl_per = (sink.host ? sink.R : S) * slab;
+    // A copy-bound march (G > 1) of column starters on a periodic ring: the starting TL sample is
+    // the same for every azimuth, so only its first azimuth row crosses PCIe (cfg4: 0.5 MB instead
+    // of 134 MB of the 402 MB a 20-step march sends) and host threads replicate it while the later
+    // groups march and the final slabs leave.
+    if (sink.host && G > 1 && (g->flags & PE3D_FLAG_STARTER_COLUMN) && g->topology == PE3D_PERIODIC &&
+        g->n_theta > 1 && !getenv("PE3D_TL0_FULL"))
+        sink.col0 = 1;
+    RowReplicator rep;
     pe3d_error best{};
     int best_st = PE3D_OK;
     for (int gi = 0; gi < G; ++gi) {
@@ -852,6 +910,7 @@ int pe3d_march_host(void* handle, const pe3d_grid* g, const pe3d_coeffs* coeffs,
             if (lower) { best = e_g; best_st = st_g; }
             continue;
         }
+        if (sink.col0) rep.start(tl, f0, f1, S, g->n_theta, g->n_depth);   // the march synchronised: row 0 is there
         if (G > 1 && u_final) {                             // this group's slab leaves while the next marches
             CK(cudaEventRecord(h->copy_ev, s), "event");
             CK(cudaStreamWaitEvent(h->copy_stream, h->copy_ev, 0), "event");
@@ -860,6 +919,7 @@ int pe3d_march_host(void* handle, const pe3d_grid* g, const pe3d_coeffs* coeffs,
         }
     }
     if (G > 1) CK(cudaStreamSynchronize(h->copy_stream), "sync");
+    rep.join();
     if (best_st != PE3D_OK) {
         if (err) *err = best;
         return best_st;

@@ -466,6 +466,14 @@ def test_grouped_host_march_bitwise_equal(monkeypatch, groups):
     ref = run()
     monkeypatch.setenv("PE3D_HOST_GROUPS", groups)
     assert run() == ref
+    # grouped marches of column starters send only the first azimuth row of the
+    # starting TL sample and replicate it on the host (pe3d_abi.cu RowReplicator):
+    # the same bytes as the full copy (PE3D_TL0_FULL), whatever the thread count
+    monkeypatch.setenv("PE3D_TL0_THREADS", "3")
+    assert run() == ref
+    monkeypatch.delenv("PE3D_TL0_THREADS")
+    monkeypatch.setenv("PE3D_TL0_FULL", "1")
+    assert run() == ref
 
 
 @pytest.mark.parametrize("shape", ["cfg4", "long"])
