@@ -550,9 +550,14 @@ def host_march_e2e(m, steps, stride, world, total_points):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         wall = float(t.item())
     h2d = (h_local.numel() + h_u0.numel()) * 8 * world
-    d2h = (h_final.numel() + h_tl.numel() + h_cl.numel()) * 8 * world
-    return {"value": total_points / wall, "unit": UNIT, "h2d_bytes_per_step": h2d / steps,
-            "d2h_bytes_per_step": d2h / steps, "wall_s": wall, "output_stride": stride, "tl_samples": S,
+    d2h = (h_final.numel() + h_tl.numel() + h_cl.numel()) * 8 * world      # the result tensors
+    # bytes the library actually moved (a copy-bound march sends one azimuth row of the
+    # azimuth-uniform starting TL sample and replicates it on host threads)
+    b_in, b_out = C.c_int64(0), C.c_int64(0)
+    m.lib.pe3d_last_copy_bytes(m.h, C.byref(b_in), C.byref(b_out))
+    return {"value": total_points / wall, "unit": UNIT, "h2d_bytes_per_step": b_in.value * world / steps,
+            "d2h_bytes_per_step": b_out.value * world / steps, "result_bytes_per_step": d2h / steps,
+            "wall_s": wall, "output_stride": stride, "tl_samples": S,
             "path": "pe3d_march_host (C ABI, pinned host buffers; starter columns + medium in, final slab + "
                     "TL stack out)"}
 
@@ -573,9 +578,16 @@ def dropin_e2e(name, steps, device, total_points):
     r0 = rep.results[0]
     S, NT, NZ = r0.tl_field.shape
     h2d = len(freqs) * 2 * NZ * 16                      # starter column + medium column
-    d2h = len(freqs) * (S * NT * NZ * 8 + NT * NZ * 16 + 8)
-    return {"value": total_points / wall, "unit": UNIT, "h2d_bytes_per_step": h2d / steps,
-            "d2h_bytes_per_step": d2h / steps, "wall_s": wall, "output_stride": r0.output_stride,
+    d2h = len(freqs) * (S * NT * NZ * 8 + NT * NZ * 16 + 8)     # the result arrays
+    import ctypes as C
+    from paper_1711_00005_b200 import _native
+    b_in, b_out = C.c_int64(0), C.c_int64(0)
+    _native.load_library().pe3d_last_copy_bytes(_native.handle(device), C.byref(b_in), C.byref(b_out))
+    if b_out.value <= 0:                                # the farm marched on another handle: count the arrays
+        b_in, b_out = C.c_int64(h2d), C.c_int64(d2h)
+    return {"value": total_points / wall, "unit": UNIT, "h2d_bytes_per_step": b_in.value / steps,
+            "d2h_bytes_per_step": b_out.value / steps, "result_bytes_per_step": d2h / steps, "wall_s": wall,
+            "output_stride": r0.output_stride,
             "path": "paper_1711_00005_b200.frequency_farm(config, frequencies): host starter + medium, "
                     "one batched march, FrequencyResults in page-locked numpy arrays"}
 

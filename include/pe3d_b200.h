@@ -266,6 +266,15 @@ PE3D_API int pe3d_profile_last(void* handle, double* ms, int32_t* launches);
 PE3D_API int pe3d_last_launches(void* handle, int64_t* launches);
 
 /*
+ * pe3d_last_copy_bytes -- bytes the last pe3d_march_host call on this handle
+ * moved host-to-device and device-to-host (a grouped march of column
+ * starters sends one azimuth row of the starting TL sample and replicates it
+ * on the host, so d2h can be less than the size of the result buffers).
+ * Measurement only.
+ */
+PE3D_API int pe3d_last_copy_bytes(void* handle, int64_t* h2d, int64_t* d2h);
+
+/*
  * pe3d_profile_launches -- the individual CUDA-event times (ms, launch order)
  * of kernel class `cls` (0 depth sweep, 1 azimuth sweep, 2 other, 3 the carry
  * and edge fix of a split-ring azimuth sweep) in the last PE3D_FLAG_PROFILE

@@ -29,7 +29,7 @@ EXPORTED_SYMBOLS = (
     "pe3d_abi_version", "pe3d_device_count", "pe3d_handle_create", "pe3d_handle_destroy",
     "pe3d_sample_count", "pe3d_march_host", "pe3d_march_device", "pe3d_step_general_host",
     "pe3d_solve_batch_host", "pe3d_profile_last", "pe3d_march_medium_host", "pe3d_slab_unique_id",
-    "pe3d_march_slab", "pe3d_slab_p2p_export", "pe3d_march_slab_p2p", "pe3d_last_launches",
+    "pe3d_march_slab", "pe3d_slab_p2p_export", "pe3d_march_slab_p2p", "pe3d_last_launches", "pe3d_last_copy_bytes",
     "pe3d_profile_launches", "pe3d_host_alloc", "pe3d_host_free",
 )
 SLAB_IPC_BYTES = 192
@@ -90,6 +90,7 @@ _SIGNATURES = {
                                         Strided, _P, C.POINTER(ErrorRecord)]),
     "pe3d_profile_last": (C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_int32)]),
     "pe3d_last_launches": (C.c_int, [_P, C.POINTER(C.c_int64)]),
+    "pe3d_last_copy_bytes": (C.c_int, [_P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "pe3d_profile_launches": (C.c_int, [_P, C.c_int32, C.POINTER(C.c_double), C.c_int32, C.POINTER(C.c_int32)]),
     "pe3d_host_alloc": (C.c_int, [C.c_uint64, C.POINTER(C.c_void_p)]),
     "pe3d_host_free": (C.c_int, [_P]),

@@ -798,7 +798,13 @@ struct RowReplicator {
         // 4 threads 6.8-7.6 ms, full copy 7.9-8.1 ms; profiles/r02_ab_tl0_row.txt)
         int parts = std::thread::hardware_concurrency() >= 4 ? 2 : 1;
         if (const char* env = getenv("PE3D_TL0_THREADS")) parts = std::max(1, atoi(env));
-        for (int k = 0; k < parts; ++k) threads.emplace_back(fill, tl, f0, f1, S, n_theta, n_depth, k, parts);
+        for (int k = 0; k < parts; ++k) {
+            try {
+                threads.emplace_back(fill, tl, f0, f1, S, n_theta, n_depth, k, parts);
+            } catch (...) {                         // no thread to be had: this part on the calling thread
+                fill(tl, f0, f1, S, n_theta, n_depth, k, parts);
+            }
+        }
     }
     void join() {
         for (std::thread& t : threads)
@@ -883,6 +889,10 @@ int pe3d_march_host(void* handle, const pe3d_grid* g, const pe3d_coeffs* coeffs,
     if (sink.host && G > 1 && (g->flags & PE3D_FLAG_STARTER_COLUMN) && g->topology == PE3D_PERIODIC &&
         g->n_theta > 1 && !getenv("PE3D_TL0_FULL"))
         sink.col0 = 1;
+    h->last_h2d_bytes = (F * g->n_depth + u0_elems) * int64_t(sizeof(cplx));
+    h->last_d2h_bytes = (u_final ? F * slab * int64_t(sizeof(cplx)) : 0) + (clamped ? F * int64_t(sizeof(int64_t)) : 0) +
+                        (snapshots ? F * S * slab * int64_t(sizeof(cplx)) : 0) +
+                        (tl ? F * ((S - (sink.col0 ? 1 : 0)) * slab + (sink.col0 ? g->n_depth : 0)) * int64_t(sizeof(double)) : 0);
     RowReplicator rep;
     pe3d_error best{};
     int best_st = PE3D_OK;
@@ -1333,6 +1343,14 @@ int pe3d_march_medium_host(void* handle, const pe3d_grid* g, const pe3d_coeffs* 
 
 // NCCL is loaded lazily (only the slab march needs it), so the library has
 // no link-time dependency on a particular libnccl.
+int pe3d_last_copy_bytes(void* handle, int64_t* h2d, int64_t* d2h) {
+    Handle* h = static_cast<Handle*>(handle);
+    if (!h) return PE3D_BAD_ARGUMENT;
+    if (h2d) *h2d = h->last_h2d_bytes;
+    if (d2h) *d2h = h->last_d2h_bytes;
+    return PE3D_OK;
+}
+
 int pe3d_last_launches(void* handle, int64_t* launches) {
     Handle* h = static_cast<Handle*>(handle);
     if (!h || !launches) return PE3D_BAD_ARGUMENT;

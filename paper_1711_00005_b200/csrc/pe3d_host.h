@@ -108,6 +108,7 @@ struct Handle {
     std::vector<double> prof_list[4];     // per launch, in launch order
     // kernels launched by the last march (graph replays included)
     int64_t graph_launches = 0, last_launches = 0;
+    int64_t last_h2d_bytes = 0, last_d2h_bytes = 0;     // pe3d_march_host: bytes moved each way
     // concurrent step-loop chains over disjoint frequency groups
     static constexpr int MAX_CHAINS = 8;
     cudaStream_t chain_stream[MAX_CHAINS] = {};
