@@ -469,11 +469,23 @@ def test_grouped_host_march_bitwise_equal(monkeypatch, groups):
     # grouped marches of column starters send only the first azimuth row of the
     # starting TL sample and replicate it on the host (pe3d_abi.cu RowReplicator):
     # the same bytes as the full copy (PE3D_TL0_FULL), whatever the thread count
+    import ctypes as C
+
+    def d2h_bytes():
+        b_in, b_out = C.c_int64(0), C.c_int64(0)
+        _native.load_library().pe3d_last_copy_bytes(_native.handle(0), C.byref(b_in), C.byref(b_out))
+        assert b_in.value == len(freqs) * 2 * 1024 * 16          # starter and medium columns
+        return b_out.value
+
+    slab, S = 256 * 1024, 4
+    full = len(freqs) * (S * slab * 8 + slab * 16 + 8)
     monkeypatch.setenv("PE3D_TL0_THREADS", "3")
     assert run() == ref
+    assert d2h_bytes() == (full - len(freqs) * (slab - 1024) * 8 if int(groups) > 1 else full)
     monkeypatch.delenv("PE3D_TL0_THREADS")
     monkeypatch.setenv("PE3D_TL0_FULL", "1")
     assert run() == ref
+    assert d2h_bytes() == full
 
 
 @pytest.mark.parametrize("shape", ["cfg4", "long"])
