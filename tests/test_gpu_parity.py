@@ -321,15 +321,17 @@ def test_cluster_depth_sweep_matches_single_cta(monkeypatch, n_depth, topology):
     assert tl_err(got.tl_field, orc.tl_field) <= TL_TOL
 
 
-@pytest.mark.parametrize("family", ["split_cluster", "lockstep_cluster", "warp_chains"])
+@pytest.mark.parametrize("family", ["split_cluster", "split_halo", "lockstep_cluster", "warp_chains"])
 def test_async_kernels_race_stress(monkeypatch, family):
     """Race stress for the asynchronous kernels (compute-sanitizer is closed on
     this GPU pool, profiles/r02_compute_sanitizer_closed.txt): TMA producer /
     consumer mbarrier rings, DSMEM st.async exchanges, the split-column
     carries.  Twenty marches per family, graphed and unGraphed, must be
     bitwise identical -- the split sweeps with the corrected cluster ring
-    (cfg5 shape), the lock-step cluster sweeps, and the ring-per-warp TMA
-    sweep with 1, 2 and 8 concurrent step chains (cfg4 shape)."""
+    (cfg5 shape), the same from 400 m on, where every step runs the halo-form
+    split-ring kernel (segment + neighbour granules on one mbarrier), the
+    lock-step cluster sweeps, and the ring-per-warp TMA sweep with 1, 2 and 8
+    concurrent step chains (cfg4 shape)."""
     if family == "warp_chains":
         cfg = configs.build("cfg4", n_range=6, frequencies=(50.0, 80.0, 130.0, 200.0, 310.0, 420.0, 460.0, 500.0),
                             output_stride=3)
@@ -340,7 +342,8 @@ def test_async_kernels_race_stress(monkeypatch, family):
             monkeypatch.setenv("PE3D_DEPTH_NO_SPLIT", "1")
         cfg5 = configs.build("cfg5", n_range=6, output_stride=3)
         grid = cfg5.grid
-        cfg = Config(Grid3D(6, 2048, 4096, grid.delta_r, 2 * math.pi / 2048, grid.delta_z, grid.r_start),
+        r_start = 400.0 if family == "split_halo" else grid.r_start
+        cfg = Config(Grid3D(6, 2048, 4096, grid.delta_r, 2 * math.pi / 2048, grid.delta_z, r_start),
                      cfg5.environment, SourceSpec((500.0,), 600.0), RunOptions(output_stride=3))
         freqs = [500.0]
         settings = [(None, fl) for fl in (0, _native.FLAG_NO_GRAPH)] * 10
