@@ -41,23 +41,17 @@ struct MarchPlan {
     // column starter: the prologue leaves the first temp as one column per frequency
     // ([F][n_tiles][8]) and the first depth sweep reads it (null: the full field)
     pe3d::cplx* temp_col;
-    // split rings (pe3d_ring.cu k_sring_*): tables [step][F][sring_table_elems], segment
-    // totals, carries, and per step the corrected span (0: that step runs the cluster kernel)
-    pe3d::cplx *sr_coef, *sr_tot, *sr_cd;
+    // split rings (k_azimuth_tma SEG/HALO): per step the number of neighbouring points per side
+    // a ring segment takes its carries from (0: that step runs the cluster kernel)
     const int* sr_span;
-    // halo form of the split rings (k_azimuth_tma HALO): the segmented sweep takes its
-    // carries from sr_span[s] neighbouring points per side; no totals, carry or fix kernels
-    bool sr_halo;
 };
 
-// Split-ring plan of a march: per step, the number of points from each segment
-// edge whose next temp needs the carry correction (k_sring_fix), from the largest
-// |rho| of the step's frequencies: the dropped terms are below 1e-22 of the
-// carries.  0 (the exact cluster kernel) where the span exceeds 0.17 of the
-// segment: the segmented sweep + carry + fix beat the cluster kernel (cfg5:
-// ~105 + ~4 + fix vs 142 us) only while the fix rewrites at most ~1/3 of the field.
-// With max_span > 0 (the halo form) the bound is max_span points instead.
-static std::vector<int> sring_spans(const pe3d_grid* g, const std::vector<pe3d::FreqDev>& fd, int ns, int max_span) {
+// Split-ring plan of a march: per step, the number of neighbouring points per side
+// whose weights |rho|^t still matter to a ring segment's carries, from the largest
+// |rho| of the step's frequencies: the dropped terms are below 1e-22 of the carries.
+// 0 (the exact cluster kernel) where that span exceeds max_span, the halo a segment
+// can load (cfg5: the first 168 steps, rho -> 1 at short range).
+static std::vector<int> sring_spans(const pe3d_grid* g, const std::vector<pe3d::FreqDev>& fd, int max_span) {
     std::vector<int> span(g->n_steps, 0);
     for (int s = 0; s < g->n_steps; ++s) {
         const double r_new = g->r_start + double(g->first_index + s + 1) * g->delta_r;
@@ -75,7 +69,7 @@ static std::vector<int> sring_spans(const pe3d_grid* g, const std::vector<pe3d::
         if (rmax == 0.0) { span[s] = 1; continue; }
         if (!(rmax < 1.0 - 1e-9)) continue;
         const double need = (std::log(1e-22) + std::log(1.0 - rmax * rmax)) / std::log(rmax) + 2.0;
-        if (need <= (max_span > 0 ? double(max_span) : 0.17 * ns)) span[s] = std::max(1, int(std::ceil(need)));
+        if (need <= double(max_span)) span[s] = std::max(1, int(std::ceil(need)));
     }
     return span;
 }
@@ -245,22 +239,9 @@ cudaError_t enqueue_group(Handle* h, const pe3d_grid* g, const MarchPlan& p, int
             ea.sample = k % sink->R;
         }
         const cplx* tab = h->ring_tab.as<cplx>() + (int64_t(s) * c.n_freq + f0) * E;
-        const bool split_ring = p.sr_span && p.sr_span[s] > 0 && !ea.final_out && (p.sr_halo || (!ea.tl && !ea.snap));
-        if (split_ring && p.sr_halo) {
+        if (p.sr_span && p.sr_span[s] > 0 && !ea.final_out) {
             // segments on all SMs, carries from the neighbours' halo points, TL in the same kernel
             e = prof.run(1, [&] { return pe3d::launch_azimuth_halo(cg, B, A, tab, ea, p.sr_span[s]); });
-        } else if (split_ring) {
-            // segments with zero carries, then the exact carries and the edge fix of the next temp
-            const int nseg = c.n_theta / pe3d::sring_segment(c.n_theta);
-            const int64_t rows = int64_t(c.n_tiles) * 8;
-            pe3d::LaunchCtx cs = cg;
-            cs.sring_tot = p.sr_tot + int64_t(f0) * nseg * 2 * rows;
-            const cplx* coef = p.sr_coef + (int64_t(s) * c.n_freq + f0) * pe3d::sring_table_elems(c.n_theta);
-            e = prof.run(1, [&] { return pe3d::launch_azimuth_seg(cs, B, A, tab, ea); });
-            cplx* cd = p.sr_cd + int64_t(f0) * nseg * 3 * rows;
-            if (e == cudaSuccess) e = prof.run(3, [&] { return pe3d::launch_sring_carry(cs, cs.sring_tot, coef, cd); });
-            if (e == cudaSuccess)
-                e = prof.run(3, [&] { return pe3d::launch_sring_fix(cs, A, cd, coef, p.sr_span[s]); });
         } else {
             e = prof.run(1, [&] { return pe3d::launch_azimuth_scan(cg, B, A, tab, r_new, ea); });
         }
@@ -545,22 +526,10 @@ static int march_device_impl(void* handle, const pe3d_grid* g, const pe3d_coeffs
     if (ring_tables) CK(h->ring_tab.ensure(int64_t(g->n_steps) * F * pe3d::ring_table_elems(NT) * sizeof(cplx)),
                         "alloc ring table");
     // split rings for cluster-sized rings (cfg5): steps whose carries only reach the
-    // segment edges run the segmented sweep + carry + edge fix instead of the cluster kernel
+    // neighbouring segments' edges run the segmented halo sweep instead of the cluster kernel
     std::vector<int> sr_span;
-    const int sr_ns = ring_tables && !getenv("PE3D_NO_SPLIT_RING") ? pe3d::sring_segment(NT) : 0;
-    p.sr_halo = sr_ns && !getenv("PE3D_SRING_FIX");     // A/B: the carry + edge-fix kernels of the first split rings
-    if (sr_ns && p.sr_halo) {
-        sr_span = sring_spans(g, fd, sr_ns, pe3d::sring_halo_max_span());
-        p.sr_span = sr_span.data();
-    } else if (sr_ns) {
-        sr_span = sring_spans(g, fd, sr_ns, 0);
-        const int nseg = NT / sr_ns;
-        CK(h->sr_coef.ensure(int64_t(g->n_steps) * F * pe3d::sring_table_elems(NT) * sizeof(cplx)), "alloc split ring");
-        CK(h->sr_tot.ensure(int64_t(F) * nseg * 2 * n_tiles * 8 * sizeof(cplx)), "alloc split ring");
-        CK(h->sr_cd.ensure(int64_t(F) * nseg * 3 * n_tiles * 8 * sizeof(cplx)), "alloc split ring");
-        p.sr_coef = h->sr_coef.as<cplx>();
-        p.sr_tot = h->sr_tot.as<cplx>();
-        p.sr_cd = h->sr_cd.as<cplx>();
+    if (ring_tables && !getenv("PE3D_NO_SPLIT_RING") && pe3d::sring_segment(NT)) {
+        sr_span = sring_spans(g, fd, pe3d::sring_halo_max_span());
         p.sr_span = sr_span.data();
     }
 
@@ -573,11 +542,8 @@ static int march_device_impl(void* handle, const pe3d_grid* g, const pe3d_coeffs
     };
     auto enqueue_ring_setup = [&](pe3d::LaunchCtx& cs) -> cudaError_t {
         if (!ring_tables) return cudaSuccess;
-        cudaError_t e = prof.run(2, [&] { return pe3d::launch_ring_setup(cs, h->ring_tab.as<cplx>(), g->n_steps,
-                                                                        g->first_index, g->r_start, g->delta_r); });
-        if (e == cudaSuccess && p.sr_coef)
-            e = prof.run(2, [&] { return pe3d::launch_sring_setup(cs, p.sr_coef, h->ring_tab.as<cplx>(), g->n_steps); });
-        return e;
+        return prof.run(2, [&] { return pe3d::launch_ring_setup(cs, h->ring_tab.as<cplx>(), g->n_steps,
+                                                                g->first_index, g->r_start, g->delta_r); });
     };
     auto enqueue_setup = [&](pe3d::LaunchCtx& cs) -> cudaError_t {
         cudaError_t e = enqueue_depth_setup(cs);
@@ -640,8 +606,8 @@ static int march_device_impl(void* handle, const pe3d_grid* g, const pe3d_coeffs
         add(coeffs, sizeof(pe3d_coeffs) * F);
         add(ptrs, sizeof(ptrs));
         add(&stream, sizeof(stream));
-        const void* tabs[10] = {h->w_abs.ptr, h->fdev.ptr, h->loc_tab.ptr, h->err.ptr, h->ring_tab.ptr, p.ctx.k1_tab,
-                                p.temp_col, p.sr_coef, p.sr_tot, p.sr_cd};
+        const void* tabs[7] = {h->w_abs.ptr, h->fdev.ptr, h->loc_tab.ptr, h->err.ptr, h->ring_tab.ptr, p.ctx.k1_tab,
+                               p.temp_col};
         add(tabs, sizeof(tabs));
         if (!sr_span.empty()) add(sr_span.data(), sr_span.size() * sizeof(int));
         const int chains = step_chains(p.ctx, false);
@@ -655,7 +621,7 @@ static int march_device_impl(void* handle, const pe3d_grid* g, const pe3d_coeffs
         for (const char* name : {"PE3D_NO_PDL", "PE3D_CLUSTER_L", "PE3D_DEPTH_NO_CLUSTER", "PE3D_RING_BLOCK",
                                  "PE3D_RING_CPASYNC", "PE3D_DEPTH_NO_SPLIT", "PE3D_FACTOR_SERIAL",
                                  "PE3D_PREPARE_STAGED", "PE3D_PARAMS_MEMCPY", "PE3D_FINAL_STORES",
-                                 "PE3D_FIRST_STEP_FIELD", "PE3D_NO_SPLIT_RING", "PE3D_SRING_FIX", "PE3D_DEPTH_SMALL_CTA_OFF"}) {
+                                 "PE3D_FIRST_STEP_FIELD", "PE3D_NO_SPLIT_RING", "PE3D_DEPTH_SMALL_CTA_OFF"}) {
             const char* v = getenv(name);
             const std::string val = v ? std::string("=") + v : std::string("-");
             add(val.data(), val.size() + 1);

@@ -83,13 +83,12 @@ struct Handle {
     // column starter: the first temp as one column per frequency (MarchPlan::temp_col)
     DevBuf col_tab;
     // split rings: per-(step, frequency) tables, segment totals, carries
-    DevBuf sr_coef, sr_tot, sr_cd;
     // every workspace buffer (release, allocation generation)
     std::vector<DevBuf*> buffers() {
         return {&field_a, &field_b, &field_c, &loc_tab, &mul_tab, &fdev, &w_abs, &err, &k1_tab, &az_cp, &az_inv,
                 &az_q, &az_ring, &fail_row, &fail_mag, &ring_tab, &h_local, &h_local2, &h_u0, &h_final, &h_tl,
                 &h_snap, &h_clamped, &sb_in, &sb_x, &sb_cp, &sb_inv, &sb_y, &sb_q, &med_prof, &med_lat, &med_local,
-                &slab_flags, &sp_tot, &sp_aq, &sp_pa, &sp_cd, &col_tab, &sr_coef, &sr_tot, &sr_cd};
+                &slab_flags, &sp_tot, &sp_aq, &sp_pa, &sp_cd, &col_tab};
     }
     // changes whenever any workspace buffer was reallocated since the last call
     uint64_t alloc_generation() {

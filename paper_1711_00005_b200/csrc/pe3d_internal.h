@@ -123,8 +123,6 @@ struct LaunchCtx {
     // sweep reads its input from one column per frequency, [F][n_tiles][8], instead of the
     // azimuth-uniform field the prologue would otherwise have to write
     const cplx* src_col;
-    // split-ring azimuth sweep (launch_azimuth_seg): segment totals [F][nseg][2][n_tiles*8]
-    cplx* sring_tot;
     int n_peers;
     int peer_tiles;
     cplx* peer_dst[MAX_PEERS];
@@ -197,19 +195,13 @@ cudaError_t launch_azimuth_scan(const LaunchCtx& c, const cplx* src, cplx* dst, 
                                 const EpilogueArgs& ea);
 cudaError_t launch_finish(const LaunchCtx& c, const cplx* src, int src_tiled, cplx* dst, double r,
                           const EpilogueArgs& ea);
-// Split rings (pe3d_ring.cu, k_sring_*): segment length (0: the ring is not split),
-// per-(step, frequency) table size, and the launches of one split step.
+// Split rings (pe3d_ring.cu, k_azimuth_tma SEG/HALO): a cluster-sized ring swept segment by
+// segment on all SMs, each segment taking its carries from `span` neighbouring points per side
+// loaded with it.  sring_segment: segment length (0: the ring is not split).
 int sring_segment(int n_theta);
-int64_t sring_table_elems(int n_theta);
-cudaError_t launch_sring_setup(const LaunchCtx& c, cplx* coef, const cplx* ring_tab, int n_steps);
-cudaError_t launch_azimuth_seg(const LaunchCtx& c, const cplx* src, cplx* dst, const cplx* table_step,
-                               const EpilogueArgs& ea);
-// Halo form (k_azimuth_tma HALO): one kernel, carries from `span` neighbouring points per side.
 int sring_halo_max_span();
 cudaError_t launch_azimuth_halo(const LaunchCtx& c, const cplx* src, cplx* dst, const cplx* table_step,
                                 const EpilogueArgs& ea, int span);
-cudaError_t launch_sring_carry(const LaunchCtx& c, const cplx* tot, const cplx* coef_step, cplx* cd);
-cudaError_t launch_sring_fix(const LaunchCtx& c, cplx* temp, const cplx* cd, const cplx* coef_step, int span);
 cudaError_t launch_depth_serial(const LaunchCtx& c, const cplx* src, cplx* dst, cplx* scratch, const cplx* local_now,
                                 const cplx* local_new, int64_t fstride, int64_t mstride, int64_t lstride, int* fail_row,
                                 double* fail_mag);

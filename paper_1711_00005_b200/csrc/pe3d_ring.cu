@@ -118,159 +118,6 @@ __global__ void k_ring_setup(cplx* __restrict__ table, const FreqDev* __restrict
     T[7] = cmul(rf.rho, s_inf);
 }
 
-// ------------------------------------------------------------ split rings
-// A ring of nseg segments of NS points solved segment by segment with zero
-// carries (k_azimuth_tma SEG: all SMs, no cluster) and chained exactly
-// afterwards.  With w = w0 + rho^(o+1) c inside segment s (c: w at the point
-// before it) and x = z + A_o c + B_o d (d: x at the point after it),
-//   A_o = rho^(o+1) S_(NS-o),  B_o = rho^(NS-o),  S_n = sum_(t<n) rho^(2t),
-// the carries follow from the segments' zero-carry totals W_s (w0 at the last
-// point) and X0_s (z at the first point): X_s = X0_s + gamma c_s with
-// gamma = rho S_NS, and the cyclic chains of the cluster kernel.  The next
-// temp b1 x + b2 (x+ + x-) of segment s then differs from the one the segment
-// wrote (zero neighbours outside it) by alpha_o c_s + beta_o d_s, plus b2 times
-// the true left neighbour at o = 0 (alpha, beta below; B_NS = 1 carries the
-// right neighbour d_s).  |rho| < 1, so alpha and beta decay away from the
-// segment edges: only the points within `span` of an edge are corrected
-// (k_sring_carry chains the carries, k_sring_fix applies them; the host picks per
-// step either this or the cluster kernel).
-//
-// Per (step, frequency) table (SRING_HDR + 2 NS entries):
-//   [0] rho, [1] 1/(1 - rho^N), [2] gamma, [3] A_0, [4] B_0, [5] b2,
-//   [6 + j] Rs^j (Rs = rho^NS, j < 16), then alpha[NS], beta[NS].
-constexpr int SRING_HDR = 22;
-__host__ __device__ constexpr int sring_elems(int ns) { return SRING_HDR + 2 * ns; }
-
-__global__ void k_sring_setup(cplx* __restrict__ coef, const cplx* __restrict__ ring_tab, int E, int n_items,
-                              int ns) {
-    const int gid = blockIdx.x * blockDim.x + threadIdx.x;     // (step, frequency)
-    if (gid >= n_items) return;
-    const cplx* T = ring_tab + int64_t(gid) * E;
-    cplx* C = coef + int64_t(gid) * sring_elems(ns);
-    const cplx rho = T[0], b1 = T[4], b2 = T[5];
-    cplx* al = C + SRING_HDR;
-    cplx* be = al + ns;
-    const cplx r2 = cmul(rho, rho);
-    // pass 1, o = ns-1 .. 0 (n = ns - o = 1 .. ns): S_n into al[o], B_o = rho^n into be[o]
-    cplx S = czero(), r2p = cone(), bp = cone();
-    for (int o = ns - 1; o >= 0; --o) {
-        S = cadd(S, r2p);
-        r2p = cmul(r2p, r2);
-        bp = cmul(bp, rho);
-        al[o] = S;
-        be[o] = bp;
-    }
-    const cplx S_ns = S, Rs = be[0];                           // S_NS, rho^NS
-    // pass 2: A_o = rho^(o+1) S_(ns-o)
-    cplx ap = rho;
-    for (int o = 0; o < ns; ++o) {
-        al[o] = cmul(ap, al[o]);
-        ap = cmul(ap, rho);
-    }
-    C[0] = rho;
-    C[1] = T[2];
-    C[2] = cmul(rho, S_ns);
-    C[3] = al[0];
-    C[4] = be[0];
-    C[5] = b2;
-    cplx rj = cone();
-    for (int j = 0; j < 16; ++j) { C[6 + j] = rj; rj = cmul(rj, Rs); }
-    // pass 3: alpha_o = b1 A_o + b2 (A_(o+1) + A_(o-1)), beta likewise with B_ns = 1
-    cplx a_prev = czero(), b_prev = czero();
-    for (int o = 0; o < ns; ++o) {
-        const cplx a = al[o], b = be[o];
-        const cplx a_next = o + 1 < ns ? al[o + 1] : czero();
-        const cplx b_next = o + 1 < ns ? be[o + 1] : cone();
-        al[o] = cfma(b1, a, cmul(b2, cadd(a_next, a_prev)));
-        be[o] = cfma(b1, b, cmul(b2, cadd(b_next, b_prev)));
-        a_prev = a;
-        b_prev = b;
-    }
-}
-
-// Exact carries of every segment from the zero-carry totals (tot
-// [F][nseg][2][n_rows]: W, X0), written as cd [F][nseg][3][n_rows]: c_s, d_s,
-// b2 * (true x at the point before s).  A half-warp per (frequency, row), lane j
-// holding segment j; the segment chains are 4-level scans:
-//   c_j = sum_(j'<j) Rs^(j-1-j') W_j' + Rs^j wend,  X_j = X0_j + gamma c_j,
-//   d_j = sum_(j'>j) Rs^(j'-j-1) X_j' + Rs^(nseg-1-j) xstart
-// (wend, xstart: the cyclic closures).  (Measured and not kept: the chains
-// recomputed inside the fix kernel, per (tile, segment) CTA 24.5 us or per tile
-// CTA 26.8 us, against 8.4 + 16.5 us for the two kernels, and 3 us slower per step.)
-__global__ void __launch_bounds__(128) k_sring_carry(const cplx* __restrict__ tot, const cplx* __restrict__ coef_step,
-                                                     cplx* __restrict__ cd, int n_freq, int nseg, int n_rows, int ns) {
-    const int lane = threadIdx.x & 31, j = lane & 15;
-    const int64_t pair = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 4;   // (frequency, row)
-    const bool live = pair < int64_t(n_freq) * n_rows;
-    const int f = live ? int(pair / n_rows) : 0, l = live ? int(pair - int64_t(f) * n_rows) : 0;
-    const cplx* C = coef_step + int64_t(f) * sring_elems(ns);
-    const cplx rho = C[0], inv_wrap = C[1], gamma = C[2], B0 = C[4], b2 = C[5];
-    const bool seg = live && j < nseg;
-    griddep_wait();                                            // the totals come from the segmented sweep
-    griddep_launch();
-    const cplx* T = tot + (int64_t(f) * nseg + j) * 2 * n_rows + l;
-    const cplx W = seg ? ldc(T) : czero();
-    const cplx X0 = seg ? ldc(T + n_rows) : czero();
-    cplx I = W;                                                // sum_(j'<=j) Rs^(j-j') W_j'
-#pragma unroll
-    for (int d = 1; d < 16; d <<= 1) {
-        const cplx t = shfl_up(I, d);
-        if (j >= d) I = cfma(C[6 + d], t, I);
-    }
-    const cplx wend = cmul(shfl_idx(I, (lane & 16) + nseg - 1), inv_wrap);
-    cplx ip = shfl_up(I, 1);
-    if (j == 0) ip = czero();
-    const cplx c = seg ? cfma(C[6 + (j < 16 ? j : 0)], wend, ip) : czero();
-    const cplx X = cfma(gamma, c, X0);
-    cplx J = X;                                                // sum_(j'>=j) Rs^(j'-j) X_j'
-#pragma unroll
-    for (int d = 1; d < 16; d <<= 1) {
-        const cplx t = shfl_down(J, d);
-        if (j + d < nseg) J = cfma(C[6 + d], t, J);
-    }
-    const cplx xstart = cmul(shfl_idx(J, lane & 16), inv_wrap);
-    cplx jn = shfl_down(J, 1);
-    if (j + 1 >= nseg) jn = czero();
-    const int up = nseg - 1 - j;
-    const cplx dv = seg ? cfma(C[6 + (up >= 0 && up < 16 ? up : 0)], xstart, jn) : czero();
-    if (seg) {
-        cplx* out = cd + (int64_t(f) * nseg + j) * 3 * n_rows + l;
-        stc(out, c);
-        stc(out + n_rows, dv);
-        stc(out + 2 * n_rows, cmul(b2, cfma(rho, cfma(B0, dv, X), c)));      // b2 (c + rho x_first)
-    }
-}
-
-// temp += alpha_o c_s + beta_o d_s (+ b2 x_before at o = 0) at the points within
-// `span` of a segment edge.  One CTA per (frequency, tile, segment): the rows'
-// carries in shared memory, then the 2 span lines of 8 rows, read-modify-write.
-__global__ void __launch_bounds__(128) k_sring_fix(cplx* __restrict__ temp, const cplx* __restrict__ cd,
-                                                   const cplx* __restrict__ coef_step, int n_tiles, int n_theta,
-                                                   int nseg, int ns, int span) {
-    __shared__ cplx sc[3][8];
-    const int b = blockIdx.x;
-    const int s = b % nseg, ft = b / nseg;
-    const int tile = ft % n_tiles, f = ft / n_tiles;
-    const int n_rows = n_tiles * 8;
-    griddep_wait();                                            // carries and temp of the previous kernels
-    griddep_launch();
-    if (threadIdx.x < 24) {
-        const int k = threadIdx.x >> 3, r = threadIdx.x & 7;
-        sc[k][r] = ldc(cd + ((int64_t(f) * nseg + s) * 3 + k) * n_rows + tile * 8 + r);
-    }
-    __syncthreads();
-    const cplx* A = coef_step + int64_t(f) * sring_elems(ns) + SRING_HDR;
-    cplx* base = temp + ((int64_t(f) * n_tiles + tile) * n_theta + int64_t(s) * ns) * 8;
-    for (int e = threadIdx.x; e < 16 * span; e += blockDim.x) {
-        const int jj = e >> 3, r = e & 7;
-        const int o = jj < span ? jj : ns - 2 * span + jj;     // [0, span) then [ns - span, ns)
-        cplx dt = cfma(ldc(A + o), sc[0][r], cmul(ldc(A + ns + o), sc[1][r]));
-        if (o == 0) dt = cadd(dt, sc[2][r]);
-        cplx* p = base + o * 8 + r;
-        *p = cadd(*p, dt);
-    }
-}
-
 // Given u on this thread's azimuth chunk of RT depth rows, write the TL
 // sample / snapshot / final slab if requested and the next step's
 // temp = u + cy_rhs * s_theta * d2_theta(u)  (ref operators.py:105-122,
@@ -1193,10 +1040,10 @@ k_azimuth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant_
               const cplx* __restrict__ table, int E, int tab_elems, int n_theta, int n_tiles, int n_depth,
               int64_t total_items, int n_units, EpilogueArgs ea, const cplx* __restrict__ sp_cd,
               const cplx* __restrict__ sp_aq, const cplx* __restrict__ sp_pa, int split, int tile_perm,
-              const __grid_constant__ CUtensorMap tm_fin, int fin_tma, cplx* __restrict__ seg_tot,
+              const __grid_constant__ CUtensorMap tm_fin, int fin_tma,
               const __grid_constant__ CUtensorMap tm_halo, int halo_g) {
     static_assert(!SEG || (!CLUSTER && RT == 1), "segmented rings: plain kernel, one row per warp");
-    static_assert(!HALO || SEG, "halo carries: segmented rings only");
+    static_assert(HALO == SEG, "segmented rings take their carries from the halo");
     constexpr int HALO_SLOT = HALO ? 2 * RING_HALO_G * 256 : 0;   // cplx per slot: [side][granule][32 lines x 8 rows]
     namespace cg = cooperative_groups;
     constexpr int NW = 8 / RT;                      // consumer warps; warp NW is the TMA producer
@@ -1449,17 +1296,6 @@ k_azimuth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant_
                     for (int h = 0; h < RT; ++h) carry_w[h] = shfl_idx(cw, 16 * h);
                 } else if constexpr (HALO) {
                     carry_w[0] = halo_w;                    // w at the point before the segment
-                } else if constexpr (SEG) {
-                    // a segment of a longer ring with zero carries: its total W leaves for
-                    // k_sring_carry, which chains the segments exactly
-#pragma unroll
-                    for (int h = 0; h < RT; ++h) carry_w[h] = czero();
-                    const cplx W = shfl_idx(Y[0], 31);
-                    if (lane == 0) {
-                        const int l = tile * 8 + warp;
-                        const bool live = l + ea.row_offset != 0 && l < n_depth;
-                        stc(seg_tot + ((int64_t(f) * nseg + seg) * 2) * (n_tiles * 8) + l, live ? W : czero());
-                    }
                 } else {
 #pragma unroll
                     for (int h = 0; h < RT; ++h) carry_w[h] = cmul(shfl_idx(Y[h], 31), inv_wrap);   // cyclic closure
@@ -1510,15 +1346,6 @@ k_azimuth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant_
                     // x at the point after the segment: the halo's own forward sums closed by
                     // 1/(1 - rho^2), plus the segment's last w (carry applied above) carried through
                     carry_x[0] = cfma(T[7], shfl_idx(v[0][L - 1], 31), cmul(T[6], halo_x));
-                } else if constexpr (SEG) {
-#pragma unroll
-                    for (int h = 0; h < RT; ++h) carry_x[h] = czero();
-                    const cplx X0 = shfl_idx(X[0], 0);     // zero-carry solution at the segment's first point
-                    if (lane == 0) {
-                        const int l = tile * 8 + warp;
-                        const bool live = l + ea.row_offset != 0 && l < n_depth;
-                        stc(seg_tot + ((int64_t(f) * nseg + seg) * 2 + 1) * (n_tiles * 8) + l, live ? X0 : czero());
-                    }
                 } else {
 #pragma unroll
                     for (int h = 0; h < RT; ++h) carry_x[h] = cmul(shfl_idx(X[h], 0), inv_wrap);    // cyclic closure
@@ -1591,10 +1418,6 @@ k_azimuth_tma(const __grid_constant__ CUtensorMap tm_src, const __grid_constant_
                     if constexpr (CLUSTER || HALO) {
                         if (lane == 0) prev = prev_edge[h];
                         if (lane == 31) next = next_edge[h];
-                    } else if constexpr (SEG) {
-                        // neighbours outside the segment enter later (k_sring_fix)
-                        if (lane == 0) prev = czero();
-                        if (lane == 31) next = czero();
                     } else {
                         const cplx wrap_prev = shfl_idx(v[h][L - 1], 31), wrap_next = shfl_idx(v[h][0], 0);
                         if (lane == 0) prev = wrap_prev;
@@ -1951,7 +1774,6 @@ static cudaError_t launch_tma_ring(const LaunchCtx& c, const cplx* src, cplx* ds
     const int CL = c.n_theta / NS;
     if (c.n_theta % NS != 0 || (CLUSTER ? (CL < 2 || CL > 16) : (SEG ? (CL < 2 || CL > 16) : CL != 1)))
         return cudaErrorNotSupported;
-    if (SEG && !HALO && (!c.sring_tot || ea.tl || ea.snap || ea.final_out)) return cudaErrorNotSupported;
     const int halo_g = HALO ? (span + 31) / 32 : 0;
     if (HALO && (ea.final_out || halo_g < 1 || halo_g > RING_HALO_G)) return cudaErrorNotSupported;
     const int64_t tiles = int64_t(c.n_freq) * c.n_tiles;
@@ -2008,8 +1830,7 @@ static cudaError_t launch_tma_ring(const LaunchCtx& c, const cplx* src, cplx* ds
         }
         return launch_pdl(c.pdl != 0, kern, dim3(grid), dim3(nthr), bytes, c.stream, tm_src, tm_dst, table_step, E,
                           tab_elems, c.n_theta, c.n_tiles, c.n_depth, items, grid, ea, (const cplx*)c.sp_cd,
-                          (const cplx*)c.sp_aq, (const cplx*)c.sp_pa, c.split, 1, tm_fin, fin_tma, c.sring_tot,
-                          tm_halo, halo_g);
+                          (const cplx*)c.sp_aq, (const cplx*)c.sp_pa, c.split, 1, tm_fin, fin_tma, tm_halo, halo_g);
     } else {
         if (CL > 8) {
             e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -2043,7 +1864,7 @@ static cudaError_t launch_tma_ring(const LaunchCtx& c, const cplx* src, cplx* ds
         }
         return cudaLaunchKernelEx(&cfg, kern, tm_src, tm_dst, table_step, E, tab_elems, c.n_theta, c.n_tiles,
                                   c.n_depth, items, per, ea, (const cplx*)c.sp_cd, (const cplx*)c.sp_aq,
-                                  (const cplx*)c.sp_pa, c.split, perm, tm_dst, 0, (cplx*)nullptr, tm_dst, 0);
+                                  (const cplx*)c.sp_pa, c.split, perm, tm_dst, 0, tm_dst, 0);
     }
 }
 
@@ -2114,19 +1935,6 @@ static cudaError_t launch_cluster_ring(const LaunchCtx& c, const cplx* src, cplx
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kern, src, dst, table_step, E, c.fdev, c.n_theta, c.n_tiles, c.n_depth, items, per,
                               r_new, c.delta_theta, ea);
-}
-
-// Split-ring azimuth sweep of a cluster-sized ring (see k_sring_setup): every
-// segment solved with zero carries; c.sring_tot receives the segment totals.
-cudaError_t launch_azimuth_seg(const LaunchCtx& c, const cplx* src, cplx* dst, const cplx* table_step,
-                               const EpilogueArgs& ea) {
-    const RingPlan plan = ring_plan(c.n_theta);
-    if (plan.kind != 2 || plan.L != 16 || !ea.periodic || ea.chunk_gap != 0 || ea.peer[0] || ea.row_offset != 0 ||
-        (ea.chunk_cols != 0 && ea.chunk_cols != c.n_theta))
-        return cudaErrorNotSupported;
-    const int E = plan.lay.E;
-    if (c.split >= 2) return launch_tma_ring<16, 1, 2, false, 1, true, true>(c, src, dst, table_step, E, ea);
-    return launch_tma_ring<16, 1, 2, false, 1, false, true>(c, src, dst, table_step, E, ea);
 }
 
 // Halo form of the split-ring sweep: the carries come from `span` (<= 32 RING_HALO_G)
@@ -2254,33 +2062,6 @@ cudaError_t launch_azimuth_scan(const LaunchCtx& c, const cplx* src, cplx* dst, 
 int sring_segment(int n_theta) {
     const RingPlan p = ring_plan(n_theta);
     return (p.kind == 2 && p.L == 16) ? 32 * p.L : 0;
-}
-
-int64_t sring_table_elems(int n_theta) { return sring_elems(sring_segment(n_theta)); }
-
-cudaError_t launch_sring_setup(const LaunchCtx& c, cplx* coef, const cplx* ring_tab, int n_steps) {
-    const int ns = sring_segment(c.n_theta);
-    if (!ns) return cudaErrorNotSupported;
-    const int n_items = n_steps * c.n_freq;
-    if (n_items == 0) return cudaSuccess;
-    k_sring_setup<<<(n_items + 63) / 64, 64, 0, c.stream>>>(coef, ring_tab, ring_plan(c.n_theta).lay.E, n_items, ns);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_sring_carry(const LaunchCtx& c, const cplx* tot, const cplx* coef_step, cplx* cd) {
-    const int ns = sring_segment(c.n_theta), nseg = c.n_theta / ns, n_rows = c.n_tiles * 8;
-    if (nseg > 16) return cudaErrorNotSupported;
-    const int64_t threads = int64_t(c.n_freq) * n_rows * 16;   // a half-warp per (frequency, row)
-    return launch_pdl(c.pdl != 0, k_sring_carry, dim3(unsigned((threads + 127) / 128)), dim3(128), 0, c.stream, tot,
-                      coef_step, cd, c.n_freq, nseg, n_rows, ns);
-}
-
-cudaError_t launch_sring_fix(const LaunchCtx& c, cplx* temp, const cplx* cd, const cplx* coef_step, int span) {
-    const int ns = sring_segment(c.n_theta), nseg = c.n_theta / ns;
-    const int64_t blocks = int64_t(c.n_freq) * c.n_tiles * nseg;
-    if (blocks > 0x7fffffff) return cudaErrorNotSupported;
-    return launch_pdl(c.pdl != 0, k_sring_fix, dim3(unsigned(blocks)), dim3(128), 0, c.stream, temp, cd, coef_step,
-                      c.n_tiles, c.n_theta, nseg, ns, span);
 }
 
 cudaError_t launch_finish(const LaunchCtx& c, const cplx* src, int src_tiled, cplx* dst, double r,

@@ -422,18 +422,15 @@ def test_march_graph_variants_bitwise_equal(monkeypatch, n_steps, stride):
             assert got == ref, switch
 
 
-@pytest.mark.parametrize("mode", ["halo", "fix"])
 @pytest.mark.parametrize("n_theta,n_depth,r_start", [(1024, 1024, 400.0), (2048, 2048, 400.0), (4096, 1024, 400.0),
                                                      (4096, 2048, 190.0), (1024, 512, 700.0)])
-def test_split_rings_match_cluster_sweep(monkeypatch, n_theta, n_depth, r_start, mode):
-    """Split-ring steps (every 512-point ring segment solved on all SMs) against the
-    cluster kernel on every step: the cfg5 medium where the carries only reach the
-    segment edges (spans of 86-20 points: three, two and one halo granules), 2 to 8
-    segments, with and without split depth columns, TL every 4 steps.
-    halo: the carries come from the neighbouring segments' points loaded with each
-    segment, TL steps included (the shipped path).  fix (PE3D_SRING_FIX): zero-carry
-    segments, the exact carries chained afterwards and applied within the span of
-    each segment edge; TL steps run the cluster kernel."""
+def test_split_rings_match_cluster_sweep(monkeypatch, n_theta, n_depth, r_start):
+    """Split-ring steps (every 512-point ring segment solved on all SMs, its carries
+    taken from the neighbouring segments' points loaded with it, TL steps included)
+    against the cluster kernel on every step: the cfg5 medium where the carries only
+    reach the segment edges (spans of 86-20 points: three, two and one halo
+    granules), 2 to 8 segments, with and without split depth columns, TL every 4
+    steps."""
     import dataclasses
     cfg = configs.build("cfg5", n_range=12, output_stride=4)
     grid, env, source, options = cfg
@@ -444,8 +441,6 @@ def test_split_rings_match_cluster_sweep(monkeypatch, n_theta, n_depth, r_start,
     monkeypatch.setenv("PE3D_NO_SPLIT_RING", "1")
     ref = march_frequencies(cfg, [f])[0]
     monkeypatch.delenv("PE3D_NO_SPLIT_RING")
-    if mode == "fix":
-        monkeypatch.setenv("PE3D_SRING_FIX", "1")
     got = march_frequencies(cfg, [f])[0]
     assert rel_l2(got.final_slab.values, ref.final_slab.values) <= 1e-12
     assert tl_err(got.tl_field, ref.tl_field) <= 1e-9

@@ -1,6 +1,6 @@
 # Round evidence on one B200: the driver's bench line (plain run first), the ncu launch list of the
 # bench command, and one ncu --set full capture of each sweep kernel at cfg4 (the headline) and cfg5
-# (split long columns) and cfg5's split-ring azimuth kernels at 500 m.  Every ncu command follows the same
+# (split long columns) and cfg5's halo-form split-ring azimuth sweep at 500 m.  Every ncu command follows the same
 # command run without ncu (&&).
 set -u
 mkdir -p gpurun_out
@@ -19,5 +19,5 @@ timeout 900 ncu --set full --clock-control none --import-source on \
 P5S="python tools/profile_march.py cfg5 4 500"
 timeout 900 $P5S > gpurun_out/plain_p5s.log 2>&1 && \
 timeout 900 ncu --set full --clock-control none --import-source on \
-    -k regex:'k_azimuth_tma|k_sring' -s 1 -c 4 -f -o gpurun_out/ncu_cfg5_split_ring $P5S > gpurun_out/ncu_cfg5s.log 2>&1
+    -k regex:'k_azimuth_tma' -s 1 -c 4 -f -o gpurun_out/ncu_cfg5_split_ring $P5S > gpurun_out/ncu_cfg5s.log 2>&1
 ls gpurun_out
