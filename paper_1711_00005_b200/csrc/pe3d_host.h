@@ -119,6 +119,7 @@ struct Handle {
     // whole-march graph (pe3d_march_device): parameter staging, and the side
     // branch that builds the factorisation and ring tables during the prologue
     PinBuf params_pin;
+    PinBuf err_pin;             // the march's error record lands here (page-locked: the readback is asynchronous)
     cudaStream_t pro_side = nullptr;
     cudaEvent_t pro_fork = nullptr, pro_join = nullptr;
     // cached march graphs of pe3d_march_device, most recently used last (a grouped
@@ -133,6 +134,9 @@ struct Handle {
     // pe3d_march_host: copy stream for the per-group results and its event
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t copy_ev = nullptr;
+    // a device-to-host copy the next march enqueues on copy_stream right behind its last kernel,
+    // before the host waits for the march (pe3d_march_host: a group's final slab)
+    struct PostCopy { void* dst = nullptr; const void* src = nullptr; size_t bytes = 0; } post_copy;
 };
 
 // Launch wrapper: in profile mode, bracket each launch with events.
@@ -318,9 +322,22 @@ inline HostFail azimuth_failures(const pe3d_grid* g, const pe3d_coeffs* c) {
 }
 
 inline int decode_error(Handle* h, cudaStream_t stream, pe3d_error* err, const HostFail* hf = nullptr) {
-    pe3d::DevError de;
-    CK(cudaMemcpyAsync(&de, h->err.ptr, sizeof(de), cudaMemcpyDeviceToHost, stream), "error readback");
+    CK(h->err_pin.ensure(sizeof(pe3d::DevError)), "alloc pinned error record");
+    CK(cudaMemcpyAsync(h->err_pin.ptr, h->err.ptr, sizeof(pe3d::DevError), cudaMemcpyDeviceToHost, stream),
+       "error readback");
+    if (h->post_copy.bytes) {
+        // the caller's copy of this march's result (pe3d_march_host: a group's final slab) leaves
+        // right behind the last kernel -- queued after the error record, which the host waits for,
+        // and before the host has seen the march complete (~0.2 ms later)
+        const Handle::PostCopy pc = h->post_copy;
+        h->post_copy = Handle::PostCopy{};
+        CK(cudaEventRecord(h->copy_ev, stream), "event");
+        CK(cudaStreamWaitEvent(h->copy_stream, h->copy_ev, 0), "event");
+        CK(cudaMemcpyAsync(pc.dst, pc.src, pc.bytes, cudaMemcpyDeviceToHost, h->copy_stream), "D2H");
+    }
     CK(cudaStreamSynchronize(stream), "march");
+    pe3d::DevError de;
+    std::memcpy(&de, h->err_pin.ptr, sizeof(de));
     if (hf && hf->key < de.key) {
         de.key = hf->key;
         de.pivot = hf->pivot;

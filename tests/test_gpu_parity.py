@@ -447,13 +447,14 @@ def test_split_rings_match_cluster_sweep(monkeypatch, n_theta, n_depth, r_start)
     assert got.clamped_samples == ref.clamped_samples
 
 
-@pytest.mark.parametrize("groups", ["2", "3", "4"])
-def test_grouped_host_march_bitwise_equal(monkeypatch, groups):
+@pytest.mark.parametrize("groups,n_freq", [("2", 7), ("3", 7), ("4", 7), ("3", 12)])
+def test_grouped_host_march_bitwise_equal(monkeypatch, groups, n_freq):
     """pe3d_march_host marching its frequencies in groups (each group's final slab
     copied out while the next marches; PE3D_HOST_GROUPS) against one march of all
     of them: bitwise equal TL, final slabs and clamped counts, with uneven groups
-    (7 frequencies) and TL streamed to page-locked memory."""
-    freqs = (50.0, 80.0, 130.0, 170.0, 260.0, 340.0, 500.0)
+    (7 and 12 frequencies) and TL streamed to page-locked memory; each group's final
+    slab is queued behind its last kernel, before the host waits for the march."""
+    freqs = (50.0, 80.0, 130.0, 170.0, 260.0, 340.0, 500.0, 65.0, 95.0, 210.0, 300.0, 420.0)[:n_freq]
     cfg = configs.build("cfg4", n_range=6, frequencies=freqs, output_stride=2)
 
     def run():
