@@ -127,12 +127,22 @@ def _local_columns(env, grid: Grid3D, r: float, k0s) -> np.ndarray:
     from .medium import LayeredMedium
     medium = getattr(env, "medium", None)
     if isinstance(medium, LayeredMedium) and medium.range_independent and len(k0s) > 1:
+        # the last batch's columns are kept with the medium, next to its k0-independent
+        # parts (a farm called again on the same frequencies: 1 ms of complex square roots
+        # of a 20-step cfg4 march's 8 ms); read-only, the march only uploads them
+        key = (grid.n_depth, grid.delta_z, tuple(k0s))
+        kept = medium.__dict__.get("_local_columns_cache")
+        if kept is not None and kept[0] == key:
+            return kept[1]
         n2, dens = medium._column_parts(grid)
         n2 = np.broadcast_to(n2[0], (len(k0s), grid.n_depth))
         if dens is not None:
             k0 = np.asarray(k0s, dtype=np.float64)[:, None]
             n2 = n2 + dens[0][None, :] / (k0 * k0)
-        return np.ascontiguousarray(np.sqrt(n2) ** 2 - 1.0)
+        cols = np.ascontiguousarray(np.sqrt(n2) ** 2 - 1.0)
+        cols.setflags(write=False)
+        medium.__dict__["_local_columns_cache"] = (key, cols)
+        return cols
     return np.ascontiguousarray(np.stack([_local_column(env, grid, r, k0) for k0 in k0s]))
 
 
