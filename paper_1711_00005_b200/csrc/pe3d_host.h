@@ -129,7 +129,7 @@ struct Handle {
         cudaGraphExec_t pre = nullptr, steps = nullptr;
         int64_t launches = 0;
     };
-    static constexpr int MAX_MARCH_GRAPHS = 8;
+    static constexpr int MAX_MARCH_GRAPHS = 16;    // LRU; a grouped host march uses one entry per frequency group
     std::vector<MarchGraph> march_graphs;
     // pe3d_march_host: copy stream for the per-group results and its event
     cudaStream_t copy_stream = nullptr;
