@@ -276,8 +276,8 @@ PE3D_API int pe3d_last_copy_bytes(void* handle, int64_t* h2d, int64_t* d2h);
 
 /*
  * pe3d_profile_launches -- the individual CUDA-event times (ms, launch order)
- * of kernel class `cls` (0 depth sweep, 1 azimuth sweep, 2 other, 3 the carry
- * and edge fix of a split-ring azimuth sweep) in the last PE3D_FLAG_PROFILE
+ * of kernel class `cls` (0 depth sweep, 1 azimuth sweep, 2 other, 3 unused
+ * since the split rings became one kernel) in the last PE3D_FLAG_PROFILE
  * march on this handle; writes min(count, capacity) entries and the full count
  * to *count (measurement only: steady-state launches for the bench's roofline).
  */

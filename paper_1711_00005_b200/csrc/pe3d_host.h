@@ -82,7 +82,6 @@ struct Handle {
     DevBuf sp_tot, sp_aq, sp_pa, sp_cd;
     // column starter: the first temp as one column per frequency (MarchPlan::temp_col)
     DevBuf col_tab;
-    // split rings: per-(step, frequency) tables, segment totals, carries
     // every workspace buffer (release, allocation generation)
     std::vector<DevBuf*> buffers() {
         return {&field_a, &field_b, &field_c, &loc_tab, &mul_tab, &fdev, &w_abs, &err, &k1_tab, &az_cp, &az_inv,
@@ -100,8 +99,8 @@ struct Handle {
     std::vector<unsigned char> graph_key;
     cudaGraphExec_t graph_exec = nullptr;
     // PE3D_FLAG_PROFILE accounting
-    // classes: 0 depth sweep, 1 azimuth sweep, 2 other, 3 the split-ring carry and
-    // edge fix (part of the azimuth sweep of a split-ring step)
+    // classes: 0 depth sweep, 1 azimuth sweep, 2 other (3: unused since the split rings
+    // became one kernel)
     double prof_ms[4] = {0, 0, 0, 0};
     int32_t prof_n[4] = {0, 0, 0, 0};
     std::vector<double> prof_list[4];     // per launch, in launch order
