@@ -843,7 +843,7 @@ int pe3d_march_host(void* handle, const pe3d_grid* g, const pe3d_coeffs* coeffs,
     // frequencies are marched in groups, one after another, and each group's final
     // slab leaves on a copy stream while the next group marches.
     const int G = host_groups(g, u_final != nullptr, snapshots != nullptr);
-    if (G > 1) {
+    if (u_final) {                                          // every march's final slab leaves on the copy stream
         if (!h->copy_stream) CK(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking), "stream");
         if (!h->copy_ev) CK(cudaEventCreateWithFlags(&h->copy_ev, cudaEventDisableTiming), "event");
     }
@@ -872,7 +872,7 @@ int pe3d_march_host(void* handle, const pe3d_grid* g, const pe3d_coeffs* coeffs,
         TlSink sk = sink;
         if (sk.host) sk.host = tl + int64_t(f0) * S * slab;
         pe3d_error e_g{};
-        if (G > 1 && u_final)                               // this group's slab leaves while the next marches
+        if (u_final)                                        // this group's slab leaves while the next marches
             h->post_copy = Handle::PostCopy{u_final + f0 * slab, h->h_final.as<cplx>() + f0 * slab,
                                             size_t(f1 - f0) * slab * sizeof(cplx)};
         const int st_g =
@@ -886,7 +886,7 @@ int pe3d_march_host(void* handle, const pe3d_grid* g, const pe3d_coeffs* coeffs,
         if (st_g != PE3D_OK) {
             // the batch reports the lowest (step, sweep, frequency, member), as one march would
             if (st_g != PE3D_SINGULAR) {
-                if (G > 1) cudaStreamSynchronize(h->copy_stream);      // no copy in flight into the caller's buffers
+                if (u_final) cudaStreamSynchronize(h->copy_stream);    // no copy in flight into the caller's buffers
                 return cuda_or(err, st_g, e_g);
             }
             e_g.frequency += f0;
@@ -898,14 +898,12 @@ int pe3d_march_host(void* handle, const pe3d_grid* g, const pe3d_coeffs* coeffs,
         }
         if (sink.col0) rep.start(tl, f0, f1, S, g->n_theta, g->n_depth);   // the march synchronised: row 0 is there
     }
-    if (G > 1) CK(cudaStreamSynchronize(h->copy_stream), "sync");
+    if (u_final) CK(cudaStreamSynchronize(h->copy_stream), "sync");
     rep.join();
     if (best_st != PE3D_OK) {
         if (err) *err = best;
         return best_st;
     }
-    if (u_final && G == 1)
-        CK(cudaMemcpyAsync(u_final, h->h_final.ptr, F * slab * sizeof(cplx), cudaMemcpyDeviceToHost, s), "D2H");
     if (tl && !sink.host)
         CK(cudaMemcpyAsync(tl, h->h_tl.ptr, F * S * slab * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
     if (snapshots)
